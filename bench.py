@@ -1,0 +1,356 @@
+#!/usr/bin/env python3
+"""Benchmark: GTEPS of the B200 superstep engine vs the reference CPU path.
+
+Workload at N=1: BASELINE.json configs[1] -- Hashmin connected components
+on the symmetrised R-MAT scale-22 / edge-factor-8 graph (seed 2), run to
+quiescence (C2).  ``--config`` picks another BASELINE config (C1..C5).
+
+A "step" is one complete run of the program (every superstep to
+quiescence) over the graph.  ``value`` = sum of edges traversed by the
+senders over all supersteps / device time of the run kernel (GTEPS), with
+the CSR already resident in HBM; ``e2e`` = the same metric through the
+public ``run()`` with the CSR in pinned host memory: upload, device CSR
+preparation, the run and the result read-back are inside the timed region.
+L2 is flushed (a 512 MiB write) between timed steps.
+
+``--impl reference`` times the reference algorithm's CPU implementation:
+the oracle port of pregelite's superstep engine (oracle/pregel_oracle.c,
+OpenMP on all host cores), on the same config/metric.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "GTEPS per app (PR/CC/SSSP) + % of HBM roofline at 1/2/4/8 B200 vs host CPU"
+APP_OF = {"C1": "pagerank", "C2": "components", "C3": "sssp", "C4": "pagerank",
+          "C5": "components"}
+HBM_NORTH_STAR_GBS = 8000.0
+
+
+def measured_peaks():
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(path) as fh:
+            d = json.load(fh)
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    except Exception:
+        return 6650.0, "fallback (B200_PROFILING.md: 6.65 TB/s)"
+
+
+# ----------------------------------------------------------------------
+# algorithmic bytes (BASELINE.md section 2 / SURVEY.md 8(d))
+# ----------------------------------------------------------------------
+
+def algorithmic_bytes(app: str, n: int, m: int, steps) -> int:
+    if app == "pagerank":
+        return len(steps) * (12 * m + 48 * n)
+    total = 0
+    for s, st in enumerate(steps):
+        f_next = steps[s + 1].broadcasters if s + 1 < len(steps) else 0
+        total += 16 * st.broadcasters + 8 * st.edges + 12 * st.recipients \
+            + 8 * f_next + n // 4
+    return total
+
+
+class StepView:
+    def __init__(self, broadcasters, edges, recipients):
+        self.broadcasters, self.edges, self.recipients = broadcasters, edges, recipients
+
+
+def step_views(app, rep):
+    out = []
+    for s in rep.supersteps:
+        bc = s.messages_sent if app == "components" else s.broadcasters
+        out.append(StepView(bc, s.edges, s.recipients))
+    return out
+
+
+# ----------------------------------------------------------------------
+# clocks during the timed region
+# ----------------------------------------------------------------------
+
+class ClockSampler:
+    REASONS = {0x1: "gpu_idle", 0x2: "applications_clocks_setting",
+               0x4: "sw_power_cap", 0x8: "hw_slowdown", 0x10: "sync_boost",
+               0x20: "sw_thermal_slowdown", 0x40: "hw_thermal_slowdown",
+               0x80: "hw_power_brake_slowdown", 0x100: "display_clock_setting"}
+
+    def __init__(self, index: int):
+        self.samples, self.reasons, self.max_mhz = [], set(), None
+        self._stop = threading.Event()
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self._nv = pynvml
+            self._h = pynvml.nvmlDeviceGetHandleByIndex(index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self._h, pynvml.NVML_CLOCK_SM)
+        except Exception:
+            self._nv = None
+        self._t = threading.Thread(target=self._loop, daemon=True)
+
+    def _loop(self):
+        while not self._stop.is_set():
+            try:
+                self.samples.append(self._nv.nvmlDeviceGetClockInfo(self._h, self._nv.NVML_CLOCK_SM))
+                r = self._nv.nvmlDeviceGetCurrentClocksEventReasons(self._h)
+                for bit, name in self.REASONS.items():
+                    if r & bit and name != "gpu_idle":
+                        self.reasons.add(name)
+            except Exception:
+                pass
+            time.sleep(0.02)
+
+    def __enter__(self):
+        if self._nv is not None:
+            self._t.start()
+        return self
+
+    def __exit__(self, *exc):
+        self._stop.set()
+        if self._nv is not None:
+            self._t.join()
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": ["unsampled"]}
+        return {"sm_mhz": float(statistics.median(self.samples)),
+                "sm_max_mhz": self.max_mhz, "reasons": sorted(self.reasons),
+                "samples": len(self.samples)}
+
+
+# ----------------------------------------------------------------------
+# the B200 arm
+# ----------------------------------------------------------------------
+
+def program_for(pgx, app, graph):
+    if app == "pagerank":
+        return pgx.pagerank(10, 0.85)
+    if app == "components":
+        return pgx.connected_components()
+    import torch
+    return pgx.sssp(int(torch.argmax(graph.out_degrees)))
+
+
+def cpu_baseline(cfg: str, graph, app: str, budget_s: float = 20.0):
+    """Oracle port of pregelite's engine on all host cores, bounded sample."""
+    from oracle import oracle as O
+    n = graph.vertex_count
+    off = graph.out_offsets.cpu().numpy()
+    tgt = graph.out_targets.cpu().numpy()
+    in_off, in_tgt = (None, None) if app == "sssp" else O.transpose(n, off, tgt)
+    threads = O.max_threads()
+    src = int(np.argmax(np.diff(off)))
+    edges_total, secs, runs = 0, 0.0, 0
+    while runs == 0 or (secs < budget_s * 0.5 and runs < 3):
+        t = time.perf_counter()
+        if app == "pagerank":
+            r = O.run_pagerank(n, off, tgt, 10, 0.85, in_off, in_tgt, threads=threads)
+        elif app == "components":
+            r = O.run_cc(n, off, tgt, in_off, in_tgt, threads=threads)
+        else:
+            r = O.run_sssp(n, off, tgt, src, threads=threads)
+        secs += time.perf_counter() - t
+        edges_total += sum(r.edges)
+        runs += 1
+    return {"value": edges_total / secs / 1e9, "unit": "GTEPS", "cores": threads,
+            "kind": "port",
+            "sample": f"{runs} full {cfg} {app} run(s) (all supersteps) of the oracle "
+                      f"port of pregelite's engine, {threads} OpenMP threads, "
+                      f"{secs:.2f} s"}
+
+
+def flush_l2(buf):
+    buf.add_(1)
+
+
+def bench_gpu(args):
+    import torch
+    import paper_2010_01542_b200 as pgx
+    from paper_2010_01542_b200.rmat import rmat_graph
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    cfg = args.config
+    app = APP_OF[cfg]
+    g = rmat_graph(cfg)
+    n, m = g.vertex_count, g.edge_count
+    prog = program_for(pgx, app, g)
+    flush = torch.empty(512 << 20, dtype=torch.uint8, device="cuda")
+
+    # ---- device-resident arm: one persistent kernel per step ----
+    plan = pgx.plan_run(g, prog)
+    for _ in range(args.warmup):
+        plan.launch()
+    torch.cuda.synchronize()
+    ref = pgx.collect(plan, prog)
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+          for _ in range(args.steps)]
+    kernel_ms = []
+    if dist is not None:
+        dist.barrier()
+    torch.cuda.synchronize()
+    with ClockSampler(local) as clocks:
+        for i in range(args.steps):
+            flush_l2(flush)
+            ev[i][0].record(plan.stream)
+            plan.launch()
+            ev[i][1].record(plan.stream)
+        torch.cuda.synchronize()
+    if dist is not None:
+        dist.barrier()
+    kernel_ms = [a.elapsed_time(b) for a, b in ev]
+    rep = pgx.collect(plan, prog)
+    assert np.array_equal(rep.values, ref.values) or app == "pagerank"
+    edges = sum(s.edges for s in rep.supersteps)
+    total_ms = float(sum(kernel_ms))
+    if dist is not None:
+        t = torch.tensor([total_ms], device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        total_ms = float(t.item())
+    value = edges * args.steps * world / (total_ms * 1e-3) / 1e9
+    ms_per_step = total_ms / args.steps
+    steps_view = step_views(app, rep)
+    alg_bytes = algorithmic_bytes(app, n, m, steps_view)
+    peak, peak_src = measured_peaks()
+    achieved = alg_bytes / (ms_per_step * 1e-3) / 1e9
+
+    # ---- e2e arm: public run() with the CSR in pinned host memory ----
+    host = g.pin_memory()
+    e2e_ms = []
+    h2d = (n + 1) * 8 + m * 4
+    d2h = n * (8 if app == "pagerank" else 4)
+    for i in range(args.warmup + args.e2e_steps):
+        host.drop_device_cache()
+        flush_l2(flush)
+        torch.cuda.synchronize()
+        t = time.perf_counter()
+        r = pgx.run(host, prog)
+        dt = time.perf_counter() - t
+        if i >= args.warmup:
+            e2e_ms.append(dt * 1e3)
+    e2e_total = float(sum(e2e_ms))
+    e2e_value = edges * len(e2e_ms) / (e2e_total * 1e-3) / 1e9
+
+    line = {
+        "metric": METRIC,
+        "value": round(value, 4),
+        "unit": "GTEPS",
+        "n_gpus": world,
+        "steps": args.steps,
+        "warmup": args.warmup,
+        "ms_per_step": round(ms_per_step, 5),
+        "higher_is_better": True,
+        "scaling": "weak",
+        "vs_baseline": None,
+        "dtype": "u32" if app != "pagerank" else "f64",
+        "data": "synthetic R-MAT (SURVEY 8(d) generator, BASELINE.md CSR sha256-pinned)",
+        "config": {"workload": f"{cfg}: {app} on R-MAT scale {int(np.log2(n))}, "
+                               f"n={n}, m={m}", "n": n, "m": m,
+                   "supersteps": rep.superstep_count, "edges_per_step": edges,
+                   "l2": "flushed (512 MiB write) between timed steps",
+                   "parallelism": f"replicas x{world}" if world > 1 else "1 GPU"},
+        "e2e": {"value": round(e2e_value, 4), "unit": "GTEPS",
+                "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
+                "ms_per_step": round(e2e_total / len(e2e_ms), 4)},
+        "gpu_launches": args.steps,
+        "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak,
+                     "unit": "GB/s", "frac": round(achieved / peak, 4),
+                     "traffic": None, "peak_source": peak_src,
+                     "frac_of_8TBs": round(achieved / HBM_NORTH_STAR_GBS, 4),
+                     "alg_bytes_per_step": alg_bytes,
+                     "kernel": "min_run_kernel / pagerank_run_kernel (persistent)"},
+        "clocks": clocks.summary(),
+    }
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        line["cpu_baseline"] = cpu_baseline(cfg, g, app)
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if dist is not None:
+        dist.destroy_process_group()
+
+
+def bench_reference(args):
+    """--impl reference: the oracle port of pregelite's engine on host cores."""
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    from oracle import oracle as O
+    cfg = args.config
+    app = APP_OF[cfg]
+    spec = O.CONFIGS[cfg]
+    n, off, tgt = O.rmat_csr(spec)
+    in_off, in_tgt = (None, None) if app == "sssp" else O.transpose(n, off, tgt)
+    threads = O.max_threads()
+    src = int(np.argmax(np.diff(off)))
+
+    def once():
+        if app == "pagerank":
+            return O.run_pagerank(n, off, tgt, 10, 0.85, in_off, in_tgt, threads=threads)
+        if app == "components":
+            return O.run_cc(n, off, tgt, in_off, in_tgt, threads=threads)
+        return O.run_sssp(n, off, tgt, src, threads=threads)
+
+    for _ in range(min(args.warmup, 1)):
+        once()
+    secs, edges = 0.0, 0
+    steps = min(args.steps, 3)
+    for _ in range(steps):
+        t = time.perf_counter()
+        r = once()
+        secs += time.perf_counter() - t
+        edges += sum(r.edges)
+    v = edges / secs / 1e9
+    sample = (f"{steps} full {cfg} {app} run(s) of the oracle port of pregelite's "
+              f"engine (oracle/pregel_oracle.c), {threads} OpenMP threads")
+    line = {"metric": METRIC, "value": round(v, 5), "unit": "GTEPS", "impl": "reference",
+            "n_gpus": int(os.environ.get("WORLD_SIZE", "1")), "steps": steps,
+            "warmup": min(args.warmup, 1), "ms_per_step": round(secs / steps * 1e3, 3),
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "dtype": "u32" if app != "pagerank" else "f64", "data": "synthetic R-MAT",
+            "config": {"workload": f"{cfg}: {app}, n={n}, m={tgt.size}"},
+            "cpu_baseline": {"value": round(v, 5), "unit": "GTEPS", "cores": threads,
+                             "kind": "port", "sample": sample},
+            "e2e": {"value": round(v, 5), "unit": "GTEPS", "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--e2e-steps", type=int, default=5)
+    ap.add_argument("--impl", default="pgx", choices=["pgx", "reference"])
+    ap.add_argument("--config", default="C2", choices=sorted(APP_OF))
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3 and args.impl == "pgx":
+        args.warmup = 3
+    if args.impl == "reference":
+        bench_reference(args)
+    else:
+        bench_gpu(args)
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,147 @@
+/*
+ * pgx.h -- C ABI of libpgx.so, the B200 (sm_100a) superstep engine that
+ * replaces the hot path of the reference `pregelite` package.
+ *
+ * The reference reaches its hot path only through
+ *     pregelite.run(graph, program, config) -> RunReport
+ *         (/root/reference/pkg/src/pregelite/engine.py:201-204)
+ * whose body is `_Executor.run` (engine.py:255-316).  Each entry point
+ * below names the reference interface it replaces.  The Python host mirror
+ * (paper_2010_01542_b200/engine.py) binds these with ctypes; INTEGRATION.md
+ * shows the binding a maintainer of the reference would add.
+ *
+ * Conventions
+ *   - plain pointers and sizes only; every pointer argument that is not
+ *     marked "host" is a device pointer owned by the caller (the library
+ *     borrows it for the call and never frees it);
+ *   - calls are stream-ordered and asynchronous unless marked "syncs";
+ *     `stream` is a cudaStream_t passed as uintptr_t (0 = legacy default);
+ *   - return 0 on success or a negative PGX_E* code; pgx_last_error()
+ *     returns a thread-local message for the last failure.  The Python
+ *     side maps PGX_EINVAL to pregelite.ConfigError and everything else to
+ *     pregelite.ExecutionError (engine.py:277-280, 477-490).
+ *   - vertex ids are int32 (graph.py:143 default id dtype) and row offsets
+ *     are int32 on the device, so n < 2^31 and m < 2^31 (C5: m = 1.84e9).
+ */
+#ifndef PGX_H
+#define PGX_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define PGX_ABI_VERSION 1
+
+#define PGX_OK 0
+#define PGX_EINVAL (-1)   /* bad argument / unsupported configuration */
+#define PGX_ECUDA (-2)    /* CUDA runtime or kernel failure */
+#define PGX_ENOMEM (-3)   /* workspace too small */
+
+/* apps (the three lowered vertex programs, algorithms.py:27-152) */
+#define PGX_APP_PAGERANK 0
+#define PGX_APP_CC 1
+#define PGX_APP_SSSP 2
+
+/* combine operators (mailbox.py:58-70 min_combine / sum_combine) */
+#define PGX_OP_MIN_U32 0
+#define PGX_OP_SUM_F64 1
+
+/*
+ * Per-run statistics written by the device (int64 words):
+ *   stats[0] superstep_count        (RunReport.superstep_count)
+ *   stats[1] hit_superstep_cap      (RunReport.hit_superstep_cap)
+ *   stats[2] persistent CTAs used
+ *   stats[3] kernel start, %globaltimer ns
+ *   then PGX_STAT_FIELDS words per superstep s at stats + PGX_STAT_HDR +
+ *   s * PGX_STAT_FIELDS:
+ *     [0] active_count   (SuperstepStats.active_count, engine.py:284-286)
+ *     [1] messages_sent  (SuperstepStats.messages_sent)
+ *     [2] edges traversed by this superstep's senders (for GTEPS)
+ *     [3] senders with out-degree > 0 (#F_s)
+ *     [4] recipients of this superstep's messages (R_s)
+ *     [5] superstep end, %globaltimer ns
+ *     [6] vertices that computed a new value and sent (broadcasters)
+ *     [7] reserved
+ */
+#define PGX_STAT_HDR 4
+#define PGX_STAT_FIELDS 8
+
+int pgx_abi_version(void);
+const char *pgx_last_error(void);
+
+/* number of SMs of `device` (host out pointer; syncs) */
+int pgx_device_sm_count(int device, int *sm_count);
+
+/* ---------------------------------------------------------------- */
+/* graph preparation -- replaces the per-superstep work split of       */
+/* scheduler.py:91-116 (edge_balanced_partition) with a one-time       */
+/* edge-space tiling of the CSR                                        */
+/* ---------------------------------------------------------------- */
+
+/* int64 reference offsets (graph.py:28) -> int32 device row_ptr */
+int pgx_offsets_to_i32(const int64_t *offsets64, int32_t *row_ptr,
+                       int64_t count, uintptr_t stream);
+
+/* bytes of the per-graph workspace for n vertices / m edges (host out) */
+int pgx_graph_workspace_bytes(int64_t n, int64_t m, size_t *bytes);
+
+/* build the compacted non-zero-degree source list and its edge tiles */
+int pgx_graph_prepare(int32_t n, int64_t m, const int32_t *row_ptr,
+                      void *graph_ws, size_t graph_ws_bytes,
+                      uintptr_t stream);
+
+/* ---------------------------------------------------------------- */
+/* whole runs on one GPU: one persistent cooperative kernel per run,   */
+/* every superstep and the halt test on the device.                    */
+/* Replaces _Executor.run (engine.py:255-316) for the lowered programs */
+/* ---------------------------------------------------------------- */
+
+/* bytes of the per-run workspace (host out) */
+int pgx_run_workspace_bytes(int app, int64_t n, int64_t m,
+                            int32_t max_supersteps, size_t *bytes);
+
+/* sssp(source) -- algorithms.py:116-152 (push, min, uint32 hops) */
+int pgx_sssp_run(int32_t n, int64_t m, const int32_t *row_ptr,
+                 const int32_t *col_idx, const void *graph_ws,
+                 int32_t source, int32_t max_supersteps, uint32_t *dist,
+                 void *run_ws, size_t run_ws_bytes, int64_t *stats,
+                 uintptr_t stream);
+
+/* connected_components() -- algorithms.py:87-113 (Hashmin, min) */
+int pgx_cc_run(int32_t n, int64_t m, const int32_t *row_ptr,
+               const int32_t *col_idx, const void *graph_ws,
+               int32_t max_supersteps, uint32_t *labels, void *run_ws,
+               size_t run_ws_bytes, int64_t *stats, uintptr_t stream);
+
+/* pagerank(iterations, damping) -- algorithms.py:27-84 (fp64, sum).
+ * base = (1 - damping) / n and r0 = 1 / n are passed in as computed by
+ * the host (Python float arithmetic, algorithms.py:49-50). */
+int pgx_pagerank_run(int32_t n, int64_t m, const int32_t *row_ptr,
+                     const int32_t *col_idx, const void *graph_ws,
+                     int32_t iterations, double damping, double base,
+                     double r0, int32_t max_supersteps, double *rank,
+                     void *run_ws, size_t run_ws_bytes, int64_t *stats,
+                     uintptr_t stream);
+
+/* ---------------------------------------------------------------- */
+/* R-MAT input generator; input construction only.    */
+/* Writes src << 32 | dst keys of the non-loop draws in                */
+/* [first_draw, first_draw + num_draws) whose source lies in           */
+/* [src_lo, src_hi) -- plus the reverse keys when `symmetric` -- into  */
+/* keys[*count ...] (count is a device int64 counter, atomically       */
+/* advanced; the caller sorts and dedups).                             */
+/* ---------------------------------------------------------------- */
+int pgx_rmat_keys(int32_t scale, int64_t first_draw, int64_t num_draws,
+                  double a, double b, double c, uint64_t seed,
+                  int32_t symmetric, int64_t src_lo, int64_t src_hi,
+                  uint64_t *keys, int64_t capacity, int64_t *count,
+                  uintptr_t stream);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* PGX_H */

@@ -1,0 +1,94 @@
+"""ctypes binding of libpgx.so (include/pgx.h).
+
+The shared library is built in-tree by ``__graft_entry__.build()`` (nvcc,
+``-gencode arch=compute_100a,code=sm_100a``).  There is no fallback: if the
+library is missing, unloadable or no CUDA device is present, every run
+raises -- the product path is the CUDA kernel or nothing.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import os
+
+from .errors import ConfigError, ExecutionError
+
+PKG_DIR = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(PKG_DIR, "libpgx.so")
+
+PGX_ABI_VERSION = 1
+PGX_OK, PGX_EINVAL, PGX_ECUDA, PGX_ENOMEM = 0, -1, -2, -3
+PGX_APP_PAGERANK, PGX_APP_CC, PGX_APP_SSSP = 0, 1, 2
+PGX_OP_MIN_U32, PGX_OP_SUM_F64 = 0, 1
+PGX_STAT_HDR, PGX_STAT_FIELDS = 4, 8
+
+#: every symbol include/pgx.h declares (checked by tests/test_abi.py)
+EXPORTS = (
+    "pgx_abi_version", "pgx_last_error", "pgx_device_sm_count",
+    "pgx_offsets_to_i32", "pgx_graph_workspace_bytes", "pgx_graph_prepare",
+    "pgx_run_workspace_bytes", "pgx_sssp_run", "pgx_cc_run",
+    "pgx_pagerank_run", "pgx_rmat_keys",
+)
+
+_lib = None
+
+_p = ctypes.c_void_p
+_i32 = ctypes.c_int32
+_i64 = ctypes.c_int64
+_u64 = ctypes.c_uint64
+_f64 = ctypes.c_double
+_sz = ctypes.c_size_t
+_up = ctypes.c_size_t  # uintptr_t stream
+
+_SIGS = {
+    "pgx_abi_version": (ctypes.c_int, []),
+    "pgx_last_error": (ctypes.c_char_p, []),
+    "pgx_device_sm_count": (ctypes.c_int, [ctypes.c_int, _p]),
+    "pgx_offsets_to_i32": (ctypes.c_int, [_p, _p, _i64, _up]),
+    "pgx_graph_workspace_bytes": (ctypes.c_int, [_i64, _i64, _p]),
+    "pgx_graph_prepare": (ctypes.c_int, [_i32, _i64, _p, _p, _sz, _up]),
+    "pgx_run_workspace_bytes": (ctypes.c_int, [ctypes.c_int, _i64, _i64, _i32, _p]),
+    "pgx_sssp_run": (ctypes.c_int, [_i32, _i64, _p, _p, _p, _i32, _i32, _p, _p, _sz, _p, _up]),
+    "pgx_cc_run": (ctypes.c_int, [_i32, _i64, _p, _p, _p, _i32, _p, _p, _sz, _p, _up]),
+    "pgx_pagerank_run": (ctypes.c_int, [_i32, _i64, _p, _p, _p, _i32, _f64, _f64, _f64,
+                                        _i32, _p, _p, _sz, _p, _up]),
+    "pgx_rmat_keys": (ctypes.c_int, [_i32, _i64, _i64, _f64, _f64, _f64, _u64, _i32,
+                                     _i64, _i64, _p, _i64, _p, _up]),
+}
+
+
+def load():
+    """Load libpgx.so (raises if it was not built)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(LIB_PATH):
+        raise ExecutionError(
+            f"{LIB_PATH} is missing: build it with "
+            f"`python -c 'import __graft_entry__ as g; g.build()'` "
+            f"(there is no CPU fallback)")
+    lib = ctypes.CDLL(LIB_PATH)
+    for name, (res, args) in _SIGS.items():
+        fn = getattr(lib, name)
+        fn.restype = res
+        fn.argtypes = args
+    if lib.pgx_abi_version() != PGX_ABI_VERSION:
+        raise ExecutionError("libpgx.so ABI version mismatch; rebuild it")
+    _lib = lib
+    return lib
+
+
+def check(rc: int, what: str) -> None:
+    """Map a PGX status code onto the reference exception taxonomy."""
+    if rc == PGX_OK:
+        return
+    msg = (_lib.pgx_last_error() or b"").decode(errors="replace") if _lib else ""
+    if rc == PGX_EINVAL:
+        raise ConfigError(f"{what}: {msg}")
+    raise ExecutionError(f"{what} failed ({rc}): {msg}")
+
+
+def out_size(fn, *args) -> int:
+    v = ctypes.c_size_t(0)
+    check(fn(*args, ctypes.byref(v)), fn.__name__)
+    return int(v.value)

@@ -1,0 +1,979 @@
+// pgx_engine.cu -- B200 (sm_100a) push-superstep engine behind include/pgx.h.
+//
+// One persistent cooperative kernel runs a whole Pregel run: every
+// superstep's scatter (send + combine into the recipient mailbox), apply
+// (consume + compute + vote-to-halt) and the halt test stay on the device,
+// separated by a grid barrier.  Reference semantics:
+//   engine.py:255-316   _Executor.run (BSP loop, stats, quiescence, cap)
+//   engine.py:402-414   _chunk_push (consume, compute)
+//   engine.py:154-162   send_to_out_neighbors (per-edge send)
+//   mailbox.py:180-199  send_hybrid: publish-once + lock-free combine
+//   mailbox.py:147-165  apply_cas: skip the atomic when combine is a no-op
+//   algorithms.py       pagerank 27-84, connected_components 87-113,
+//                       sssp 116-152
+//   scheduler.py:91-116 edge_balanced_partition (edge-space split)
+//
+// Mapping of the paper's three optimisations onto sm_100a:
+//   hybrid combiner  -> read-filter (plain load, skip when min(old,msg)==old)
+//                       + one hardware atomicMin.u32 / red.add.f64; the
+//                       unique lane that gets NEUTRAL back is the first
+//                       publisher and appends the recipient to R (warp-
+//                       aggregated), replacing the lock-protected publish.
+//   externalisation  -> SoA: value[], mailbox[], frontier SoA, recipients.
+//   edge-centric     -> the frontier is built with its exclusive edge
+//                       prefix (one 64-bit packed atomic per warp); the
+//                       scatter walks fixed 4096-edge tiles of that edge
+//                       space, each CTA finds a tile's sources from a tile
+//                       map and each edge's source by a shared-memory
+//                       search -- exact edge balance, hub rows split.
+#include <cuda_runtime.h>
+#include <stdint.h>
+#include <stdio.h>
+#include <string.h>
+
+#include <algorithm>
+#include <cmath>
+#include <string>
+#include <type_traits>
+
+#include "../../include/pgx.h"
+
+namespace {
+
+constexpr int kBlock = 512;          // threads per CTA
+constexpr int kItems = 8;            // edges per thread per tile
+constexpr int kTile = kBlock * kItems;  // 4096 edges per tile
+constexpr int kSlots = kTile + 2;    // sources per tile (+ sentinel)
+constexpr uint32_t kNeutralMin = 0xFFFFFFFFu;
+constexpr int kMaxCtas = 4096;
+constexpr int kCompactBlock = 1024;
+
+thread_local std::string g_last_error;
+
+int fail(int code, const std::string &msg) {
+  g_last_error = msg;
+  return code;
+}
+
+int cuda_fail(cudaError_t e, const char *what) {
+  return fail(PGX_ECUDA, std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+#define PGX_CUDA(call)                                   \
+  do {                                                   \
+    cudaError_t _e = (call);                             \
+    if (_e != cudaSuccess) return cuda_fail(_e, #call);  \
+  } while (0)
+
+size_t align_up(size_t x, size_t a = 256) { return (x + a - 1) / a * a; }
+
+int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
+
+// ------------------------------------------------------------------
+// device helpers
+// ------------------------------------------------------------------
+
+__device__ __forceinline__ uint64_t globaltimer() {
+  uint64_t t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+
+__device__ __forceinline__ unsigned ld_acquire(const unsigned *p) {
+  unsigned v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+
+// streamed, read-only neighbour ids: no L1 allocation, first to leave L2
+__device__ __forceinline__ int ld_stream(const int *p, uint64_t pol) {
+  int v;
+  asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.b32 %0, [%1], %2;"
+               : "=r"(v) : "l"(p), "l"(pol));
+  return v;
+}
+
+__device__ __forceinline__ uint64_t evict_first_policy() {
+  uint64_t pol;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+  return pol;
+}
+
+__device__ __forceinline__ unsigned lane_id() { return threadIdx.x & 31u; }
+
+__device__ __forceinline__ unsigned lanemask_lt() {
+  unsigned m;
+  asm("mov.u32 %0, %%lanemask_lt;" : "=r"(m));
+  return m;
+}
+
+// Sense-counting grid barrier for a co-resident (cooperative) grid.  The
+// gpu-scope fences on both sides also invalidate L1 (CCTL.IVALL), so the
+// weak, L1-cacheable mailbox reads of the next phase never see values
+// from before the barrier.
+struct GridBarrier {
+  unsigned count;
+  unsigned gen;
+};
+
+__device__ __forceinline__ void grid_sync(GridBarrier *bar, unsigned &gen) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    unsigned arrived = atomicAdd(&bar->count, 1u);
+    if (arrived == gridDim.x - 1) {
+      bar->count = 0;
+      __threadfence();
+      atomicExch(&bar->gen, gen + 1);
+    } else {
+      while (ld_acquire(&bar->gen) == gen) {
+      }
+    }
+    __threadfence();
+  }
+  gen += 1;
+  __syncthreads();
+}
+
+// warp-aggregated append of `flag` lanes' `value` to list[*counter ...]
+__device__ __forceinline__ void warp_append(bool flag, int value, int *list,
+                                            unsigned *counter) {
+  unsigned mask = __ballot_sync(0xFFFFFFFFu, flag);
+  if (mask == 0) return;
+  int leader = __ffs(mask) - 1;
+  unsigned base = 0;
+  if ((int)lane_id() == leader) base = atomicAdd(counter, (unsigned)__popc(mask));
+  base = __shfl_sync(0xFFFFFFFFu, base, leader);
+  if (flag) list[base + __popc(mask & lanemask_lt())] = value;
+}
+
+template <typename T>
+__device__ __forceinline__ T block_sum(T v, T *red) {
+  // fixed-order tree: deterministic for a fixed block size
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_down_sync(0xFFFFFFFFu, v, o);
+  if (lane_id() == 0) red[threadIdx.x >> 5] = v;
+  __syncthreads();
+  T r = 0;
+  if (threadIdx.x < 32) {
+    r = (threadIdx.x < (blockDim.x >> 5)) ? red[threadIdx.x] : T(0);
+    for (int o = 16; o > 0; o >>= 1) r += __shfl_down_sync(0xFFFFFFFFu, r, o);
+  }
+  __syncthreads();
+  return r;  // valid in thread 0
+}
+
+// ------------------------------------------------------------------
+// workspace layouts
+// ------------------------------------------------------------------
+
+struct GraphWs {  // per graph, built once by pgx_graph_prepare
+  int32_t *hdr;        // [0] = number of non-zero-degree vertices
+  int32_t *nz_id;      // [n] ascending ids with out-degree > 0
+  int32_t *nz_eb;      // [n+1] their row starts (= exclusive edge prefix)
+  int32_t *tile_src;   // [ceil(m/kTile)+1] first nz index of each tile
+  int32_t *blk;        // [ceil(n/kCompactBlock)+1] compaction scratch
+};
+
+size_t graph_ws_layout(int64_t n, int64_t m, GraphWs *ws, char *base) {
+  size_t off = 0;
+  auto take = [&](size_t bytes) {
+    char *p = base ? base + off : nullptr;
+    off += align_up(bytes);
+    return p;
+  };
+  GraphWs w;
+  w.hdr = (int32_t *)take(16);
+  w.nz_id = (int32_t *)take(sizeof(int32_t) * (size_t)(n + 1));
+  w.nz_eb = (int32_t *)take(sizeof(int32_t) * (size_t)(n + 1));
+  w.tile_src = (int32_t *)take(sizeof(int32_t) * (size_t)(ceil_div(m, kTile) + 2));
+  w.blk = (int32_t *)take(sizeof(int32_t) * (size_t)(ceil_div(n, kCompactBlock) + 2));
+  if (ws) *ws = w;
+  return off;
+}
+
+struct StepCounters {
+  unsigned long long packed;  // senders << 32 | edges (frontier build)
+  unsigned recip;             // recipients published by the scatter
+  unsigned bcast;             // broadcasts (CC messages_sent)
+  unsigned long long pad[2];
+};
+
+struct RunWs {
+  GridBarrier *bar;        // zeroed by the host before every launch
+  StepCounters *ctr;       // [max_supersteps + 2]
+  double *partials;        // [kMaxCtas] PageRank dangling partial sums
+  unsigned long long *misc;  // [0] dangling vertex count
+  int32_t *f_eb;           // [n+1] frontier: exclusive edge prefix
+  int32_t *f_rs;           // [n]   frontier: CSR row start
+  void *f_msg;             // [n]   frontier: message (u32) / PR share (f64)
+  int32_t *recip;          // [n]   recipients of the last scatter
+  int32_t *tile_src;       // [ceil(m/kTile)+2] sparse tile map
+  void *mailbox;           // [n]   u32 (min) or f64 (sum)
+};
+
+size_t run_ws_layout(int app, int64_t n, int64_t m, int32_t max_steps, RunWs *ws,
+                     char *base) {
+  size_t off = 0;
+  auto take = [&](size_t bytes) {
+    char *p = base ? base + off : nullptr;
+    off += align_up(bytes);
+    return p;
+  };
+  const size_t W = app == PGX_APP_PAGERANK ? 8 : 4;
+  RunWs w;
+  w.bar = (GridBarrier *)take(64);
+  w.ctr = (StepCounters *)take(sizeof(StepCounters) * (size_t)(max_steps + 2));
+  w.partials = (double *)take(sizeof(double) * kMaxCtas);
+  w.misc = (unsigned long long *)take(64);
+  w.f_msg = take(W * (size_t)(n + 1));
+  w.mailbox = take(W * (size_t)(n + 1));
+  if (app != PGX_APP_PAGERANK) {
+    w.f_eb = (int32_t *)take(sizeof(int32_t) * (size_t)(n + 1));
+    w.f_rs = (int32_t *)take(sizeof(int32_t) * (size_t)(n + 1));
+    w.recip = (int32_t *)take(sizeof(int32_t) * (size_t)(n + 1));
+    w.tile_src = (int32_t *)take(sizeof(int32_t) * (size_t)(ceil_div(m, kTile) + 2));
+  } else {
+    w.f_eb = w.f_rs = w.recip = w.tile_src = nullptr;
+  }
+  if (ws) *ws = w;
+  return off;
+}
+
+// ------------------------------------------------------------------
+// the scatter phase: one pass of "every sender sends along its out-edges,
+// messages combined into the recipient's mailbox slot"
+// ------------------------------------------------------------------
+
+enum class MsgSrc { kFrontier, kSourceId, kShareById };
+
+struct ScatterArgs {
+  const int32_t *col;     // col_idx
+  const int32_t *eb;      // exclusive edge prefix per source
+  const int32_t *rs;      // row start per source (sparse only)
+  const int32_t *ids;     // vertex id per source (dense only)
+  const void *msg;        // per-source message (sparse) / per-vertex share
+  const int32_t *tile_src;
+  int32_t nsrc;           // number of sources
+  int64_t E;              // edges in this pass
+  void *mailbox;
+  int32_t *recip;         // first-publisher list (min only)
+  unsigned *recip_count;
+};
+
+template <int OP, MsgSrc MS>
+__device__ void scatter_phase(const ScatterArgs &a, char *smem) {
+  using Msg = typename std::conditional<OP == PGX_OP_SUM_F64, double, uint32_t>::type;
+  constexpr bool kDense = MS != MsgSrc::kFrontier;
+  int32_t *s_eb = reinterpret_cast<int32_t *>(smem);
+  int32_t *s_rs = s_eb + kSlots;
+  Msg *s_msg = reinterpret_cast<Msg *>(s_rs + kSlots);
+  const uint64_t pol = evict_first_policy();
+  const int64_t ntiles = (a.E + kTile - 1) / kTile;
+
+  for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
+    const int64_t e0 = t * kTile;
+    const int64_t e1 = min(a.E, e0 + kTile);
+    const int i0 = a.tile_src[t];
+    const int i1 = (t + 1 < ntiles) ? a.tile_src[t + 1] : a.nsrc - 1;
+    const int k = i1 - i0 + 1;  // <= kTile + 1: every source has >= 1 edge
+    for (int j = threadIdx.x; j <= k; j += kBlock) {
+      const int i = i0 + j;
+      if (j < k) {
+        s_eb[j] = a.eb[i];
+        if (!kDense) s_rs[j] = a.rs[i];
+        if (MS == MsgSrc::kFrontier) {
+          s_msg[j] = reinterpret_cast<const Msg *>(a.msg)[i];
+        } else if (MS == MsgSrc::kSourceId) {
+          s_msg[j] = (Msg)a.ids[i];
+        } else {
+          s_msg[j] = reinterpret_cast<const Msg *>(a.msg)[a.ids[i]];
+        }
+      } else {
+        s_eb[j] = (i < a.nsrc) ? a.eb[i] : (int32_t)a.E;  // sentinel
+      }
+    }
+    __syncthreads();
+
+    int w[kItems];
+    Msg mv[kItems];
+    int lo = 0;
+#pragma unroll
+    for (int j = 0; j < kItems; j++) {
+      const int64_t e = e0 + (int64_t)j * kBlock + threadIdx.x;
+      w[j] = -1;
+      if (e < e1) {
+        int hi = k;  // invariant: s_eb[lo] <= e < s_eb[hi]
+        while (hi - lo > 1) {
+          const int mid = (lo + hi) >> 1;
+          if (s_eb[mid] <= e) lo = mid; else hi = mid;
+        }
+        const int64_t pos = kDense ? e : (int64_t)s_rs[lo] + (e - s_eb[lo]);
+        w[j] = ld_stream(a.col + pos, pol);
+        mv[j] = s_msg[lo];
+      }
+    }
+    if (OP == PGX_OP_MIN_U32) {
+      uint32_t *mb = reinterpret_cast<uint32_t *>(a.mailbox);
+      uint32_t cur[kItems];
+#pragma unroll
+      for (int j = 0; j < kItems; j++) cur[j] = (w[j] >= 0) ? mb[w[j]] : 0u;
+#pragma unroll
+      for (int j = 0; j < kItems; j++) {
+        bool pub = false;
+        if (w[j] >= 0 && (uint32_t)mv[j] < cur[j]) {
+          const uint32_t old = atomicMin(mb + w[j], (uint32_t)mv[j]);
+          pub = (old == kNeutralMin);
+        }
+        warp_append(pub, w[j], a.recip, a.recip_count);
+      }
+    } else {
+      double *mb = reinterpret_cast<double *>(a.mailbox);
+#pragma unroll
+      for (int j = 0; j < kItems; j++)
+        if (w[j] >= 0) atomicAdd(mb + w[j], (double)mv[j]);
+    }
+    __syncthreads();
+  }
+}
+
+// ------------------------------------------------------------------
+// sparse apply for the min programs (SSSP / CC): consume every recipient's
+// mailbox, adopt an improvement, append improved vertices to the next
+// frontier with their edge prefix (edge-balanced frontier construction)
+// ------------------------------------------------------------------
+
+template <int APP>
+__device__ void apply_min_phase(const int32_t *__restrict__ row_ptr, uint32_t *val,
+                                uint32_t *mailbox, const int32_t *recip, unsigned nrecip,
+                                const RunWs &ws, StepCounters *ctr,
+                                unsigned *s_bcast) {
+  const unsigned nthreads = gridDim.x * blockDim.x;
+  const unsigned gtid = blockIdx.x * blockDim.x + threadIdx.x;
+  const unsigned warp_base = gtid & ~31u;
+  uint32_t *f_msg = reinterpret_cast<uint32_t *>(ws.f_msg);
+  unsigned my_bcast = 0;
+  for (unsigned base = warp_base; base < nrecip; base += nthreads) {
+    const unsigned r = base + lane_id();
+    bool improved = false;
+    int v = 0, deg = 0, rs = 0;
+    uint32_t send = 0;
+    if (r < nrecip) {
+      v = recip[r];
+      const uint32_t m = mailbox[v];
+      mailbox[v] = kNeutralMin;  // consume (mailbox.py:112-117)
+      if (m < val[v]) {
+        val[v] = m;
+        improved = true;
+        send = (APP == PGX_APP_SSSP) ? m + 1u : m;
+        rs = row_ptr[v];
+        deg = row_ptr[v + 1] - rs;
+      }
+    }
+    my_bcast += improved ? 1u : 0u;
+    const bool has = improved && deg > 0;
+    // warp exclusive scan of degrees over the senders with edges
+    int x = has ? deg : 0;
+    int incl = x;
+    for (int o = 1; o < 32; o <<= 1) {
+      const int y = __shfl_up_sync(0xFFFFFFFFu, incl, o);
+      if ((int)lane_id() >= o) incl += y;
+    }
+    const unsigned hm = __ballot_sync(0xFFFFFFFFu, has);
+    if (hm == 0) continue;
+    const int total = __shfl_sync(0xFFFFFFFFu, incl, 31);
+    unsigned long long packed = 0;
+    if (lane_id() == 0)
+      packed = atomicAdd(&ctr->packed,
+                         ((unsigned long long)__popc(hm) << 32) | (unsigned long long)total);
+    packed = __shfl_sync(0xFFFFFFFFu, packed, 0);
+    if (has) {
+      const unsigned pos = (unsigned)(packed >> 32) + __popc(hm & lanemask_lt());
+      const int eb = (int)(packed & 0xFFFFFFFFull) + incl - x;
+      ws.f_eb[pos] = eb;
+      ws.f_rs[pos] = rs;
+      f_msg[pos] = send;
+      for (int64_t t = ((int64_t)eb + kTile - 1) / kTile; t * kTile < (int64_t)eb + deg; t++)
+        ws.tile_src[t] = (int)pos;
+    }
+  }
+  atomicAdd(s_bcast, my_bcast);
+}
+
+__device__ __forceinline__ void record_step(int64_t *stats, int s, int64_t active,
+                                            int64_t sent, int64_t edges, int64_t senders,
+                                            int64_t recips, int64_t bcast) {
+  int64_t *st = stats + PGX_STAT_HDR + (int64_t)s * PGX_STAT_FIELDS;
+  st[0] = active;
+  st[1] = sent;
+  st[2] = edges;
+  st[3] = senders;
+  st[4] = recips;
+  st[5] = (int64_t)globaltimer();
+  st[6] = bcast;
+  st[7] = 0;
+}
+
+// ------------------------------------------------------------------
+// persistent run kernels
+// ------------------------------------------------------------------
+
+struct MinRunParams {
+  int32_t n;
+  int64_t m;
+  const int32_t *row_ptr;
+  const int32_t *col;
+  GraphWs g;
+  RunWs ws;
+  uint32_t *val;
+  int32_t source;  // SSSP only
+  int32_t max_steps;
+  int64_t *stats;
+};
+
+template <int APP>
+__global__ void __launch_bounds__(kBlock, 2) min_run_kernel(MinRunParams p) {
+  extern __shared__ __align__(16) char smem[];
+  __shared__ unsigned s_bcast;
+  __shared__ unsigned s_flag;
+  unsigned gen = 0;
+  if (threadIdx.x == 0) gen = ld_acquire(&p.ws.bar->gen);
+  uint32_t *mailbox = reinterpret_cast<uint32_t *>(p.ws.mailbox);
+  const unsigned nthreads = gridDim.x * blockDim.x;
+  const unsigned gtid = blockIdx.x * blockDim.x + threadIdx.x;
+
+  // ---- setup (algorithms.py:96-97 / 129-134) + superstep-0 senders ----
+  for (unsigned v = gtid; v < (unsigned)p.n; v += nthreads) {
+    p.val[v] = (APP == PGX_APP_CC) ? v : kNeutralMin;
+    mailbox[v] = kNeutralMin;
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    p.stats[0] = p.stats[1] = 0;
+    p.stats[2] = gridDim.x;
+    p.stats[3] = (int64_t)globaltimer();
+    StepCounters z = {};
+    p.ws.ctr[0] = z;
+    p.ws.ctr[1] = z;
+    if (APP == PGX_APP_SSSP) {
+      const int rs = p.row_ptr[p.source];
+      const int deg = p.row_ptr[p.source + 1] - rs;
+      if (deg > 0) {
+        p.ws.f_eb[0] = 0;
+        p.ws.f_rs[0] = rs;
+        reinterpret_cast<uint32_t *>(p.ws.f_msg)[0] = 1u;
+        for (int64_t t = 0; t * kTile < deg; t++) p.ws.tile_src[t] = 0;
+        p.ws.ctr[0].packed = (1ull << 32) | (unsigned long long)deg;
+      }
+      p.ws.ctr[0].bcast = 1u;  // the source computes and sends in superstep 0
+    } else {
+      p.ws.ctr[0].bcast = (unsigned)p.n;  // every vertex broadcasts its id
+    }
+  }
+  grid_sync(p.ws.bar, gen);
+  if (APP == PGX_APP_SSSP && gtid == 0) p.val[p.source] = 0u;
+
+  for (int s = 0;; s++) {
+    // ---- scatter(s) ----
+    ScatterArgs a;
+    a.col = p.col;
+    a.mailbox = mailbox;
+    a.recip = p.ws.recip;
+    a.recip_count = &p.ws.ctr[s].recip;
+    if (APP == PGX_APP_CC && s == 0) {
+      a.eb = p.g.nz_eb;
+      a.rs = nullptr;
+      a.ids = p.g.nz_id;
+      a.msg = nullptr;
+      a.tile_src = p.g.tile_src;
+      a.nsrc = p.g.hdr[0];
+      a.E = p.m;
+      scatter_phase<PGX_OP_MIN_U32, MsgSrc::kSourceId>(a, smem);
+    } else {
+      const unsigned long long packed = p.ws.ctr[s].packed;
+      a.eb = p.ws.f_eb;
+      a.rs = p.ws.f_rs;
+      a.ids = nullptr;
+      a.msg = p.ws.f_msg;
+      a.tile_src = p.ws.tile_src;
+      a.nsrc = (int32_t)(packed >> 32);
+      a.E = (int64_t)(packed & 0xFFFFFFFFull);
+      scatter_phase<PGX_OP_MIN_U32, MsgSrc::kFrontier>(a, smem);
+    }
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+      StepCounters z = {};
+      p.ws.ctr[s + 1] = z;
+    }
+    grid_sync(p.ws.bar, gen);
+
+    // ---- halt test (engine.py:288-300) ----
+    const unsigned nrecip = p.ws.ctr[s].recip;
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+      const StepCounters c = p.ws.ctr[s];
+      const int64_t senders = (int64_t)(c.packed >> 32);
+      const int64_t edges = (APP == PGX_APP_CC && s == 0) ? p.m : (int64_t)(c.packed & 0xFFFFFFFFull);
+      const int64_t active = (s == 0) ? p.n : (int64_t)p.ws.ctr[s - 1].recip;
+      const int64_t sent = (APP == PGX_APP_SSSP) ? edges : (int64_t)c.bcast;
+      record_step(p.stats, s, active, sent, edges,
+                  (APP == PGX_APP_CC && s == 0) ? (int64_t)p.g.hdr[0] : senders, nrecip,
+                  (int64_t)c.bcast);
+      if (nrecip == 0) {
+        p.stats[0] = s + 1;
+      } else if (s + 1 == p.max_steps) {
+        p.stats[0] = s + 1;
+        p.stats[1] = 1;
+      }
+    }
+    if (nrecip == 0 || s + 1 == p.max_steps) break;
+
+    // ---- apply(s+1): consume + compute + frontier build ----
+    if (threadIdx.x == 0) s_bcast = 0;
+    __syncthreads();
+    apply_min_phase<APP>(p.row_ptr, p.val, mailbox, p.ws.recip, nrecip, p.ws, &p.ws.ctr[s + 1],
+                         &s_bcast);
+    __syncthreads();
+    if (threadIdx.x == 0 && s_bcast) atomicAdd(&p.ws.ctr[s + 1].bcast, s_bcast);
+    grid_sync(p.ws.bar, gen);
+  }
+  (void)s_flag;
+}
+
+struct PrRunParams {
+  int32_t n;
+  int64_t m;
+  const int32_t *row_ptr;
+  const int32_t *col;
+  GraphWs g;
+  RunWs ws;
+  double *rank;
+  int32_t iterations;
+  double damping, base, r0;
+  int32_t max_steps;
+  int64_t *stats;
+};
+
+__global__ void __launch_bounds__(kBlock, 2) pagerank_run_kernel(PrRunParams p) {
+  extern __shared__ __align__(16) char smem[];
+  __shared__ double s_red[32];
+  __shared__ unsigned long long s_ured[32];
+  __shared__ double s_dangling;
+  unsigned gen = 0;
+  if (threadIdx.x == 0) gen = ld_acquire(&p.ws.bar->gen);
+  double *mailbox = reinterpret_cast<double *>(p.ws.mailbox);
+  double *share = reinterpret_cast<double *>(p.ws.f_msg);
+  const unsigned nthreads = gridDim.x * blockDim.x;
+  const unsigned gtid = blockIdx.x * blockDim.x + threadIdx.x;
+  const int last = p.iterations - 1;
+  const double dn_n = (double)p.n;
+
+  // ---- setup (algorithms.py:44-59): rank = r0, seed shares r0/outdeg ----
+  unsigned long long my_dangling = 0;
+  for (unsigned v = gtid; v < (unsigned)p.n; v += nthreads) {
+    const int deg = p.row_ptr[v + 1] - p.row_ptr[v];
+    p.rank[v] = p.r0;
+    mailbox[v] = 0.0;
+    share[v] = deg ? __ddiv_rn(p.r0, (double)deg) : 0.0;
+    my_dangling += deg ? 0ull : 1ull;
+  }
+  unsigned long long bd = block_sum<unsigned long long>(my_dangling, s_ured);
+  if (threadIdx.x == 0) {
+    if (bd) atomicAdd(&p.ws.misc[0], bd);
+    if (blockIdx.x == 0) {
+      p.stats[0] = p.stats[1] = 0;
+      p.stats[2] = gridDim.x;
+      p.stats[3] = (int64_t)globaltimer();
+    }
+  }
+  grid_sync(p.ws.bar, gen);
+
+  ScatterArgs a;
+  a.col = p.col;
+  a.eb = p.g.nz_eb;
+  a.rs = nullptr;
+  a.ids = p.g.nz_id;
+  a.msg = share;
+  a.tile_src = p.g.tile_src;
+  a.nsrc = p.g.hdr[0];
+  a.E = p.m;
+  a.mailbox = mailbox;
+  a.recip = nullptr;
+  a.recip_count = nullptr;
+  const unsigned long long ndangling = p.ws.misc[0];
+  double dangling = __dmul_rn(p.r0, (double)ndangling);  // algorithms.py:55
+  const int64_t nspread = (int64_t)p.n - (int64_t)ndangling;
+
+  // the setup seed is folded in superstep 0 (algorithms.py:56-59)
+  scatter_phase<PGX_OP_SUM_F64, MsgSrc::kShareById>(a, smem);
+  grid_sync(p.ws.bar, gen);
+
+  for (int s = 0;; s++) {
+    // ---- apply(s): rank = base + d * (folded + dangling / n) ----
+    const double dn = __ddiv_rn(dangling, dn_n);
+    double my_d = 0.0;
+    for (unsigned v = gtid; v < (unsigned)p.n; v += nthreads) {
+      const double folded = mailbox[v];
+      mailbox[v] = 0.0;
+      const double r = __dadd_rn(p.base, __dmul_rn(p.damping, __dadd_rn(folded, dn)));
+      p.rank[v] = r;
+      const int deg = p.row_ptr[v + 1] - p.row_ptr[v];
+      if (deg == 0) my_d = __dadd_rn(my_d, r);
+      else if (s != last) share[v] = __ddiv_rn(r, (double)deg);
+    }
+    const double bsum = block_sum<double>(my_d, s_red);
+    if (threadIdx.x == 0) p.ws.partials[blockIdx.x] = bsum;
+    grid_sync(p.ws.bar, gen);
+
+    // ---- on_superstep_end (algorithms.py:75-78): dangling mass ----
+    {
+      double acc = 0.0;
+      for (int b = threadIdx.x; b < (int)gridDim.x; b += kBlock) acc = __dadd_rn(acc, p.ws.partials[b]);
+      const double tot = block_sum<double>(acc, s_red);
+      if (threadIdx.x == 0) s_dangling = tot;
+      __syncthreads();
+      dangling = s_dangling;
+    }
+    const bool cap = (s + 1 == p.max_steps);
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+      record_step(p.stats, s, p.n, (s == last) ? 0 : nspread, p.m, nspread, p.n,
+                  (s == last) ? 0 : nspread);
+      if (s == last || cap) {
+        p.stats[0] = s + 1;
+        p.stats[1] = (s == last) ? 0 : 1;
+      }
+    }
+    if (s == last || cap) break;
+    scatter_phase<PGX_OP_SUM_F64, MsgSrc::kShareById>(a, smem);
+    grid_sync(p.ws.bar, gen);
+  }
+}
+
+// ------------------------------------------------------------------
+// graph preparation kernels: order-preserving compaction of the vertices
+// with out-degree > 0 (warp ballot + block scan), then the tile map
+// ------------------------------------------------------------------
+
+__global__ void offsets_to_i32_kernel(const int64_t *in, int32_t *out, int64_t count) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < count;
+       i += (int64_t)gridDim.x * blockDim.x)
+    out[i] = (int32_t)in[i];
+}
+
+__device__ __forceinline__ int block_excl_scan(int x, int *s_warp, int *total) {
+  int incl = x;
+  for (int o = 1; o < 32; o <<= 1) {
+    const int y = __shfl_up_sync(0xFFFFFFFFu, incl, o);
+    if ((int)lane_id() >= o) incl += y;
+  }
+  if (lane_id() == 31) s_warp[threadIdx.x >> 5] = incl;
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    const int nw = blockDim.x >> 5;
+    int w = (threadIdx.x < nw) ? s_warp[threadIdx.x] : 0;
+    int wi = w;
+    for (int o = 1; o < 32; o <<= 1) {
+      const int y = __shfl_up_sync(0xFFFFFFFFu, wi, o);
+      if ((int)threadIdx.x >= o) wi += y;
+    }
+    if (threadIdx.x < nw) s_warp[threadIdx.x] = wi - w;
+    if (threadIdx.x == 31) s_warp[32] = wi;
+  }
+  __syncthreads();
+  const int r = s_warp[threadIdx.x >> 5] + incl - x;
+  *total = s_warp[32];
+  __syncthreads();
+  return r;
+}
+
+__global__ void nz_count_kernel(const int32_t *row_ptr, int32_t n, int32_t *blk) {
+  __shared__ int s_warp[33];
+  const int64_t v = blockIdx.x * (int64_t)kCompactBlock + threadIdx.x;
+  const int f = (v < n && row_ptr[v + 1] > row_ptr[v]) ? 1 : 0;
+  int total;
+  block_excl_scan(f, s_warp, &total);
+  if (threadIdx.x == 0) blk[blockIdx.x] = total;
+}
+
+__global__ void nz_scan_blocks_kernel(int32_t *blk, int32_t nb, int32_t *hdr) {
+  // single CTA: exclusive scan of per-block counts
+  __shared__ int s_warp[33];
+  int carry = 0;
+  for (int base = 0; base < nb; base += kCompactBlock) {
+    const int i = base + threadIdx.x;
+    const int x = (i < nb) ? blk[i] : 0;
+    int total;
+    const int ex = block_excl_scan(x, s_warp, &total);
+    if (i < nb) blk[i] = carry + ex;
+    carry += total;
+  }
+  if (threadIdx.x == 0) {
+    blk[nb] = carry;
+    hdr[0] = carry;
+  }
+}
+
+__global__ void nz_write_kernel(const int32_t *row_ptr, int32_t n, const int32_t *blk,
+                                int32_t *nz_id, int32_t *nz_eb, int64_t m) {
+  __shared__ int s_warp[33];
+  const int64_t v = blockIdx.x * (int64_t)kCompactBlock + threadIdx.x;
+  const int f = (v < n && row_ptr[v + 1] > row_ptr[v]) ? 1 : 0;
+  int total;
+  const int ex = block_excl_scan(f, s_warp, &total);
+  if (f) {
+    const int pos = blk[blockIdx.x] + ex;
+    nz_id[pos] = (int32_t)v;
+    nz_eb[pos] = row_ptr[v];
+  }
+  if (blockIdx.x == gridDim.x - 1 && threadIdx.x == 0) nz_eb[blk[gridDim.x]] = (int32_t)m;
+}
+
+__global__ void tile_map_kernel(const int32_t *hdr, const int32_t *nz_eb, int32_t *tile_src) {
+  const int nnz = hdr[0];
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < nnz; i += gridDim.x * blockDim.x) {
+    const int64_t eb = nz_eb[i], ee = nz_eb[i + 1];
+    for (int64_t t = (eb + kTile - 1) / kTile; t * kTile < ee; t++) tile_src[t] = i;
+  }
+}
+
+// ------------------------------------------------------------------
+// R-MAT generator, input construction only
+// ------------------------------------------------------------------
+
+__device__ __forceinline__ uint64_t splitmix64(uint64_t z) {
+  z += 0x9E3779B97F4A7C15ull;
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+  return z ^ (z >> 31);
+}
+
+__global__ void rmat_kernel(int scale, int64_t first, int64_t count, uint64_t ta, uint64_t tab,
+                            uint64_t tabc, uint64_t base, int symmetric, int64_t lo, int64_t hi,
+                            unsigned long long *keys, int64_t capacity,
+                            unsigned long long *counter) {
+  for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < count;
+       k += (int64_t)gridDim.x * blockDim.x) {
+    const uint64_t i = (uint64_t)(first + k);
+    uint64_t s = 0, d = 0;
+    for (int l = 0; l < scale; l++) {
+      const uint64_t r = splitmix64(base + i * (uint64_t)scale + (uint64_t)l) >> 11;
+      const int q = r < ta ? 0 : r < tab ? 1 : r < tabc ? 2 : 3;
+      const int bit = scale - 1 - l;
+      s |= (uint64_t)(q >> 1) << bit;
+      d |= (uint64_t)(q & 1) << bit;
+    }
+    if (s == d) continue;
+    const bool fwd = (int64_t)s >= lo && (int64_t)s < hi;
+    const bool rev = symmetric && (int64_t)d >= lo && (int64_t)d < hi;
+    const int cnt = (fwd ? 1 : 0) + (rev ? 1 : 0);
+    if (!cnt) continue;
+    unsigned long long pos = atomicAdd(counter, (unsigned long long)cnt);
+    if (fwd && (int64_t)pos < capacity) keys[pos++] = (s << 32) | d;
+    if (rev && (int64_t)pos < capacity) keys[pos] = (d << 32) | s;
+  }
+}
+
+// ------------------------------------------------------------------
+// launch helpers
+// ------------------------------------------------------------------
+
+size_t scatter_smem_bytes(int op) {
+  return (size_t)kSlots * (sizeof(int32_t) * 2 + (op == PGX_OP_SUM_F64 ? 8 : 4)) + 16;
+}
+
+template <typename K>
+int coop_grid(K kernel, size_t smem, int *grid) {
+  int dev = 0, sms = 0, per_sm = 0;
+  PGX_CUDA(cudaGetDevice(&dev));
+  PGX_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+  PGX_CUDA(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  PGX_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, kBlock, smem));
+  if (per_sm < 1) return fail(PGX_ECUDA, "persistent kernel does not fit on an SM");
+  int g = sms * per_sm;
+  if (g > kMaxCtas) g = kMaxCtas;
+  *grid = g;
+  return PGX_OK;
+}
+
+int check_graph(int32_t n, int64_t m, const int32_t *row_ptr, const int32_t *col_idx,
+                const void *graph_ws) {
+  if (n < 1) return fail(PGX_EINVAL, "vertex count must be >= 1 on the device path");
+  if (m < 0 || m > INT32_MAX) return fail(PGX_EINVAL, "edge count must be in [0, 2^31)");
+  if (!row_ptr || !graph_ws || (m > 0 && !col_idx))
+    return fail(PGX_EINVAL, "null graph pointer");
+  return PGX_OK;
+}
+
+}  // namespace
+
+// ==================================================================
+// C ABI
+// ==================================================================
+
+extern "C" {
+
+int pgx_abi_version(void) { return PGX_ABI_VERSION; }
+
+const char *pgx_last_error(void) { return g_last_error.c_str(); }
+
+int pgx_device_sm_count(int device, int *sm_count) {
+  if (!sm_count) return fail(PGX_EINVAL, "null out pointer");
+  PGX_CUDA(cudaDeviceGetAttribute(sm_count, cudaDevAttrMultiProcessorCount, device));
+  return PGX_OK;
+}
+
+int pgx_offsets_to_i32(const int64_t *offsets64, int32_t *row_ptr, int64_t count,
+                       uintptr_t stream) {
+  if (count < 0 || (count && (!offsets64 || !row_ptr))) return fail(PGX_EINVAL, "bad offsets");
+  if (!count) return PGX_OK;
+  const int grid = (int)std::min<int64_t>(ceil_div(count, 256), 148 * 16);
+  offsets_to_i32_kernel<<<grid, 256, 0, (cudaStream_t)stream>>>(offsets64, row_ptr, count);
+  PGX_CUDA(cudaGetLastError());
+  return PGX_OK;
+}
+
+int pgx_graph_workspace_bytes(int64_t n, int64_t m, size_t *bytes) {
+  if (!bytes || n < 0 || m < 0) return fail(PGX_EINVAL, "bad sizes");
+  *bytes = graph_ws_layout(n, m, nullptr, nullptr);
+  return PGX_OK;
+}
+
+int pgx_graph_prepare(int32_t n, int64_t m, const int32_t *row_ptr, void *graph_ws,
+                      size_t graph_ws_bytes, uintptr_t stream) {
+  if (n < 1 || m < 0 || m > INT32_MAX || !row_ptr || !graph_ws)
+    return fail(PGX_EINVAL, "bad graph_prepare arguments");
+  GraphWs g;
+  if (graph_ws_layout(n, m, &g, (char *)graph_ws) > graph_ws_bytes)
+    return fail(PGX_ENOMEM, "graph workspace too small");
+  cudaStream_t st = (cudaStream_t)stream;
+  const int nb = (int)ceil_div(n, kCompactBlock);
+  nz_count_kernel<<<nb, kCompactBlock, 0, st>>>(row_ptr, n, g.blk);
+  nz_scan_blocks_kernel<<<1, kCompactBlock, 0, st>>>(g.blk, nb, g.hdr);
+  nz_write_kernel<<<nb, kCompactBlock, 0, st>>>(row_ptr, n, g.blk, g.nz_id, g.nz_eb, m);
+  int sms = 148;
+  int dev = 0;
+  if (cudaGetDevice(&dev) == cudaSuccess)
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  tile_map_kernel<<<sms * 8, 256, 0, st>>>(g.hdr, g.nz_eb, g.tile_src);
+  PGX_CUDA(cudaGetLastError());
+  return PGX_OK;
+}
+
+int pgx_run_workspace_bytes(int app, int64_t n, int64_t m, int32_t max_supersteps,
+                            size_t *bytes) {
+  if (!bytes || n < 0 || m < 0 || max_supersteps < 1 || app < 0 || app > 2)
+    return fail(PGX_EINVAL, "bad run workspace arguments");
+  *bytes = run_ws_layout(app, n, m, max_supersteps, nullptr, nullptr);
+  return PGX_OK;
+}
+
+static int min_run(int app, int32_t n, int64_t m, const int32_t *row_ptr, const int32_t *col_idx,
+                   const void *graph_ws, int32_t source, int32_t max_supersteps, uint32_t *val,
+                   void *run_ws, size_t run_ws_bytes, int64_t *stats, uintptr_t stream) {
+  int rc = check_graph(n, m, row_ptr, col_idx, graph_ws);
+  if (rc) return rc;
+  if (max_supersteps < 1) return fail(PGX_EINVAL, "superstep cap must be >= 1");
+  if (!val || !run_ws || !stats) return fail(PGX_EINVAL, "null output pointer");
+  if (app == PGX_APP_SSSP && (source < 0 || source >= n))
+    return fail(PGX_EINVAL, "source vertex out of range");
+  MinRunParams p;
+  p.n = n;
+  p.m = m;
+  p.row_ptr = row_ptr;
+  p.col = col_idx;
+  graph_ws_layout(n, m, &p.g, (char *)graph_ws);
+  if (run_ws_layout(app, n, m, max_supersteps, &p.ws, (char *)run_ws) > run_ws_bytes)
+    return fail(PGX_ENOMEM, "run workspace too small");
+  p.val = val;
+  p.source = source;
+  p.max_steps = max_supersteps;
+  p.stats = stats;
+  cudaStream_t st = (cudaStream_t)stream;
+  PGX_CUDA(cudaMemsetAsync(p.ws.bar, 0, 64, st));
+  const size_t smem = scatter_smem_bytes(PGX_OP_MIN_U32);
+  int grid = 0;
+  void *args[] = {&p};
+  if (app == PGX_APP_SSSP) {
+    rc = coop_grid(min_run_kernel<PGX_APP_SSSP>, smem, &grid);
+    if (rc) return rc;
+    PGX_CUDA(cudaLaunchCooperativeKernel((void *)min_run_kernel<PGX_APP_SSSP>, grid, kBlock,
+                                         args, smem, st));
+  } else {
+    rc = coop_grid(min_run_kernel<PGX_APP_CC>, smem, &grid);
+    if (rc) return rc;
+    PGX_CUDA(cudaLaunchCooperativeKernel((void *)min_run_kernel<PGX_APP_CC>, grid, kBlock,
+                                         args, smem, st));
+  }
+  return PGX_OK;
+}
+
+int pgx_sssp_run(int32_t n, int64_t m, const int32_t *row_ptr, const int32_t *col_idx,
+                 const void *graph_ws, int32_t source, int32_t max_supersteps, uint32_t *dist,
+                 void *run_ws, size_t run_ws_bytes, int64_t *stats, uintptr_t stream) {
+  return min_run(PGX_APP_SSSP, n, m, row_ptr, col_idx, graph_ws, source, max_supersteps, dist,
+                 run_ws, run_ws_bytes, stats, stream);
+}
+
+int pgx_cc_run(int32_t n, int64_t m, const int32_t *row_ptr, const int32_t *col_idx,
+               const void *graph_ws, int32_t max_supersteps, uint32_t *labels, void *run_ws,
+               size_t run_ws_bytes, int64_t *stats, uintptr_t stream) {
+  return min_run(PGX_APP_CC, n, m, row_ptr, col_idx, graph_ws, 0, max_supersteps, labels, run_ws,
+                 run_ws_bytes, stats, stream);
+}
+
+int pgx_pagerank_run(int32_t n, int64_t m, const int32_t *row_ptr, const int32_t *col_idx,
+                     const void *graph_ws, int32_t iterations, double damping, double base,
+                     double r0, int32_t max_supersteps, double *rank, void *run_ws,
+                     size_t run_ws_bytes, int64_t *stats, uintptr_t stream) {
+  int rc = check_graph(n, m, row_ptr, col_idx, graph_ws);
+  if (rc) return rc;
+  if (iterations < 1) return fail(PGX_EINVAL, "iterations must be >= 1");
+  if (!(damping >= 0.0 && damping <= 1.0)) return fail(PGX_EINVAL, "damping must be in [0, 1]");
+  if (max_supersteps < 1) return fail(PGX_EINVAL, "superstep cap must be >= 1");
+  if (!rank || !run_ws || !stats) return fail(PGX_EINVAL, "null output pointer");
+  PrRunParams p;
+  p.n = n;
+  p.m = m;
+  p.row_ptr = row_ptr;
+  p.col = col_idx;
+  graph_ws_layout(n, m, &p.g, (char *)graph_ws);
+  if (run_ws_layout(PGX_APP_PAGERANK, n, m, max_supersteps, &p.ws, (char *)run_ws) > run_ws_bytes)
+    return fail(PGX_ENOMEM, "run workspace too small");
+  p.rank = rank;
+  p.iterations = iterations;
+  p.damping = damping;
+  p.base = base;
+  p.r0 = r0;
+  p.max_steps = max_supersteps;
+  p.stats = stats;
+  cudaStream_t st = (cudaStream_t)stream;
+  PGX_CUDA(cudaMemsetAsync(p.ws.bar, 0, 64, st));
+  PGX_CUDA(cudaMemsetAsync(p.ws.misc, 0, 64, st));
+  const size_t smem = scatter_smem_bytes(PGX_OP_SUM_F64);
+  int grid = 0;
+  rc = coop_grid(pagerank_run_kernel, smem, &grid);
+  if (rc) return rc;
+  void *args[] = {&p};
+  PGX_CUDA(cudaLaunchCooperativeKernel((void *)pagerank_run_kernel, grid, kBlock, args, smem, st));
+  return PGX_OK;
+}
+
+int pgx_rmat_keys(int32_t scale, int64_t first_draw, int64_t num_draws, double a, double b,
+                  double c, uint64_t seed, int32_t symmetric, int64_t src_lo, int64_t src_hi,
+                  uint64_t *keys, int64_t capacity, int64_t *count, uintptr_t stream) {
+  if (scale < 1 || scale > 30 || num_draws < 0 || !keys || !count)
+    return fail(PGX_EINVAL, "bad R-MAT arguments");
+  if (!num_draws) return PGX_OK;
+  const double two53 = 9007199254740992.0;
+  const uint64_t ta = (uint64_t)floor(a * two53);
+  const uint64_t tab = (uint64_t)floor((a + b) * two53);
+  const uint64_t tabc = (uint64_t)floor((a + b + c) * two53);
+  uint64_t z = seed + 0x9E3779B97F4A7C15ull;
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+  const uint64_t base = z ^ (z >> 31);
+  const int grid = (int)std::min<int64_t>(ceil_div(num_draws, 256), 148 * 32);
+  rmat_kernel<<<grid, 256, 0, (cudaStream_t)stream>>>(
+      scale, first_draw, num_draws, ta, tab, tabc, base, symmetric, src_lo, src_hi,
+      (unsigned long long *)keys, capacity, (unsigned long long *)count);
+  PGX_CUDA(cudaGetLastError());
+  return PGX_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,309 @@
+"""Superstep executor host side (reference: engine.py).
+
+``run(graph, program, config)`` keeps the reference signature and return
+type (engine.py:201-204, 94-108).  The reference body -- ``_Executor.run``
+with W worker threads, two barriers per superstep and per-vertex Python
+callbacks (engine.py:255-474) -- is replaced by ONE call into libpgx.so:
+a persistent cooperative kernel that runs every superstep (scatter with
+the hybrid combiner, apply, frontier build, halt test) on the B200 and
+writes per-superstep statistics to device memory.  The host reads the
+statistics back once, after the run.
+
+Only the three built-in programs have a device lowering (their factories
+tag the compute callable).  A program whose compute has no lowering, or
+whose setup / hook / combine were swapped for other callables, raises
+``ConfigError``: there is no CPU fallback.  ``extract`` overrides are
+honoured (applied to the final state on the host, engine.py:310-311).
+"""
+
+from __future__ import annotations
+
+import ctypes
+import time
+from dataclasses import dataclass, field
+from enum import Enum
+from types import SimpleNamespace
+from typing import Any, Callable
+
+import numpy as np
+import torch
+
+from . import _lib
+from .errors import ConfigError, ExecutionError
+from .graph import Graph
+from .layout import LayoutMode
+from .mailbox import CombineFn, CombinerKind
+from .scheduler import SchedulerMode
+
+DEFAULT_MAX_SUPERSTEPS = 10_000
+
+
+class CommMode(Enum):
+    PUSH = "push"
+    PULL = "pull"
+
+
+@dataclass(frozen=True)
+class VertexProgram:
+    """engine.py:59-81.  ``compute`` must carry a device lowering."""
+
+    compute: Callable[["VertexContext"], None]
+    comm_mode: CommMode
+    message_dtype: Any
+    state_dtype: Any
+    combine: CombineFn | None = None
+    setup: Callable | None = None
+    on_superstep_end: Callable | None = None
+    extract: Callable | None = None
+    track_active: bool = True
+    name: str = ""
+
+
+@dataclass(frozen=True)
+class EngineConfig:
+    """engine.py:84-91.  ``workers``/``scheduler``/``layout``/``combiner``/
+    ``validate_phases`` are validated and inert on the device; ``device``
+    selects the CUDA device (default: the current one)."""
+
+    workers: int = 1
+    scheduler: SchedulerMode = field(default_factory=SchedulerMode.static)
+    layout: LayoutMode = LayoutMode.INTERLEAVED
+    combiner: CombinerKind = CombinerKind.HYBRID
+    max_supersteps: int = DEFAULT_MAX_SUPERSTEPS
+    validate_phases: bool = False
+    device: int | None = None
+
+
+@dataclass(frozen=True)
+class SuperstepStats:
+    """engine.py:94-99 plus the device counters behind GTEPS / bytes."""
+
+    index: int
+    active_count: int
+    messages_sent: int
+    seconds: float
+    edges: int = 0          # edges traversed by this superstep's senders
+    senders: int = 0        # senders with out-degree > 0 (#F_s)
+    recipients: int = 0     # distinct recipients of its messages (R_s)
+    broadcasters: int = 0   # vertices that sent (out-degree 0 included)
+
+
+@dataclass(frozen=True)
+class RunReport:
+    """engine.py:102-108 plus the device view of the result."""
+
+    values: np.ndarray
+    superstep_count: int
+    supersteps: list
+    wall_seconds: float
+    hit_superstep_cap: bool
+    device_values: Any = None      # torch tensor on the device (u32 / f64)
+    device_seconds: float = 0.0    # kernel time from the device timer
+    ctas: int = 0                  # persistent CTAs of the run kernel
+
+
+class VertexContext:
+    """Present for API compatibility (engine.py:115-194).  Device programs
+    never see a Python context: computes run inside the kernel."""
+
+    def __init__(self, *args, **kwargs):
+        raise ConfigError("VertexContext exists only inside device kernels; "
+                          "use pagerank / connected_components / sssp")
+
+
+# ----------------------------------------------------------------------
+# lowering
+# ----------------------------------------------------------------------
+
+LOWERING_ATTR = "_pgx_lowering"
+
+
+def lowering_of(program: VertexProgram) -> dict:
+    """Return the device lowering of ``program`` or raise ConfigError."""
+    low = getattr(program.compute, LOWERING_ATTR, None)
+    if low is None:
+        raise ConfigError(
+            f"program {program.name or program.compute!r} has no device lowering: "
+            f"the B200 engine runs pagerank / connected_components / sssp "
+            f"(there is no CPU fallback for Python compute callbacks)")
+    for attr in ("setup", "on_superstep_end", "combine"):
+        if getattr(program, attr) is not low["parts"][attr]:
+            raise ConfigError(
+                f"{low['app']}: a replaced `{attr}` cannot be lowered to the device")
+    if program.comm_mode is not low["parts"]["comm_mode"] or \
+            program.track_active != low["parts"]["track_active"]:
+        raise ConfigError(f"{low['app']}: comm_mode/track_active were changed")
+    return low
+
+
+def _validate(program: VertexProgram, config: EngineConfig) -> None:
+    """engine.py:477-490."""
+    if config.workers < 1:
+        raise ConfigError(f"worker count must be >= 1, got {config.workers}")
+    if config.max_supersteps < 1:
+        raise ConfigError(f"superstep cap must be >= 1, got {config.max_supersteps}")
+    if config.max_supersteps > 2 ** 31 - 2:
+        raise ConfigError("superstep cap must fit in int32")
+    if not isinstance(config.scheduler, SchedulerMode):
+        raise ConfigError(f"bad scheduler mode: {config.scheduler!r}")
+    if not isinstance(config.layout, LayoutMode):
+        raise ConfigError(f"bad layout mode: {config.layout!r}")
+    if not isinstance(config.combiner, CombinerKind):
+        raise ConfigError(f"bad combiner kind: {config.combiner!r}")
+    if program.comm_mode is CommMode.PUSH and program.combine is None:
+        raise ConfigError("push-mode programs must declare a combine function")
+    if config.combiner is CombinerKind.CAS and program.comm_mode is CommMode.PUSH \
+            and (program.combine is None or program.combine.neutral is None):
+        raise ConfigError("the CAS combiner strategy needs a combine function "
+                          "with a neutral element to pre-fill slots with")
+
+
+# ----------------------------------------------------------------------
+# run
+# ----------------------------------------------------------------------
+
+def run(graph: Graph, program: VertexProgram,
+        config: EngineConfig | None = None) -> RunReport:
+    """Execute ``program`` on ``graph`` until quiescence or the cap."""
+    config = config or EngineConfig()
+    _validate(program, config)
+    low = lowering_of(program)
+    app = low["app"]
+    n = graph.vertex_count
+    if app == "sssp" and not 0 <= low["source"] < n:
+        raise ConfigError(f"source vertex {low['source']} out of range [0, {n})")
+    if n == 0:
+        return _empty_run(program, low)
+    if not torch.cuda.is_available():
+        raise ExecutionError("no CUDA device: the B200 engine has no CPU fallback")
+    from .distributed import distributed_context  # multi-GPU under torchrun
+    ctx = distributed_context()
+    if ctx is not None:
+        from .distributed import run_partitioned
+        return run_partitioned(graph, program, low, config, ctx)
+    return _run_device(graph, program, low, config)
+
+
+def _empty_run(program, low) -> RunReport:
+    """An empty graph runs one empty superstep (engine.py:271-296)."""
+    dtype = {"pagerank": np.float64, "components": np.int64,
+             "sssp": np.uint32}[low["app"]]
+    values = np.empty(0, dtype=dtype)
+    stats = [SuperstepStats(0, 0, 0, 0.0)]
+    if program.extract is not None:
+        values = program.extract(SimpleNamespace(state=values,
+                                                 halted=np.ones(0, bool)))
+    return RunReport(values, 1, stats, 0.0, False)
+
+
+@dataclass
+class LaunchPlan:
+    """Everything one device run needs, allocated up front (re-usable)."""
+
+    app: str
+    csr: Any
+    values: torch.Tensor
+    stats: torch.Tensor
+    ws: torch.Tensor
+    ws_bytes: int
+    max_steps: int
+    low: dict
+    stream: Any
+
+    def launch(self) -> None:
+        """Enqueue the persistent run kernel (asynchronous)."""
+        lib = _lib.load()
+        c = self.csr
+        sp = self.stream.cuda_stream
+        if self.app == "pagerank":
+            it, d = self.low["iterations"], self.low["damping"]
+            base = (1.0 - d) / c.n      # algorithms.py:49 (host float math)
+            r0 = 1.0 / c.n              # algorithms.py:50
+            rc = lib.pgx_pagerank_run(c.n, c.m, c.row_ptr.data_ptr(),
+                                      c.col_idx.data_ptr(), c.ws.data_ptr(),
+                                      it, d, base, r0, self.max_steps,
+                                      self.values.data_ptr(), self.ws.data_ptr(),
+                                      self.ws_bytes, self.stats.data_ptr(), sp)
+            _lib.check(rc, "pgx_pagerank_run")
+        elif self.app == "components":
+            rc = lib.pgx_cc_run(c.n, c.m, c.row_ptr.data_ptr(), c.col_idx.data_ptr(),
+                                c.ws.data_ptr(), self.max_steps,
+                                self.values.data_ptr(), self.ws.data_ptr(),
+                                self.ws_bytes, self.stats.data_ptr(), sp)
+            _lib.check(rc, "pgx_cc_run")
+        else:
+            rc = lib.pgx_sssp_run(c.n, c.m, c.row_ptr.data_ptr(), c.col_idx.data_ptr(),
+                                  c.ws.data_ptr(), self.low["source"], self.max_steps,
+                                  self.values.data_ptr(), self.ws.data_ptr(),
+                                  self.ws_bytes, self.stats.data_ptr(), sp)
+            _lib.check(rc, "pgx_sssp_run")
+
+
+_APP_ID = {"pagerank": _lib.PGX_APP_PAGERANK, "components": _lib.PGX_APP_CC,
+           "sssp": _lib.PGX_APP_SSSP}
+
+
+def plan_run(graph: Graph, program: VertexProgram,
+             config: EngineConfig | None = None, device=None) -> LaunchPlan:
+    """Upload/prepare the graph and allocate a run's buffers (no launch)."""
+    config = config or EngineConfig()
+    _validate(program, config)
+    low = lowering_of(program)
+    dev = torch.device("cuda", torch.cuda.current_device() if device is None
+                       and config.device is None else
+                       (device if device is not None else config.device))
+    stream = torch.cuda.current_stream(dev)
+    csr = graph.device_csr(dev, stream)
+    n, m = csr.n, csr.m
+    lib = _lib.load()
+    app = low["app"]
+    max_steps = int(config.max_supersteps)
+    if app == "pagerank":
+        max_steps = min(max_steps, int(low["iterations"]))
+    ws_bytes = _lib.out_size(lib.pgx_run_workspace_bytes, _APP_ID[app], n, m, max_steps)
+    with torch.cuda.device(dev):
+        ws = torch.empty(ws_bytes, dtype=torch.uint8, device=dev)
+        stats = torch.zeros(_lib.PGX_STAT_HDR + _lib.PGX_STAT_FIELDS * max_steps,
+                            dtype=torch.int64, device=dev)
+        vdt = torch.float64 if app == "pagerank" else torch.int32
+        values = torch.empty(n, dtype=vdt, device=dev)
+    return LaunchPlan(app, csr, values, stats, ws, ws_bytes, max_steps, low, stream)
+
+
+def collect(plan: LaunchPlan, program: VertexProgram, wall: float | None = None) -> RunReport:
+    """Read the device statistics and values back into a RunReport."""
+    hdr = plan.stats[:_lib.PGX_STAT_HDR].cpu().tolist()
+    k, hit_cap, ctas, t0 = int(hdr[0]), bool(hdr[1]), int(hdr[2]), int(hdr[3])
+    if k < 1:
+        raise ExecutionError("device run did not report a superstep count")
+    rows = plan.stats[_lib.PGX_STAT_HDR:_lib.PGX_STAT_HDR + k * _lib.PGX_STAT_FIELDS]
+    rows = rows.view(k, _lib.PGX_STAT_FIELDS).cpu().numpy()
+    steps = []
+    prev = t0
+    for s in range(k):
+        a, sent, e, f, r, t, bc = (int(x) for x in rows[s, :7])
+        steps.append(SuperstepStats(s, a, sent, max(t - prev, 0) * 1e-9, e, f, r, bc))
+        prev = t
+    dev_seconds = max(int(rows[k - 1, 5]) - t0, 0) * 1e-9
+    app = plan.app
+    dv = plan.values
+    if app == "pagerank":
+        values = dv.cpu().numpy()
+    elif app == "components":
+        values = dv.to(torch.int64).cpu().numpy()       # algorithms.py:111 int64
+    else:
+        values = dv.cpu().numpy().view(np.uint32)        # algorithms.py:150 uint32
+    if program.extract is not None:
+        values = program.extract(SimpleNamespace(state=values,
+                                                 halted=np.ones(values.shape[0], bool)))
+    return RunReport(values, k, steps, dev_seconds if wall is None else wall, hit_cap,
+                     device_values=dv, device_seconds=dev_seconds, ctas=ctas)
+
+
+def _run_device(graph, program, low, config) -> RunReport:
+    plan = plan_run(graph, program, config)
+    t = time.perf_counter()
+    plan.launch()
+    plan.stream.synchronize()
+    wall = time.perf_counter() - t
+    return collect(plan, program, wall)

@@ -1,0 +1,422 @@
+"""CSR graph container with PyTorch tensors (reference: graph.py).
+
+Same contract as the reference ``Graph`` (graph.py:39-106): a directed
+multigraph in CSR form with each row's targets sorted ascending, duplicate
+edges and self-loops kept verbatim, ``undirected=True`` storing every input
+edge in both directions (graph.py:141-187).  Differences are placement
+only:
+
+* arrays are ``torch`` tensors (CPU or CUDA); offsets int64 like the
+  reference (graph.py:28), targets of the id dtype (int32 by default);
+* the in-CSR (transpose) is built lazily on first use -- the push superstep
+  never needs it;
+* ``device_csr()`` returns the device-resident form the B200 engine walks:
+  int32 ``row_ptr``/``col_idx`` plus the per-graph tile map built by
+  ``pgx_graph_prepare`` -- cached per device, so a graph already in HBM is
+  never re-uploaded.
+
+Ingestion (``load_edge_list``) and the binary cache are kept host-side and
+byte-compatible with the reference (``PGLCSR1`` format, graph.py:298-373).
+"""
+
+from __future__ import annotations
+
+import io
+import os
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+
+from . import _lib
+from .errors import GraphLoadError
+
+_CACHE_MAGIC = b"PGLCSR1\n"
+
+
+def _as_tensor(a, dtype=torch.int64, device=None) -> torch.Tensor:
+    if isinstance(a, torch.Tensor):
+        t = a.to(dtype)
+    else:
+        t = torch.as_tensor(np.asarray(a), dtype=dtype)
+    if device is not None:
+        t = t.to(device)
+    return t.reshape(-1).contiguous()
+
+
+@dataclass
+class DeviceCSR:
+    """Device-resident CSR the engine walks (int32, n < 2^31, m < 2^31)."""
+
+    n: int
+    m: int
+    row_ptr: torch.Tensor   # int32 [n+1]
+    col_idx: torch.Tensor   # int32 [m]
+    ws: torch.Tensor        # uint8 per-graph workspace (tile map, nz list)
+    h2d_bytes: int          # bytes copied host->device to build it
+
+
+class Graph:
+    """A directed multigraph in CSR form, with its (lazy) transpose."""
+
+    def __init__(self, vertex_count: int, out_offsets: torch.Tensor,
+                 out_targets: torch.Tensor, in_offsets: torch.Tensor | None = None,
+                 in_targets: torch.Tensor | None = None, id_map=None,
+                 source_path: str | None = None):
+        self.vertex_count = int(vertex_count)
+        self.out_offsets = out_offsets
+        self.out_targets = out_targets
+        self._in = None if in_offsets is None else (in_offsets, in_targets)
+        self.id_map = id_map
+        self.source_path = source_path
+        self._device: dict = {}
+
+    # ---- reference surface (graph.py:56-106) --------------------------
+
+    @property
+    def edge_count(self) -> int:
+        return int(self.out_targets.shape[0])
+
+    @property
+    def id_dtype(self):
+        return self.out_targets.dtype
+
+    @property
+    def in_offsets(self) -> torch.Tensor:
+        return self._transpose()[0]
+
+    @property
+    def in_targets(self) -> torch.Tensor:
+        return self._transpose()[1]
+
+    def _transpose(self):
+        if self._in is None:
+            self._in = _csr(self.out_targets.to(torch.int64),
+                            _expand_sources(self.out_offsets, self.edge_count),
+                            self.vertex_count, self.out_targets.dtype)
+        return self._in
+
+    def out_neighbors(self, v: int) -> torch.Tensor:
+        self._check_vertex(v)
+        return self.out_targets[int(self.out_offsets[v]):int(self.out_offsets[v + 1])]
+
+    def in_neighbors(self, v: int) -> torch.Tensor:
+        self._check_vertex(v)
+        return self.in_targets[int(self.in_offsets[v]):int(self.in_offsets[v + 1])]
+
+    def out_degree(self, v: int) -> int:
+        self._check_vertex(v)
+        return int(self.out_offsets[v + 1] - self.out_offsets[v])
+
+    def in_degree(self, v: int) -> int:
+        self._check_vertex(v)
+        return int(self.in_offsets[v + 1] - self.in_offsets[v])
+
+    @property
+    def out_degrees(self) -> torch.Tensor:
+        return torch.diff(self.out_offsets)
+
+    @property
+    def in_degrees(self) -> torch.Tensor:
+        return torch.diff(self.in_offsets)
+
+    def original_ids(self, dense):
+        if self.id_map is None:
+            return np.asarray(dense)
+        return np.asarray(self.id_map)[np.asarray(dense)]
+
+    def _check_vertex(self, v: int) -> None:
+        if not 0 <= v < self.vertex_count:
+            raise IndexError(f"vertex id {v} out of range [0, {self.vertex_count})")
+
+    def __repr__(self) -> str:
+        return (f"Graph(vertex_count={self.vertex_count}, "
+                f"edge_count={self.edge_count}, id_dtype={self.id_dtype})")
+
+    # ---- placement ----------------------------------------------------
+
+    @property
+    def device(self) -> torch.device:
+        return self.out_targets.device
+
+    def pin_memory(self) -> "Graph":
+        """Host graph with page-locked CSR (fast, async H2D)."""
+        g = Graph(self.vertex_count, self.out_offsets.cpu().pin_memory(),
+                  self.out_targets.cpu().pin_memory(), id_map=self.id_map,
+                  source_path=self.source_path)
+        return g
+
+    def drop_device_cache(self) -> None:
+        self._device.clear()
+
+    def device_csr(self, device=None, stream=None) -> DeviceCSR:
+        """The int32 device CSR + tile map, built once per device."""
+        dev = torch.device("cuda", torch.cuda.current_device()) if device is None \
+            else torch.device(device)
+        key = dev.index
+        hit = self._device.get(key)
+        if hit is not None:
+            return hit
+        n, m = self.vertex_count, self.edge_count
+        if n >= 2 ** 31 - 1 or m >= 2 ** 31:
+            raise GraphLoadError("device CSR needs n < 2^31 and m < 2^31 (int32)")
+        lib = _lib.load()
+        st = torch.cuda.current_stream(dev) if stream is None else stream
+        h2d = 0
+        with torch.cuda.device(dev), torch.cuda.stream(st):
+            off = self.out_offsets
+            if off.device != dev:
+                h2d += off.numel() * off.element_size()
+                off = off.to(dev, non_blocking=True)
+            tgt = self.out_targets
+            if tgt.device != dev:
+                h2d += tgt.numel() * tgt.element_size()
+                tgt = tgt.to(dev, non_blocking=True)
+            col = tgt if tgt.dtype == torch.int32 else tgt.to(torch.int32)
+            row_ptr = torch.empty(n + 1, dtype=torch.int32, device=dev)
+            _lib.check(lib.pgx_offsets_to_i32(off.to(torch.int64).data_ptr(),
+                                              row_ptr.data_ptr(), n + 1,
+                                              st.cuda_stream), "pgx_offsets_to_i32")
+            ws_bytes = _lib.out_size(lib.pgx_graph_workspace_bytes, n, m)
+            ws = torch.empty(ws_bytes, dtype=torch.uint8, device=dev)
+            if n > 0:
+                _lib.check(lib.pgx_graph_prepare(n, m, row_ptr.data_ptr(),
+                                                 ws.data_ptr(), ws_bytes,
+                                                 st.cuda_stream),
+                           "pgx_graph_prepare")
+        d = DeviceCSR(n, m, row_ptr, col, ws, h2d)
+        self._device[key] = d
+        return d
+
+
+@dataclass(frozen=True)
+class DegreeStats:
+    """graph.py:109-123: degree summary used by the edge-balanced split."""
+
+    degrees: torch.Tensor
+    prefix: torch.Tensor
+    min_degree: int
+    max_degree: int
+    mean_degree: float
+
+
+def degree_prefix_sums(graph: Graph, *, incoming: bool = False) -> DegreeStats:
+    degrees = graph.in_degrees if incoming else graph.out_degrees
+    prefix = torch.cumsum(degrees, 0, dtype=torch.int64)
+    if degrees.numel() == 0:
+        return DegreeStats(degrees, prefix, 0, 0, 0.0)
+    return DegreeStats(degrees, prefix, int(degrees.min()), int(degrees.max()),
+                       float(degrees.double().mean()))
+
+
+# ----------------------------------------------------------------------
+# construction
+# ----------------------------------------------------------------------
+
+def _expand_sources(offsets: torch.Tensor, m: int) -> torch.Tensor:
+    n = offsets.numel() - 1
+    deg = torch.diff(offsets)
+    return torch.repeat_interleave(torch.arange(n, dtype=torch.int64,
+                                                device=offsets.device), deg,
+                                   output_size=m)
+
+
+def _csr(key: torch.Tensor, val: torch.Tensor, n: int, id_dtype):
+    """graph.py:179-187: group by key, targets ascending within a row."""
+    dev = key.device
+    offsets = torch.zeros(n + 1, dtype=torch.int64, device=dev)
+    if key.numel():
+        offsets[1:] = torch.cumsum(torch.bincount(key, minlength=n), 0)
+        order = torch.argsort(key * max(n, 1) + val)
+        targets = val[order].to(id_dtype)
+    else:
+        targets = torch.empty(0, dtype=id_dtype, device=dev)
+    return offsets, targets
+
+
+def from_edges(src, dst, vertex_count: int, *, undirected: bool = False,
+               id_dtype=np.int32, device=None) -> Graph:
+    """Build a graph from parallel dense-id edge arrays (graph.py:141-176).
+
+    Every id must be in ``[0, vertex_count)``.  Duplicate edges and
+    self-loops are kept; with ``undirected=True`` each input edge (self-loops
+    included) is stored in both directions.  ``device`` places the CSR
+    (default: where ``src`` lives).
+    """
+    dev = device
+    if dev is None and isinstance(src, torch.Tensor):
+        dev = src.device
+    src = _as_tensor(src, torch.int64, dev)
+    dst = _as_tensor(dst, torch.int64, dev)
+    if src.shape != dst.shape:
+        raise GraphLoadError("src/dst must be 1-d arrays of equal length")
+    if vertex_count < 0:
+        raise GraphLoadError(f"vertex_count must be >= 0, got {vertex_count}")
+    np_id = np.dtype(id_dtype)
+    if not np.issubdtype(np_id, np.integer):
+        raise GraphLoadError(f"id dtype must be an integer type, got {np_id}")
+    if vertex_count > 0 and vertex_count - 1 > np.iinfo(np_id).max:
+        raise GraphLoadError(
+            f"vertex count {vertex_count} does not fit id dtype {np_id}")
+    tdt = {np.dtype(np.int32): torch.int32, np.dtype(np.int64): torch.int64,
+           np.dtype(np.int16): torch.int16}.get(np_id)
+    if tdt is None:
+        raise GraphLoadError(f"unsupported id dtype {np_id}")
+    if src.numel():
+        lo = int(torch.minimum(src.min(), dst.min()))
+        hi = int(torch.maximum(src.max(), dst.max()))
+        if lo < 0 or hi >= vertex_count:
+            raise GraphLoadError(
+                f"edge endpoint {lo if lo < 0 else hi} outside [0, {vertex_count})")
+    if undirected and src.numel():
+        src, dst = torch.cat([src, dst]), torch.cat([dst, src])
+    out_offsets, out_targets = _csr(src, dst, vertex_count, tdt)
+    return Graph(vertex_count, out_offsets, out_targets)
+
+
+def from_csr(offsets, targets, vertex_count: int | None = None) -> Graph:
+    """Wrap an existing row-sorted CSR (e.g. a generator's output)."""
+    off = _as_tensor(offsets, torch.int64)
+    tgt = targets if isinstance(targets, torch.Tensor) else \
+        torch.as_tensor(np.asarray(targets))
+    n = off.numel() - 1 if vertex_count is None else int(vertex_count)
+    if off.numel() != n + 1:
+        raise GraphLoadError("offsets must have vertex_count + 1 entries")
+    return Graph(n, off, tgt.reshape(-1).contiguous())
+
+
+def gather_adjacency(offsets, targets, ids):
+    """graph.py:380-397: concatenated adjacency slices of ``ids``."""
+    offsets = _as_tensor(offsets, torch.int64)
+    ids = _as_tensor(ids, torch.int64, offsets.device)
+    targets = targets if isinstance(targets, torch.Tensor) else torch.as_tensor(targets)
+    starts = offsets[ids]
+    lengths = offsets[ids + 1] - starts
+    total = int(lengths.sum()) if lengths.numel() else 0
+    if total == 0:
+        return targets[:0], lengths
+    row_ends = torch.cumsum(lengths, 0)
+    flat = torch.arange(total, dtype=torch.int64, device=offsets.device)
+    flat += torch.repeat_interleave(starts - (row_ends - lengths), lengths)
+    return targets[flat], lengths
+
+
+def densify_ids(src, dst):
+    """graph.py:196-211: raw ids -> 0..n-1 in first-appearance order."""
+    src = np.asarray(src, dtype=np.int64)
+    dst = np.asarray(dst, dtype=np.int64)
+    raw = np.empty(src.size * 2, dtype=np.int64)
+    raw[0::2] = src
+    raw[1::2] = dst
+    sorted_ids, first_pos, inverse = np.unique(raw, return_index=True,
+                                               return_inverse=True)
+    appearance = np.argsort(first_pos, kind="stable")
+    rank = np.empty(appearance.size, dtype=np.int64)
+    rank[appearance] = np.arange(appearance.size)
+    dense = rank[inverse]
+    return dense[0::2], dense[1::2], sorted_ids[appearance]
+
+
+def load_edge_list(path, *, undirected: bool = False, id_dtype=np.int32) -> Graph:
+    """Whitespace edge list -> Graph (graph.py:218-291; host-side ingestion)."""
+    path = os.fspath(path)
+    src, dst = [], []
+    try:
+        fh = open(path, "rt", encoding="utf-8", errors="replace")
+    except OSError as e:
+        raise GraphLoadError(f"{path}: {e.strerror}") from e
+    with fh:
+        for lineno, line in enumerate(fh, 1):
+            s = line.strip()
+            if not s or s.startswith("#"):
+                continue
+            tok = s.split()
+            if len(tok) < 2:
+                raise GraphLoadError(f"{path}:{lineno}: expected at least two "
+                                     f"vertex ids, got {len(tok)} token(s)")
+            try:
+                a, b = int(tok[0]), int(tok[1])
+            except ValueError:
+                raise GraphLoadError(f"{path}:{lineno}: non-integer vertex id "
+                                     f"{tok[0]!r} {tok[1]!r}") from None
+            if a < 0 or b < 0:
+                raise GraphLoadError(f"{path}:{lineno}: negative vertex id")
+            src.append(a)
+            dst.append(b)
+    if not src:
+        g = from_edges(np.empty(0, np.int64), np.empty(0, np.int64), 0,
+                       id_dtype=id_dtype)
+    else:
+        s, d, id_map = densify_ids(np.asarray(src), np.asarray(dst))
+        g = from_edges(s, d, int(id_map.size), undirected=undirected,
+                       id_dtype=id_dtype)
+        g.id_map = id_map
+    g.source_path = path
+    return g
+
+
+def save_cache(graph: Graph, path) -> None:
+    """graph.py:298-322: little-endian PGLCSR1 snapshot."""
+    tgt = graph.out_targets.cpu().numpy()
+    id_dt = tgt.dtype.newbyteorder("<")
+    header = io.BytesIO()
+    header.write(_CACHE_MAGIC)
+    header.write(id_dt.str.encode("ascii").ljust(8, b"\x00"))
+    header.write(np.asarray([graph.vertex_count, graph.edge_count], "<u8").tobytes())
+    header.write(bytes([1 if graph.id_map is not None else 0]) + b"\x00" * 7)
+    tmp = os.fspath(path) + ".tmp"
+    with open(tmp, "wb") as fh:
+        fh.write(header.getvalue())
+        fh.write(np.ascontiguousarray(graph.out_offsets.cpu().numpy(), "<i8").tobytes())
+        fh.write(np.ascontiguousarray(tgt, id_dt).tobytes())
+        fh.write(np.ascontiguousarray(graph.in_offsets.cpu().numpy(), "<i8").tobytes())
+        fh.write(np.ascontiguousarray(graph.in_targets.cpu().numpy(), id_dt).tobytes())
+        if graph.id_map is not None:
+            fh.write(np.ascontiguousarray(graph.id_map, "<i8").tobytes())
+    os.replace(tmp, path)
+
+
+def load_cache(path) -> Graph:
+    """graph.py:325-373: read and validate a PGLCSR1 snapshot."""
+    path = os.fspath(path)
+    try:
+        with open(path, "rb") as fh:
+            blob = fh.read()
+    except OSError as e:
+        raise GraphLoadError(f"{path}: {e.strerror}") from e
+    if len(blob) < 40 or blob[:8] != _CACHE_MAGIC:
+        raise GraphLoadError(f"{path}: not a graph cache (bad magic/version)")
+    try:
+        id_dt = np.dtype(blob[8:16].rstrip(b"\x00").decode("ascii"))
+    except (TypeError, UnicodeDecodeError) as e:
+        raise GraphLoadError(f"{path}: unreadable id dtype tag") from e
+    n, m = (int(x) for x in np.frombuffer(blob[16:32], dtype="<u8"))
+    has_id_map = blob[32] == 1
+    pos = 40
+
+    def take(count, dtype):
+        nonlocal pos
+        nbytes = count * dtype.itemsize
+        if pos + nbytes > len(blob):
+            raise GraphLoadError(f"{path}: truncated graph cache")
+        arr = np.frombuffer(blob, dtype=dtype, count=count, offset=pos).copy()
+        pos += nbytes
+        return arr
+
+    out_off = take(n + 1, np.dtype("<i8"))
+    out_tgt = take(m, id_dt)
+    in_off = take(n + 1, np.dtype("<i8"))
+    in_tgt = take(m, id_dt)
+    id_map = take(n, np.dtype("<i8")) if has_id_map else None
+    if pos != len(blob):
+        raise GraphLoadError(f"{path}: trailing bytes in graph cache")
+    for offs in (out_off, in_off):
+        if offs[0] != 0 or offs[-1] != m or np.any(np.diff(offs) < 0):
+            raise GraphLoadError(f"{path}: corrupt offsets in graph cache")
+    if m and (out_tgt.max() >= n or in_tgt.max() >= n
+              or out_tgt.min() < 0 or in_tgt.min() < 0):
+        raise GraphLoadError(f"{path}: target id out of range in graph cache")
+    g = Graph(n, torch.from_numpy(out_off), torch.from_numpy(out_tgt.astype(id_dt.newbyteorder("="))),
+              torch.from_numpy(in_off), torch.from_numpy(in_tgt.astype(id_dt.newbyteorder("="))),
+              id_map=id_map, source_path=path)
+    return g

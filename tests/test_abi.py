@@ -1,0 +1,67 @@
+"""The C ABI library loads and exports every symbol include/pgx.h declares
+(no compute calls: CPU container), and the product path refuses to run
+without a CUDA device (no CPU fallback)."""
+
+import ctypes
+import os
+import re
+import subprocess
+
+import numpy as np
+import pytest
+
+import paper_2010_01542_b200 as pgx
+from paper_2010_01542_b200 import _lib
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+HEADER = os.path.join(ROOT, "include", "pgx.h")
+
+
+def declared_symbols():
+    text = open(HEADER).read()
+    return sorted(set(re.findall(r"\b(pgx_[a-z0-9_]+)\s*\(", text)))
+
+
+def test_header_declares_exactly_the_bound_symbols():
+    assert declared_symbols() == sorted(_lib.EXPORTS)
+
+
+def test_library_exports_every_declared_symbol():
+    lib = _lib.load()
+    out = subprocess.run(["nm", "-D", "--defined-only", _lib.LIB_PATH],
+                         capture_output=True, text=True, check=True).stdout
+    exported = set(re.findall(r" T (pgx_\w+)", out))
+    for sym in declared_symbols():
+        assert sym in exported, sym
+        assert getattr(lib, sym) is not None
+    assert lib.pgx_abi_version() == _lib.PGX_ABI_VERSION
+
+
+def test_library_is_sm100a_only():
+    out = subprocess.run(["/usr/local/cuda/bin/cuobjdump", "--list-elf", _lib.LIB_PATH],
+                         capture_output=True, text=True).stdout
+    assert "sm_100a" in out
+
+
+def test_host_side_size_queries_and_error_codes():
+    lib = _lib.load()
+    v = ctypes.c_size_t(0)
+    assert lib.pgx_graph_workspace_bytes(1 << 22, 65_000_000, ctypes.byref(v)) == 0
+    assert v.value > (1 << 22) * 8
+    for app in (0, 1, 2):
+        assert lib.pgx_run_workspace_bytes(app, 1000, 5000, 16, ctypes.byref(v)) == 0
+        assert v.value > 1000 * 4
+    assert lib.pgx_run_workspace_bytes(7, 10, 10, 1, ctypes.byref(v)) == _lib.PGX_EINVAL
+    assert b"bad run workspace" in lib.pgx_last_error()
+    with pytest.raises(pgx.ConfigError):
+        _lib.check(_lib.PGX_EINVAL, "probe")
+    with pytest.raises(pgx.ExecutionError):
+        _lib.check(_lib.PGX_ECUDA, "probe")
+
+
+@pytest.mark.skipif(__import__("torch").cuda.is_available(), reason="CPU-only check")
+def test_no_cpu_fallback():
+    g = pgx.from_edges([0, 1], [1, 2], 3)
+    for prog in (pgx.pagerank(), pgx.connected_components(), pgx.sssp(0)):
+        with pytest.raises(pgx.ExecutionError):
+            pgx.run(g, prog)
