@@ -260,6 +260,32 @@ struct ScatterArgs {
   unsigned *recip_count;
 };
 
+constexpr int kWarps = kBlock / 32;
+constexpr int kWarpEdges = kTile / kWarps;  // 256 = kItems rounds of 32
+
+// shared-memory footprint of the scatter: source slots + publish queue
+__host__ __device__ constexpr size_t scatter_smem(int op) {
+  return (size_t)kSlots * (sizeof(int32_t) * 2 + (op == PGX_OP_SUM_F64 ? 8 : 4)) +
+         (op == PGX_OP_MIN_U32 ? sizeof(int32_t) * kTile : 0) + 16;
+}
+
+// Edge -> source mapping, one warp per 32 consecutive edges: lane j holds
+// the start of candidate source cur+1+j; the OR-reduction of the
+// in-window boundary bits gives every lane its source with one popc.
+// Sources have >= 1 edge, so at most 32 boundaries fall in a window.
+__device__ __forceinline__ int warp_find_first(const int32_t *s_eb, int k, int64_t e) {
+  int lo = 0, hi = k;  // s_eb[lo] <= e < s_eb[hi]
+  while (hi - lo > 1) {
+    const int step = (hi - lo + 31) >> 5;
+    const int p = lo + (int)lane_id() * step;
+    const bool le = (p < hi) && ((int64_t)s_eb[p] <= e);
+    const unsigned b = __ballot_sync(0xFFFFFFFFu, le);
+    lo += (31 - __clz(b)) * step;
+    hi = min(hi, lo + step);
+  }
+  return lo;
+}
+
 template <int OP, MsgSrc MS>
 __device__ void scatter_phase(const ScatterArgs &a, char *smem) {
   using Msg = typename std::conditional<OP == PGX_OP_SUM_F64, double, uint32_t>::type;
@@ -267,8 +293,13 @@ __device__ void scatter_phase(const ScatterArgs &a, char *smem) {
   int32_t *s_eb = reinterpret_cast<int32_t *>(smem);
   int32_t *s_rs = s_eb + kSlots;
   Msg *s_msg = reinterpret_cast<Msg *>(s_rs + kSlots);
+  int32_t *s_q = reinterpret_cast<int32_t *>(s_msg + kSlots);  // publish queue
+  __shared__ unsigned s_qn, s_qbase;
   const uint64_t pol = evict_first_policy();
   const int64_t ntiles = (a.E + kTile - 1) / kTile;
+  const int lane = (int)lane_id();
+  const int warp = threadIdx.x >> 5;
+  const unsigned upto = (lane == 31) ? 0xFFFFFFFFu : ((2u << lane) - 1u);
 
   for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
     const int64_t e0 = t * kTile;
@@ -292,45 +323,76 @@ __device__ void scatter_phase(const ScatterArgs &a, char *smem) {
         s_eb[j] = (i < a.nsrc) ? a.eb[i] : (int32_t)a.E;  // sentinel
       }
     }
+    if (threadIdx.x == 0) s_qn = 0;
     __syncthreads();
 
+    const int64_t we0 = e0 + (int64_t)warp * kWarpEdges;
+    const int64_t we1 = min(e1, we0 + kWarpEdges);
     int w[kItems];
     Msg mv[kItems];
-    int lo = 0;
 #pragma unroll
-    for (int j = 0; j < kItems; j++) {
-      const int64_t e = e0 + (int64_t)j * kBlock + threadIdx.x;
-      w[j] = -1;
-      if (e < e1) {
-        int hi = k;  // invariant: s_eb[lo] <= e < s_eb[hi]
-        while (hi - lo > 1) {
-          const int mid = (lo + hi) >> 1;
-          if (s_eb[mid] <= e) lo = mid; else hi = mid;
+    for (int r = 0; r < kItems; r++) w[r] = -1;
+    if (we0 < e1) {  // warp-uniform
+      int cur = warp_find_first(s_eb, k, we0);
+#pragma unroll
+      for (int r = 0; r < kItems; r++) {
+        const int64_t base = we0 + r * 32;
+        const int64_t e = base + lane;
+        const int ci = cur + 1 + lane;
+        unsigned bit = 0;
+        if (ci <= k) {
+          const int64_t pp = (int64_t)s_eb[ci] - base;
+          if (pp >= 0 && pp < 32) bit = 1u << pp;
         }
-        const int64_t pos = kDense ? e : (int64_t)s_rs[lo] + (e - s_eb[lo]);
-        w[j] = ld_stream(a.col + pos, pol);
-        mv[j] = s_msg[lo];
+        const unsigned bm = __reduce_or_sync(0xFFFFFFFFu, bit);
+        const int src = cur + __popc(bm & upto);
+        cur += __popc(bm);
+        if (e < we1) {
+          const int64_t pos = kDense ? e : (int64_t)s_rs[src] + (e - s_eb[src]);
+          w[r] = ld_stream(a.col + pos, pol);
+          mv[r] = s_msg[src];
+        }
       }
     }
     if (OP == PGX_OP_MIN_U32) {
+      // hybrid combiner: read-filter (mailbox.py:159 short-circuit), then
+      // one atomicMin; the unique lane that sees NEUTRAL come back is the
+      // first publisher (mailbox.py:190-199) and queues the recipient.
       uint32_t *mb = reinterpret_cast<uint32_t *>(a.mailbox);
-      uint32_t cur[kItems];
+      uint32_t old[kItems];
 #pragma unroll
-      for (int j = 0; j < kItems; j++) cur[j] = (w[j] >= 0) ? mb[w[j]] : 0u;
+      for (int r = 0; r < kItems; r++) old[r] = (w[r] >= 0) ? mb[w[r]] : 0u;
 #pragma unroll
-      for (int j = 0; j < kItems; j++) {
-        bool pub = false;
-        if (w[j] >= 0 && (uint32_t)mv[j] < cur[j]) {
-          const uint32_t old = atomicMin(mb + w[j], (uint32_t)mv[j]);
-          pub = (old == kNeutralMin);
+      for (int r = 0; r < kItems; r++) {
+        if (w[r] >= 0 && (uint32_t)mv[r] < old[r])
+          old[r] = atomicMin(mb + w[r], (uint32_t)mv[r]);
+        else
+          old[r] = 0u;
+      }
+#pragma unroll
+      for (int r = 0; r < kItems; r++) {
+        const bool pub = (old[r] == kNeutralMin);
+        const unsigned pm = __ballot_sync(0xFFFFFFFFu, pub);
+        if (pm) {
+          unsigned qb = 0;
+          if (lane == __ffs(pm) - 1) qb = atomicAdd(&s_qn, (unsigned)__popc(pm));
+          qb = __shfl_sync(0xFFFFFFFFu, qb, __ffs(pm) - 1);
+          if (pub) s_q[qb + __popc(pm & lanemask_lt())] = w[r];
         }
-        warp_append(pub, w[j], a.recip, a.recip_count);
+      }
+      __syncthreads();
+      const unsigned qn = s_qn;
+      if (qn) {
+        if (threadIdx.x == 0) s_qbase = atomicAdd(a.recip_count, qn);
+        __syncthreads();
+        const unsigned qb = s_qbase;
+        for (unsigned j = threadIdx.x; j < qn; j += kBlock) a.recip[qb + j] = s_q[j];
       }
     } else {
       double *mb = reinterpret_cast<double *>(a.mailbox);
 #pragma unroll
-      for (int j = 0; j < kItems; j++)
-        if (w[j] >= 0) atomicAdd(mb + w[j], (double)mv[j]);
+      for (int r = 0; r < kItems; r++)
+        if (w[r] >= 0) atomicAdd(mb + w[r], (double)mv[r]);
     }
     __syncthreads();
   }
@@ -339,62 +401,101 @@ __device__ void scatter_phase(const ScatterArgs &a, char *smem) {
 // ------------------------------------------------------------------
 // sparse apply for the min programs (SSSP / CC): consume every recipient's
 // mailbox, adopt an improvement, append improved vertices to the next
-// frontier with their edge prefix (edge-balanced frontier construction)
+// frontier with their edge prefix (edge-balanced frontier construction).
+// One 64-bit atomic per block chunk reserves (frontier slots, edge range).
 // ------------------------------------------------------------------
+
+constexpr int kApplyItems = 4;
+constexpr int kApplyChunk = kBlock * kApplyItems;
+
+__device__ __forceinline__ unsigned long long block_excl_scan_u64(unsigned long long x,
+                                                                  unsigned long long *s_w,
+                                                                  unsigned long long *total) {
+  unsigned long long incl = x;
+  for (int o = 1; o < 32; o <<= 1) {
+    const unsigned long long y = __shfl_up_sync(0xFFFFFFFFu, incl, o);
+    if ((int)lane_id() >= o) incl += y;
+  }
+  if (lane_id() == 31) s_w[threadIdx.x >> 5] = incl;
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    const unsigned long long w = (threadIdx.x < kWarps) ? s_w[threadIdx.x] : 0ull;
+    unsigned long long wi = w;
+    for (int o = 1; o < 32; o <<= 1) {
+      const unsigned long long y = __shfl_up_sync(0xFFFFFFFFu, wi, o);
+      if ((int)threadIdx.x >= o) wi += y;
+    }
+    if (threadIdx.x < kWarps) s_w[threadIdx.x] = wi - w;
+    if (threadIdx.x == 31) s_w[32] = wi;
+  }
+  __syncthreads();
+  const unsigned long long r = s_w[threadIdx.x >> 5] + incl - x;
+  *total = s_w[32];
+  return r;
+}
 
 template <int APP>
 __device__ void apply_min_phase(const int32_t *__restrict__ row_ptr, uint32_t *val,
                                 uint32_t *mailbox, const int32_t *recip, unsigned nrecip,
                                 const RunWs &ws, StepCounters *ctr,
                                 unsigned *s_bcast) {
-  const unsigned nthreads = gridDim.x * blockDim.x;
-  const unsigned gtid = blockIdx.x * blockDim.x + threadIdx.x;
-  const unsigned warp_base = gtid & ~31u;
+  __shared__ unsigned long long s_w[33];
+  __shared__ unsigned long long s_gbase;
   uint32_t *f_msg = reinterpret_cast<uint32_t *>(ws.f_msg);
   unsigned my_bcast = 0;
-  for (unsigned base = warp_base; base < nrecip; base += nthreads) {
-    const unsigned r = base + lane_id();
-    bool improved = false;
-    int v = 0, deg = 0, rs = 0;
-    uint32_t send = 0;
-    if (r < nrecip) {
-      v = recip[r];
-      const uint32_t m = mailbox[v];
-      mailbox[v] = kNeutralMin;  // consume (mailbox.py:112-117)
-      if (m < val[v]) {
-        val[v] = m;
-        improved = true;
-        send = (APP == PGX_APP_SSSP) ? m + 1u : m;
-        rs = row_ptr[v];
-        deg = row_ptr[v + 1] - rs;
+  for (unsigned base = blockIdx.x * kApplyChunk; base < nrecip;
+       base += gridDim.x * kApplyChunk) {  // block-uniform
+    int v[kApplyItems], deg[kApplyItems], rs[kApplyItems];
+    uint32_t send[kApplyItems], m[kApplyItems];
+    bool has[kApplyItems];
+#pragma unroll
+    for (int j = 0; j < kApplyItems; j++) {
+      const unsigned r = base + j * kBlock + threadIdx.x;
+      v[j] = (r < nrecip) ? recip[r] : -1;
+    }
+#pragma unroll
+    for (int j = 0; j < kApplyItems; j++) m[j] = (v[j] >= 0) ? mailbox[v[j]] : kNeutralMin;
+    unsigned long long mine = 0;
+#pragma unroll
+    for (int j = 0; j < kApplyItems; j++) {
+      has[j] = false;
+      deg[j] = 0;
+      if (v[j] >= 0) {
+        mailbox[v[j]] = kNeutralMin;  // consume (mailbox.py:112-117)
+        if (m[j] < val[v[j]]) {
+          val[v[j]] = m[j];
+          my_bcast++;
+          send[j] = (APP == PGX_APP_SSSP) ? m[j] + 1u : m[j];
+          rs[j] = row_ptr[v[j]];
+          deg[j] = row_ptr[v[j] + 1] - rs[j];
+          has[j] = deg[j] > 0;
+          if (has[j]) mine += (1ull << 32) | (unsigned long long)deg[j];
+        }
       }
     }
-    my_bcast += improved ? 1u : 0u;
-    const bool has = improved && deg > 0;
-    // warp exclusive scan of degrees over the senders with edges
-    int x = has ? deg : 0;
-    int incl = x;
-    for (int o = 1; o < 32; o <<= 1) {
-      const int y = __shfl_up_sync(0xFFFFFFFFu, incl, o);
-      if ((int)lane_id() >= o) incl += y;
+    unsigned long long total;
+    unsigned long long run = block_excl_scan_u64(mine, s_w, &total);
+    if (total == 0) {  // block-uniform
+      __syncthreads();
+      continue;
     }
-    const unsigned hm = __ballot_sync(0xFFFFFFFFu, has);
-    if (hm == 0) continue;
-    const int total = __shfl_sync(0xFFFFFFFFu, incl, 31);
-    unsigned long long packed = 0;
-    if (lane_id() == 0)
-      packed = atomicAdd(&ctr->packed,
-                         ((unsigned long long)__popc(hm) << 32) | (unsigned long long)total);
-    packed = __shfl_sync(0xFFFFFFFFu, packed, 0);
-    if (has) {
-      const unsigned pos = (unsigned)(packed >> 32) + __popc(hm & lanemask_lt());
-      const int eb = (int)(packed & 0xFFFFFFFFull) + incl - x;
-      ws.f_eb[pos] = eb;
-      ws.f_rs[pos] = rs;
-      f_msg[pos] = send;
-      for (int64_t t = ((int64_t)eb + kTile - 1) / kTile; t * kTile < (int64_t)eb + deg; t++)
-        ws.tile_src[t] = (int)pos;
+    if (threadIdx.x == 0) s_gbase = atomicAdd(&ctr->packed, total);
+    __syncthreads();
+    run += s_gbase;
+#pragma unroll
+    for (int j = 0; j < kApplyItems; j++) {
+      if (has[j]) {
+        const unsigned pos = (unsigned)(run >> 32);
+        const int eb = (int)(run & 0xFFFFFFFFull);
+        ws.f_eb[pos] = eb;
+        ws.f_rs[pos] = rs[j];
+        f_msg[pos] = send[j];
+        for (int64_t t = ((int64_t)eb + kTile - 1) / kTile; t * kTile < (int64_t)eb + deg[j]; t++)
+          ws.tile_src[t] = (int)pos;
+        run += (1ull << 32) | (unsigned long long)deg[j];
+      }
     }
+    __syncthreads();
   }
   atomicAdd(s_bcast, my_bcast);
 }
@@ -773,9 +874,7 @@ __global__ void rmat_kernel(int scale, int64_t first, int64_t count, uint64_t ta
 // launch helpers
 // ------------------------------------------------------------------
 
-size_t scatter_smem_bytes(int op) {
-  return (size_t)kSlots * (sizeof(int32_t) * 2 + (op == PGX_OP_SUM_F64 ? 8 : 4)) + 16;
-}
+size_t scatter_smem_bytes(int op) { return scatter_smem(op); }
 
 template <typename K>
 int coop_grid(K kernel, size_t smem, int *grid) {
