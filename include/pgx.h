@@ -64,13 +64,19 @@ extern "C" {
  *     [4] recipients of this superstep's messages (R_s)
  *     [5] superstep end, %globaltimer ns
  *     [6] vertices that computed a new value and sent (broadcasters)
- *     [7] reserved
+ *     [7] scatter start (end of this superstep's apply), %globaltimer ns
  */
 #define PGX_STAT_HDR 4
 #define PGX_STAT_FIELDS 8
 
 int pgx_abi_version(void);
 const char *pgx_last_error(void);
+
+/* process-wide tuning knobs (A/B experiments; defaults are shipped) */
+#define PGX_OPT_READ_FILTER 0   /* 1: skip the atomic when min(old,msg)==old */
+#define PGX_OPT_CTAS_PER_SM 1   /* persistent CTAs per SM, 0 = occupancy max */
+#define PGX_OPT_COUNT 2
+int pgx_set_option(int key, int value);
 
 /* number of SMs of `device` (host out pointer; syncs) */
 int pgx_device_sm_count(int device, int *sm_count);

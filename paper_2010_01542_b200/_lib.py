@@ -21,10 +21,16 @@ PGX_OK, PGX_EINVAL, PGX_ECUDA, PGX_ENOMEM = 0, -1, -2, -3
 PGX_APP_PAGERANK, PGX_APP_CC, PGX_APP_SSSP = 0, 1, 2
 PGX_OP_MIN_U32, PGX_OP_SUM_F64 = 0, 1
 PGX_STAT_HDR, PGX_STAT_FIELDS = 4, 8
+PGX_OPT_READ_FILTER, PGX_OPT_CTAS_PER_SM = 0, 1
+
+
+def set_option(key: int, value: int) -> None:
+    """Process-wide tuning knob of libpgx.so (A/B experiments)."""
+    check(load().pgx_set_option(key, value), "pgx_set_option")
 
 #: every symbol include/pgx.h declares (checked by tests/test_abi.py)
 EXPORTS = (
-    "pgx_abi_version", "pgx_last_error", "pgx_device_sm_count",
+    "pgx_abi_version", "pgx_last_error", "pgx_set_option", "pgx_device_sm_count",
     "pgx_offsets_to_i32", "pgx_graph_workspace_bytes", "pgx_graph_prepare",
     "pgx_run_workspace_bytes", "pgx_sssp_run", "pgx_cc_run",
     "pgx_pagerank_run", "pgx_rmat_keys",
@@ -43,6 +49,7 @@ _up = ctypes.c_size_t  # uintptr_t stream
 _SIGS = {
     "pgx_abi_version": (ctypes.c_int, []),
     "pgx_last_error": (ctypes.c_char_p, []),
+    "pgx_set_option": (ctypes.c_int, [ctypes.c_int, ctypes.c_int]),
     "pgx_device_sm_count": (ctypes.c_int, [ctypes.c_int, _p]),
     "pgx_offsets_to_i32": (ctypes.c_int, [_p, _p, _i64, _up]),
     "pgx_graph_workspace_bytes": (ctypes.c_int, [_i64, _i64, _p]),

@@ -41,14 +41,21 @@
 namespace {
 
 constexpr int kBlock = 512;          // threads per CTA
-constexpr int kItems = 8;            // edges per thread per tile
-constexpr int kTile = kBlock * kItems;  // 4096 edges per tile
-constexpr int kSlots = kTile + 2;    // sources per tile (+ sentinel)
+constexpr int kWarps = kBlock / 32;
+constexpr int kItems = 8;            // 32-edge rounds per warp tile
+constexpr int kTile = 32 * kItems;   // 256 edges per warp tile
+constexpr int kSlots = kTile + 2;    // sources per warp tile (+ sentinel)
 constexpr uint32_t kNeutralMin = 0xFFFFFFFFu;
 constexpr int kMaxCtas = 4096;
 constexpr int kCompactBlock = 1024;
 
 thread_local std::string g_last_error;
+
+// tuning knobs (pgx_set_option); defaults are the shipped configuration
+int g_opt[PGX_OPT_COUNT] = {
+    /* PGX_OPT_READ_FILTER */ 1,
+    /* PGX_OPT_CTAS_PER_SM */ 0,   // 0 = occupancy maximum
+};
 
 int fail(int code, const std::string &msg) {
   g_last_error = msg;
@@ -206,7 +213,7 @@ struct RunWs {
   int32_t *f_eb;           // [n+1] frontier: exclusive edge prefix
   int32_t *f_rs;           // [n]   frontier: CSR row start
   void *f_msg;             // [n]   frontier: message (u32) / PR share (f64)
-  int32_t *recip;          // [n]   recipients of the last scatter
+  uint32_t *has;           // [n/32+1] has-message bitmask (first publishers)
   int32_t *tile_src;       // [ceil(m/kTile)+2] sparse tile map
   void *mailbox;           // [n]   u32 (min) or f64 (sum)
 };
@@ -230,10 +237,11 @@ size_t run_ws_layout(int app, int64_t n, int64_t m, int32_t max_steps, RunWs *ws
   if (app != PGX_APP_PAGERANK) {
     w.f_eb = (int32_t *)take(sizeof(int32_t) * (size_t)(n + 1));
     w.f_rs = (int32_t *)take(sizeof(int32_t) * (size_t)(n + 1));
-    w.recip = (int32_t *)take(sizeof(int32_t) * (size_t)(n + 1));
+    w.has = (uint32_t *)take(sizeof(uint32_t) * (size_t)(n / 32 + 2));
     w.tile_src = (int32_t *)take(sizeof(int32_t) * (size_t)(ceil_div(m, kTile) + 2));
   } else {
-    w.f_eb = w.f_rs = w.recip = w.tile_src = nullptr;
+    w.f_eb = w.f_rs = w.tile_src = nullptr;
+    w.has = nullptr;
   }
   if (ws) *ws = w;
   return off;
@@ -252,62 +260,56 @@ struct ScatterArgs {
   const int32_t *rs;      // row start per source (sparse only)
   const int32_t *ids;     // vertex id per source (dense only)
   const void *msg;        // per-source message (sparse) / per-vertex share
-  const int32_t *tile_src;
+  const int32_t *tile_src;  // source containing the first edge of each warp tile
   int32_t nsrc;           // number of sources
   int64_t E;              // edges in this pass
   void *mailbox;
-  int32_t *recip;         // first-publisher list (min only)
-  unsigned *recip_count;
+  uint32_t *has;          // has-message bitmask (min only)
 };
 
-constexpr int kWarps = kBlock / 32;
-constexpr int kWarpEdges = kTile / kWarps;  // 256 = kItems rounds of 32
-
-// shared-memory footprint of the scatter: source slots + publish queue
+// shared memory of the scatter: one source window per warp
 __host__ __device__ constexpr size_t scatter_smem(int op) {
-  return (size_t)kSlots * (sizeof(int32_t) * 2 + (op == PGX_OP_SUM_F64 ? 8 : 4)) +
-         (op == PGX_OP_MIN_U32 ? sizeof(int32_t) * kTile : 0) + 16;
+  return (size_t)kWarps * kSlots * (sizeof(int32_t) * 2 + (op == PGX_OP_SUM_F64 ? 8 : 4)) + 16;
 }
 
-// Edge -> source mapping, one warp per 32 consecutive edges: lane j holds
-// the start of candidate source cur+1+j; the OR-reduction of the
-// in-window boundary bits gives every lane its source with one popc.
-// Sources have >= 1 edge, so at most 32 boundaries fall in a window.
-__device__ __forceinline__ int warp_find_first(const int32_t *s_eb, int k, int64_t e) {
-  int lo = 0, hi = k;  // s_eb[lo] <= e < s_eb[hi]
-  while (hi - lo > 1) {
-    const int step = (hi - lo + 31) >> 5;
-    const int p = lo + (int)lane_id() * step;
-    const bool le = (p < hi) && ((int64_t)s_eb[p] <= e);
-    const unsigned b = __ballot_sync(0xFFFFFFFFu, le);
-    lo += (31 - __clz(b)) * step;
-    hi = min(hi, lo + step);
-  }
-  return lo;
-}
-
+// One superstep's scatter.  Every warp owns whole 256-edge tiles of the
+// senders' edge space (exact edge balance; a hub row spans many tiles) and
+// runs without block barriers:
+//   1. the tile map gives the source holding the tile's first edge; the
+//      <= 257 sources of the tile are staged in the warp's smem window;
+//   2. per round of 32 consecutive edges, lane j holds the start of
+//      candidate source cur+1+j; the OR-reduction (REDUX) of the boundary
+//      bits that fall in the window gives every lane its source with one
+//      popc (sources have >= 1 edge, so <= 32 boundaries per window);
+//   3. the 8 neighbour ids are streamed (L1::no_allocate, L2 evict_first),
+//      then combined (min: read-filter + atomicMin, first publisher sets
+//      the has-message bit; sum: red.add.f64).
+// Returns the number of first publications made by this thread.
 template <int OP, MsgSrc MS>
-__device__ void scatter_phase(const ScatterArgs &a, char *smem) {
+__device__ unsigned scatter_phase(const ScatterArgs &a, char *smem, bool read_filter = true) {
   using Msg = typename std::conditional<OP == PGX_OP_SUM_F64, double, uint32_t>::type;
   constexpr bool kDense = MS != MsgSrc::kFrontier;
-  int32_t *s_eb = reinterpret_cast<int32_t *>(smem);
-  int32_t *s_rs = s_eb + kSlots;
-  Msg *s_msg = reinterpret_cast<Msg *>(s_rs + kSlots);
-  int32_t *s_q = reinterpret_cast<int32_t *>(s_msg + kSlots);  // publish queue
-  __shared__ unsigned s_qn, s_qbase;
-  const uint64_t pol = evict_first_policy();
-  const int64_t ntiles = (a.E + kTile - 1) / kTile;
   const int lane = (int)lane_id();
   const int warp = threadIdx.x >> 5;
+  int32_t *s_eb = reinterpret_cast<int32_t *>(smem) + warp * kSlots;
+  int32_t *s_rs = reinterpret_cast<int32_t *>(smem) + kWarps * kSlots + warp * kSlots;
+  Msg *s_msg = reinterpret_cast<Msg *>(reinterpret_cast<int32_t *>(smem) + 2 * kWarps * kSlots) +
+               warp * kSlots;
+  const uint64_t pol = evict_first_policy();
+  const int64_t ntiles = (a.E + kTile - 1) / kTile;
   const unsigned upto = (lane == 31) ? 0xFFFFFFFFu : ((2u << lane) - 1u);
+  const int64_t gwarp = (int64_t)blockIdx.x * kWarps + warp;
+  const int64_t nwarps = (int64_t)gridDim.x * kWarps;
+  unsigned published = 0;
 
-  for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
+  for (int64_t t = gwarp; t < ntiles; t += nwarps) {
     const int64_t e0 = t * kTile;
     const int64_t e1 = min(a.E, e0 + kTile);
     const int i0 = a.tile_src[t];
     const int i1 = (t + 1 < ntiles) ? a.tile_src[t + 1] : a.nsrc - 1;
-    const int k = i1 - i0 + 1;  // <= kTile + 1: every source has >= 1 edge
-    for (int j = threadIdx.x; j <= k; j += kBlock) {
+    const int k = i1 - i0 + 1;  // <= kTile + 1
+    __syncwarp();
+    for (int j = lane; j <= k; j += 32) {
       const int i = i0 + j;
       if (j < k) {
         s_eb[j] = a.eb[i];
@@ -323,45 +325,40 @@ __device__ void scatter_phase(const ScatterArgs &a, char *smem) {
         s_eb[j] = (i < a.nsrc) ? a.eb[i] : (int32_t)a.E;  // sentinel
       }
     }
-    if (threadIdx.x == 0) s_qn = 0;
-    __syncthreads();
+    __syncwarp();
 
-    const int64_t we0 = e0 + (int64_t)warp * kWarpEdges;
-    const int64_t we1 = min(e1, we0 + kWarpEdges);
     int w[kItems];
     Msg mv[kItems];
+    int cur = 0;  // s_eb[0] <= e0: tile_src names the source holding e0
 #pragma unroll
-    for (int r = 0; r < kItems; r++) w[r] = -1;
-    if (we0 < e1) {  // warp-uniform
-      int cur = warp_find_first(s_eb, k, we0);
-#pragma unroll
-      for (int r = 0; r < kItems; r++) {
-        const int64_t base = we0 + r * 32;
-        const int64_t e = base + lane;
-        const int ci = cur + 1 + lane;
-        unsigned bit = 0;
-        if (ci <= k) {
-          const int64_t pp = (int64_t)s_eb[ci] - base;
-          if (pp >= 0 && pp < 32) bit = 1u << pp;
-        }
-        const unsigned bm = __reduce_or_sync(0xFFFFFFFFu, bit);
-        const int src = cur + __popc(bm & upto);
-        cur += __popc(bm);
-        if (e < we1) {
-          const int64_t pos = kDense ? e : (int64_t)s_rs[src] + (e - s_eb[src]);
-          w[r] = ld_stream(a.col + pos, pol);
-          mv[r] = s_msg[src];
-        }
+    for (int r = 0; r < kItems; r++) {
+      const int64_t base = e0 + r * 32;
+      const int64_t e = base + lane;
+      const int ci = cur + 1 + lane;
+      unsigned bit = 0;
+      if (ci <= k) {
+        const int64_t pp = (int64_t)s_eb[ci] - base;
+        if (pp >= 0 && pp < 32) bit = 1u << pp;
+      }
+      const unsigned bm = __reduce_or_sync(0xFFFFFFFFu, bit);
+      const int src = cur + __popc(bm & upto);
+      cur += __popc(bm);
+      w[r] = -1;
+      if (e < e1) {
+        const int64_t pos = kDense ? e : (int64_t)s_rs[src] + (e - s_eb[src]);
+        w[r] = ld_stream(a.col + pos, pol);
+        mv[r] = s_msg[src];
       }
     }
     if (OP == PGX_OP_MIN_U32) {
       // hybrid combiner: read-filter (mailbox.py:159 short-circuit), then
       // one atomicMin; the unique lane that sees NEUTRAL come back is the
-      // first publisher (mailbox.py:190-199) and queues the recipient.
+      // first publisher (mailbox.py:190-199) and sets the has-message bit.
       uint32_t *mb = reinterpret_cast<uint32_t *>(a.mailbox);
       uint32_t old[kItems];
 #pragma unroll
-      for (int r = 0; r < kItems; r++) old[r] = (w[r] >= 0) ? mb[w[r]] : 0u;
+      for (int r = 0; r < kItems; r++)
+        old[r] = (w[r] >= 0) ? (read_filter ? mb[w[r]] : kNeutralMin) : 0u;
 #pragma unroll
       for (int r = 0; r < kItems; r++) {
         if (w[r] >= 0 && (uint32_t)mv[r] < old[r])
@@ -371,22 +368,10 @@ __device__ void scatter_phase(const ScatterArgs &a, char *smem) {
       }
 #pragma unroll
       for (int r = 0; r < kItems; r++) {
-        const bool pub = (old[r] == kNeutralMin);
-        const unsigned pm = __ballot_sync(0xFFFFFFFFu, pub);
-        if (pm) {
-          unsigned qb = 0;
-          if (lane == __ffs(pm) - 1) qb = atomicAdd(&s_qn, (unsigned)__popc(pm));
-          qb = __shfl_sync(0xFFFFFFFFu, qb, __ffs(pm) - 1);
-          if (pub) s_q[qb + __popc(pm & lanemask_lt())] = w[r];
+        if (old[r] == kNeutralMin) {
+          atomicOr(a.has + (w[r] >> 5), 1u << (w[r] & 31));
+          published++;
         }
-      }
-      __syncthreads();
-      const unsigned qn = s_qn;
-      if (qn) {
-        if (threadIdx.x == 0) s_qbase = atomicAdd(a.recip_count, qn);
-        __syncthreads();
-        const unsigned qb = s_qbase;
-        for (unsigned j = threadIdx.x; j < qn; j += kBlock) a.recip[qb + j] = s_q[j];
       }
     } else {
       double *mb = reinterpret_cast<double *>(a.mailbox);
@@ -394,19 +379,17 @@ __device__ void scatter_phase(const ScatterArgs &a, char *smem) {
       for (int r = 0; r < kItems; r++)
         if (w[r] >= 0) atomicAdd(mb + w[r], (double)mv[r]);
     }
-    __syncthreads();
   }
+  return published;
 }
 
 // ------------------------------------------------------------------
-// sparse apply for the min programs (SSSP / CC): consume every recipient's
-// mailbox, adopt an improvement, append improved vertices to the next
-// frontier with their edge prefix (edge-balanced frontier construction).
-// One 64-bit atomic per block chunk reserves (frontier slots, edge range).
+// sparse apply for the min programs (SSSP / CC), driven by the
+// has-message bitmask: consume every flagged mailbox (vertex order),
+// adopt an improvement, append improved vertices to the next frontier
+// with their edge prefix.  One 64-bit atomic per block chunk reserves
+// (frontier slots, edge range); the tile map is written as a side effect.
 // ------------------------------------------------------------------
-
-constexpr int kApplyItems = 4;
-constexpr int kApplyChunk = kBlock * kApplyItems;
 
 __device__ __forceinline__ unsigned long long block_excl_scan_u64(unsigned long long x,
                                                                   unsigned long long *s_w,
@@ -431,73 +414,87 @@ __device__ __forceinline__ unsigned long long block_excl_scan_u64(unsigned long 
   __syncthreads();
   const unsigned long long r = s_w[threadIdx.x >> 5] + incl - x;
   *total = s_w[32];
+  __syncthreads();
   return r;
 }
 
 template <int APP>
-__device__ void apply_min_phase(const int32_t *__restrict__ row_ptr, uint32_t *val,
-                                uint32_t *mailbox, const int32_t *recip, unsigned nrecip,
-                                const RunWs &ws, StepCounters *ctr,
-                                unsigned *s_bcast) {
+__device__ unsigned apply_min_phase(const int32_t *__restrict__ row_ptr, uint32_t *val,
+                                    uint32_t *mailbox, int32_t n, const RunWs &ws,
+                                    StepCounters *ctr) {
   __shared__ unsigned long long s_w[33];
   __shared__ unsigned long long s_gbase;
   uint32_t *f_msg = reinterpret_cast<uint32_t *>(ws.f_msg);
-  unsigned my_bcast = 0;
-  for (unsigned base = blockIdx.x * kApplyChunk; base < nrecip;
-       base += gridDim.x * kApplyChunk) {  // block-uniform
-    int v[kApplyItems], deg[kApplyItems], rs[kApplyItems];
-    uint32_t send[kApplyItems], m[kApplyItems];
-    bool has[kApplyItems];
-#pragma unroll
-    for (int j = 0; j < kApplyItems; j++) {
-      const unsigned r = base + j * kBlock + threadIdx.x;
-      v[j] = (r < nrecip) ? recip[r] : -1;
+  const int words = (n + 31) >> 5;
+  unsigned bcast = 0;
+  for (int base = blockIdx.x * kBlock; base < words; base += gridDim.x * kBlock) {
+    const int wi = base + threadIdx.x;
+    uint32_t word = 0;
+    if (wi < words) {
+      word = ws.has[wi];
+      if (word) ws.has[wi] = 0u;
     }
-#pragma unroll
-    for (int j = 0; j < kApplyItems; j++) m[j] = (v[j] >= 0) ? mailbox[v[j]] : kNeutralMin;
+    uint32_t imp = 0;
     unsigned long long mine = 0;
+    uint32_t rem = word;
+    while (rem) {  // batches of up to 4 flagged vertices, independent loads
+      int vb[4];
+      uint32_t m[4], cv[4];
 #pragma unroll
-    for (int j = 0; j < kApplyItems; j++) {
-      has[j] = false;
-      deg[j] = 0;
-      if (v[j] >= 0) {
-        mailbox[v[j]] = kNeutralMin;  // consume (mailbox.py:112-117)
-        if (m[j] < val[v[j]]) {
-          val[v[j]] = m[j];
-          my_bcast++;
-          send[j] = (APP == PGX_APP_SSSP) ? m[j] + 1u : m[j];
-          rs[j] = row_ptr[v[j]];
-          deg[j] = row_ptr[v[j] + 1] - rs[j];
-          has[j] = deg[j] > 0;
-          if (has[j]) mine += (1ull << 32) | (unsigned long long)deg[j];
+      for (int j = 0; j < 4; j++) {
+        vb[j] = rem ? __ffs(rem) - 1 : -1;
+        if (rem) rem &= rem - 1;
+      }
+#pragma unroll
+      for (int j = 0; j < 4; j++) {
+        if (vb[j] >= 0) {
+          const int v = (wi << 5) + vb[j];
+          m[j] = mailbox[v];
+          cv[j] = val[v];
+        }
+      }
+#pragma unroll
+      for (int j = 0; j < 4; j++) {
+        if (vb[j] >= 0) {
+          const int v = (wi << 5) + vb[j];
+          mailbox[v] = kNeutralMin;  // consume (mailbox.py:112-117)
+          if (m[j] < cv[j]) {
+            val[v] = m[j];
+            imp |= 1u << vb[j];
+            bcast++;
+            const int deg = row_ptr[v + 1] - row_ptr[v];
+            if (deg > 0) mine += (1ull << 32) | (unsigned long long)deg;
+          }
         }
       }
     }
     unsigned long long total;
     unsigned long long run = block_excl_scan_u64(mine, s_w, &total);
-    if (total == 0) {  // block-uniform
-      __syncthreads();
-      continue;
-    }
+    if (total == 0) continue;  // block-uniform
     if (threadIdx.x == 0) s_gbase = atomicAdd(&ctr->packed, total);
     __syncthreads();
     run += s_gbase;
-#pragma unroll
-    for (int j = 0; j < kApplyItems; j++) {
-      if (has[j]) {
+    while (imp) {
+      const int b = __ffs(imp) - 1;
+      imp &= imp - 1;
+      const int v = (wi << 5) + b;
+      const int rs = row_ptr[v];
+      const int deg = row_ptr[v + 1] - rs;
+      if (deg > 0) {
         const unsigned pos = (unsigned)(run >> 32);
         const int eb = (int)(run & 0xFFFFFFFFull);
+        const uint32_t mv = val[v];
         ws.f_eb[pos] = eb;
-        ws.f_rs[pos] = rs[j];
-        f_msg[pos] = send[j];
-        for (int64_t t = ((int64_t)eb + kTile - 1) / kTile; t * kTile < (int64_t)eb + deg[j]; t++)
+        ws.f_rs[pos] = rs;
+        f_msg[pos] = (APP == PGX_APP_SSSP) ? mv + 1u : mv;
+        for (int64_t t = ((int64_t)eb + kTile - 1) / kTile; t * kTile < (int64_t)eb + deg; t++)
           ws.tile_src[t] = (int)pos;
-        run += (1ull << 32) | (unsigned long long)deg[j];
+        run += (1ull << 32) | (unsigned long long)deg;
       }
     }
     __syncthreads();
   }
-  atomicAdd(s_bcast, my_bcast);
+  return bcast;
 }
 
 __device__ __forceinline__ void record_step(int64_t *stats, int s, int64_t active,
@@ -511,7 +508,6 @@ __device__ __forceinline__ void record_step(int64_t *stats, int s, int64_t activ
   st[4] = recips;
   st[5] = (int64_t)globaltimer();
   st[6] = bcast;
-  st[7] = 0;
 }
 
 // ------------------------------------------------------------------
@@ -528,14 +524,14 @@ struct MinRunParams {
   uint32_t *val;
   int32_t source;  // SSSP only
   int32_t max_steps;
+  int32_t read_filter;
   int64_t *stats;
 };
 
 template <int APP>
 __global__ void __launch_bounds__(kBlock, 2) min_run_kernel(MinRunParams p) {
   extern __shared__ __align__(16) char smem[];
-  __shared__ unsigned s_bcast;
-  __shared__ unsigned s_flag;
+  __shared__ unsigned s_red[32];
   unsigned gen = 0;
   if (threadIdx.x == 0) gen = ld_acquire(&p.ws.bar->gen);
   uint32_t *mailbox = reinterpret_cast<uint32_t *>(p.ws.mailbox);
@@ -547,6 +543,7 @@ __global__ void __launch_bounds__(kBlock, 2) min_run_kernel(MinRunParams p) {
     p.val[v] = (APP == PGX_APP_CC) ? v : kNeutralMin;
     mailbox[v] = kNeutralMin;
   }
+  for (unsigned wi = gtid; wi < (unsigned)(p.n / 32 + 2); wi += nthreads) p.ws.has[wi] = 0u;
   if (blockIdx.x == 0 && threadIdx.x == 0) {
     p.stats[0] = p.stats[1] = 0;
     p.stats[2] = gridDim.x;
@@ -571,14 +568,15 @@ __global__ void __launch_bounds__(kBlock, 2) min_run_kernel(MinRunParams p) {
   }
   grid_sync(p.ws.bar, gen);
   if (APP == PGX_APP_SSSP && gtid == 0) p.val[p.source] = 0u;
+  if (gtid == 0) p.stats[PGX_STAT_HDR + 7] = (int64_t)globaltimer();
 
   for (int s = 0;; s++) {
     // ---- scatter(s) ----
     ScatterArgs a;
     a.col = p.col;
     a.mailbox = mailbox;
-    a.recip = p.ws.recip;
-    a.recip_count = &p.ws.ctr[s].recip;
+    a.has = p.ws.has;
+    unsigned pub;
     if (APP == PGX_APP_CC && s == 0) {
       a.eb = p.g.nz_eb;
       a.rs = nullptr;
@@ -587,7 +585,7 @@ __global__ void __launch_bounds__(kBlock, 2) min_run_kernel(MinRunParams p) {
       a.tile_src = p.g.tile_src;
       a.nsrc = p.g.hdr[0];
       a.E = p.m;
-      scatter_phase<PGX_OP_MIN_U32, MsgSrc::kSourceId>(a, smem);
+      pub = scatter_phase<PGX_OP_MIN_U32, MsgSrc::kSourceId>(a, smem, p.read_filter);
     } else {
       const unsigned long long packed = p.ws.ctr[s].packed;
       a.eb = p.ws.f_eb;
@@ -597,8 +595,10 @@ __global__ void __launch_bounds__(kBlock, 2) min_run_kernel(MinRunParams p) {
       a.tile_src = p.ws.tile_src;
       a.nsrc = (int32_t)(packed >> 32);
       a.E = (int64_t)(packed & 0xFFFFFFFFull);
-      scatter_phase<PGX_OP_MIN_U32, MsgSrc::kFrontier>(a, smem);
+      pub = scatter_phase<PGX_OP_MIN_U32, MsgSrc::kFrontier>(a, smem, p.read_filter);
     }
+    pub = block_sum<unsigned>(pub, s_red);
+    if (threadIdx.x == 0 && pub) atomicAdd(&p.ws.ctr[s].recip, pub);
     if (blockIdx.x == 0 && threadIdx.x == 0) {
       StepCounters z = {};
       p.ws.ctr[s + 1] = z;
@@ -626,15 +626,13 @@ __global__ void __launch_bounds__(kBlock, 2) min_run_kernel(MinRunParams p) {
     if (nrecip == 0 || s + 1 == p.max_steps) break;
 
     // ---- apply(s+1): consume + compute + frontier build ----
-    if (threadIdx.x == 0) s_bcast = 0;
-    __syncthreads();
-    apply_min_phase<APP>(p.row_ptr, p.val, mailbox, p.ws.recip, nrecip, p.ws, &p.ws.ctr[s + 1],
-                         &s_bcast);
-    __syncthreads();
-    if (threadIdx.x == 0 && s_bcast) atomicAdd(&p.ws.ctr[s + 1].bcast, s_bcast);
+    unsigned bc = apply_min_phase<APP>(p.row_ptr, p.val, mailbox, p.n, p.ws, &p.ws.ctr[s + 1]);
+    bc = block_sum<unsigned>(bc, s_red);
+    if (threadIdx.x == 0 && bc) atomicAdd(&p.ws.ctr[s + 1].bcast, bc);
     grid_sync(p.ws.bar, gen);
+    if (blockIdx.x == 0 && threadIdx.x == 0)  // apply(s+1) end = scatter(s+1) start
+      p.stats[PGX_STAT_HDR + (int64_t)(s + 1) * PGX_STAT_FIELDS + 7] = (int64_t)globaltimer();
   }
-  (void)s_flag;
 }
 
 struct PrRunParams {
@@ -695,8 +693,7 @@ __global__ void __launch_bounds__(kBlock, 2) pagerank_run_kernel(PrRunParams p) 
   a.nsrc = p.g.hdr[0];
   a.E = p.m;
   a.mailbox = mailbox;
-  a.recip = nullptr;
-  a.recip_count = nullptr;
+  a.has = nullptr;
   const unsigned long long ndangling = p.ws.misc[0];
   double dangling = __dmul_rn(p.r0, (double)ndangling);  // algorithms.py:55
   const int64_t nspread = (int64_t)p.n - (int64_t)ndangling;
@@ -733,6 +730,7 @@ __global__ void __launch_bounds__(kBlock, 2) pagerank_run_kernel(PrRunParams p) 
     }
     const bool cap = (s + 1 == p.max_steps);
     if (blockIdx.x == 0 && threadIdx.x == 0) {
+      p.stats[PGX_STAT_HDR + (int64_t)s * PGX_STAT_FIELDS + 7] = (int64_t)globaltimer();
       record_step(p.stats, s, p.n, (s == last) ? 0 : nspread, p.m, nspread, p.n,
                   (s == last) ? 0 : nspread);
       if (s == last || cap) {
@@ -884,6 +882,8 @@ int coop_grid(K kernel, size_t smem, int *grid) {
   PGX_CUDA(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   PGX_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, kBlock, smem));
   if (per_sm < 1) return fail(PGX_ECUDA, "persistent kernel does not fit on an SM");
+  if (g_opt[PGX_OPT_CTAS_PER_SM] > 0 && g_opt[PGX_OPT_CTAS_PER_SM] < per_sm)
+    per_sm = g_opt[PGX_OPT_CTAS_PER_SM];
   int g = sms * per_sm;
   if (g > kMaxCtas) g = kMaxCtas;
   *grid = g;
@@ -910,6 +910,12 @@ extern "C" {
 int pgx_abi_version(void) { return PGX_ABI_VERSION; }
 
 const char *pgx_last_error(void) { return g_last_error.c_str(); }
+
+int pgx_set_option(int key, int value) {
+  if (key < 0 || key >= PGX_OPT_COUNT) return fail(PGX_EINVAL, "unknown option");
+  g_opt[key] = value;
+  return PGX_OK;
+}
 
 int pgx_device_sm_count(int device, int *sm_count) {
   if (!sm_count) return fail(PGX_EINVAL, "null out pointer");
@@ -982,6 +988,7 @@ static int min_run(int app, int32_t n, int64_t m, const int32_t *row_ptr, const 
   p.val = val;
   p.source = source;
   p.max_steps = max_supersteps;
+  p.read_filter = g_opt[PGX_OPT_READ_FILTER];
   p.stats = stats;
   cudaStream_t st = (cudaStream_t)stream;
   PGX_CUDA(cudaMemsetAsync(p.ws.bar, 0, 64, st));

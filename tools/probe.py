@@ -7,6 +7,11 @@ from paper_2010_01542_b200.rmat import rmat_graph
 
 cfgs = sys.argv[1].split(",") if len(sys.argv) > 1 else ["C2", "C3", "C1", "C4"]
 reps = int(sys.argv[2]) if len(sys.argv) > 2 else 5
+from paper_2010_01542_b200 import _lib
+for kv in sys.argv[3:]:
+    k, v = kv.split("=")
+    _lib.set_option(getattr(_lib, "PGX_OPT_" + k.upper()), int(v))
+    print("option", k, v)
 for c in cfgs:
     t = time.time()
     g = rmat_graph(c)
@@ -28,7 +33,10 @@ for c in cfgs:
     E = sum(x.edges for x in rep.supersteps)
     print(f"{c} {app} n={g.vertex_count} m={g.edge_count} gen={tg:.2f}s ctas={rep.ctas} "
           f"event={ms:.3f}ms device={rep.device_seconds*1e3:.3f}ms GTEPS={E/ms/1e6:.1f}")
+    st = plan.stats.cpu().numpy()
     for x in rep.supersteps:
-        print(f"   s{x.index}: {x.seconds*1e6:9.1f} us  act={x.active_count} F={x.broadcasters} E={x.edges} R={x.recipients}")
+        row = st[4 + 8 * x.index: 4 + 8 * x.index + 8]
+        scat = (row[5] - row[7]) * 1e-3
+        print(f"   s{x.index}: {x.seconds*1e6:9.1f} us (scatter {scat:8.1f}) act={x.active_count} F={x.broadcasters} E={x.edges} R={x.recipients}")
     del g, plan
     torch.cuda.empty_cache()
