@@ -38,12 +38,17 @@
 
 #include "../../include/pgx.h"
 
+#ifndef PGX_MIN_BLOCKS
+#define PGX_MIN_BLOCKS 2
+#endif
+
 namespace {
 
 constexpr int kBlock = 512;          // threads per CTA
 constexpr int kWarps = kBlock / 32;
 constexpr int kItems = 8;            // 32-edge rounds per warp tile
 constexpr int kTile = 32 * kItems;   // 256 edges per warp tile
+constexpr int kPass = 4;             // rounds in flight per pass
 constexpr int kSlots = kTile + 2;    // sources per warp tile (+ sentinel)
 constexpr uint32_t kNeutralMin = 0xFFFFFFFFu;
 constexpr int kMaxCtas = 4096;
@@ -327,57 +332,60 @@ __device__ unsigned scatter_phase(const ScatterArgs &a, char *smem, bool read_fi
     }
     __syncwarp();
 
-    int w[kItems];
-    Msg mv[kItems];
     int cur = 0;  // s_eb[0] <= e0: tile_src names the source holding e0
+#pragma unroll 1
+    for (int pass = 0; pass < kItems / kPass; pass++) {
+      int w[kPass];
+      Msg mv[kPass];
 #pragma unroll
-    for (int r = 0; r < kItems; r++) {
-      const int64_t base = e0 + r * 32;
-      const int64_t e = base + lane;
-      const int ci = cur + 1 + lane;
-      unsigned bit = 0;
-      if (ci <= k) {
-        const int64_t pp = (int64_t)s_eb[ci] - base;
-        if (pp >= 0 && pp < 32) bit = 1u << pp;
-      }
-      const unsigned bm = __reduce_or_sync(0xFFFFFFFFu, bit);
-      const int src = cur + __popc(bm & upto);
-      cur += __popc(bm);
-      w[r] = -1;
-      if (e < e1) {
-        const int64_t pos = kDense ? e : (int64_t)s_rs[src] + (e - s_eb[src]);
-        w[r] = ld_stream(a.col + pos, pol);
-        mv[r] = s_msg[src];
-      }
-    }
-    if (OP == PGX_OP_MIN_U32) {
-      // hybrid combiner: read-filter (mailbox.py:159 short-circuit), then
-      // one atomicMin; the unique lane that sees NEUTRAL come back is the
-      // first publisher (mailbox.py:190-199) and sets the has-message bit.
-      uint32_t *mb = reinterpret_cast<uint32_t *>(a.mailbox);
-      uint32_t old[kItems];
-#pragma unroll
-      for (int r = 0; r < kItems; r++)
-        old[r] = (w[r] >= 0) ? (read_filter ? mb[w[r]] : kNeutralMin) : 0u;
-#pragma unroll
-      for (int r = 0; r < kItems; r++) {
-        if (w[r] >= 0 && (uint32_t)mv[r] < old[r])
-          old[r] = atomicMin(mb + w[r], (uint32_t)mv[r]);
-        else
-          old[r] = 0u;
-      }
-#pragma unroll
-      for (int r = 0; r < kItems; r++) {
-        if (old[r] == kNeutralMin) {
-          atomicOr(a.has + (w[r] >> 5), 1u << (w[r] & 31));
-          published++;
+      for (int r = 0; r < kPass; r++) {
+        const int64_t base = e0 + (pass * kPass + r) * 32;
+        const int64_t e = base + lane;
+        const int ci = cur + 1 + lane;
+        unsigned bit = 0;
+        if (ci <= k) {
+          const int64_t pp = (int64_t)s_eb[ci] - base;
+          if (pp >= 0 && pp < 32) bit = 1u << pp;
+        }
+        const unsigned bm = __reduce_or_sync(0xFFFFFFFFu, bit);
+        const int src = cur + __popc(bm & upto);
+        cur += __popc(bm);
+        w[r] = -1;
+        if (e < e1) {
+          const int64_t pos = kDense ? e : (int64_t)s_rs[src] + (e - s_eb[src]);
+          w[r] = ld_stream(a.col + pos, pol);
+          mv[r] = s_msg[src];
         }
       }
-    } else {
-      double *mb = reinterpret_cast<double *>(a.mailbox);
+      if (OP == PGX_OP_MIN_U32) {
+        // hybrid combiner: read-filter (mailbox.py:159 short-circuit), then
+        // one atomicMin; the unique lane that sees NEUTRAL come back is the
+        // first publisher (mailbox.py:190-199) and sets the has-message bit.
+        uint32_t *mb = reinterpret_cast<uint32_t *>(a.mailbox);
+        uint32_t old[kPass];
 #pragma unroll
-      for (int r = 0; r < kItems; r++)
-        if (w[r] >= 0) atomicAdd(mb + w[r], (double)mv[r]);
+        for (int r = 0; r < kPass; r++)
+          old[r] = (w[r] >= 0) ? (read_filter ? mb[w[r]] : kNeutralMin) : 0u;
+#pragma unroll
+        for (int r = 0; r < kPass; r++) {
+          if (w[r] >= 0 && (uint32_t)mv[r] < old[r])
+            old[r] = atomicMin(mb + w[r], (uint32_t)mv[r]);
+          else
+            old[r] = 0u;
+        }
+#pragma unroll
+        for (int r = 0; r < kPass; r++) {
+          if (old[r] == kNeutralMin) {
+            atomicOr(a.has + (w[r] >> 5), 1u << (w[r] & 31));
+            published++;
+          }
+        }
+      } else {
+        double *mb = reinterpret_cast<double *>(a.mailbox);
+#pragma unroll
+        for (int r = 0; r < kPass; r++)
+          if (w[r] >= 0) atomicAdd(mb + w[r], (double)mv[r]);
+      }
     }
   }
   return published;
@@ -418,81 +426,103 @@ __device__ __forceinline__ unsigned long long block_excl_scan_u64(unsigned long 
   return r;
 }
 
+// Apply chunk: kApplyWords bitmask words per block iteration.  The set
+// bits are first compacted into a shared-memory vertex list (block scan
+// of popcounts), then every thread consumes up to kApplyItems recipients
+// with independent loads -- no per-word serial chains.
+constexpr int kApplyWords = 64;
+constexpr int kApplyItems = kApplyWords * 32 / kBlock;  // 4
+
 template <int APP>
 __device__ unsigned apply_min_phase(const int32_t *__restrict__ row_ptr, uint32_t *val,
                                     uint32_t *mailbox, int32_t n, const RunWs &ws,
-                                    StepCounters *ctr) {
+                                    StepCounters *ctr, char *smem) {
   __shared__ unsigned long long s_w[33];
   __shared__ unsigned long long s_gbase;
+  int32_t *s_list = reinterpret_cast<int32_t *>(smem);  // kApplyWords * 32 ids
   uint32_t *f_msg = reinterpret_cast<uint32_t *>(ws.f_msg);
   const int words = (n + 31) >> 5;
   unsigned bcast = 0;
-  for (int base = blockIdx.x * kBlock; base < words; base += gridDim.x * kBlock) {
-    const int wi = base + threadIdx.x;
+  for (int base = blockIdx.x * kApplyWords; base < words; base += gridDim.x * kApplyWords) {
+    // ---- expand the chunk's set bits into s_list (vertex order) ----
     uint32_t word = 0;
-    if (wi < words) {
+    const int wi = base + threadIdx.x;
+    if (threadIdx.x < kApplyWords && wi < words) {
       word = ws.has[wi];
       if (word) ws.has[wi] = 0u;
     }
-    uint32_t imp = 0;
+    unsigned long long tot64;
+    const int off = (int)block_excl_scan_u64((unsigned long long)__popc(word), s_w, &tot64);
+    const int T = (int)tot64;
+    if (T == 0) continue;  // block-uniform
+    {
+      int o = off;
+      uint32_t rem = word;
+      while (rem) {
+        const int b = __ffs(rem) - 1;
+        rem &= rem - 1;
+        s_list[o++] = (wi << 5) + b;
+      }
+    }
+    __syncthreads();
+    // ---- consume + compute, kApplyItems independent recipients / thread ----
+    int v[kApplyItems];
+    uint32_t m[kApplyItems], cv[kApplyItems];
+    int deg[kApplyItems], rs[kApplyItems];
+#pragma unroll
+    for (int j = 0; j < kApplyItems; j++) {
+      const int idx = j * kBlock + threadIdx.x;
+      v[j] = (idx < T) ? s_list[idx] : -1;
+    }
+#pragma unroll
+    for (int j = 0; j < kApplyItems; j++) {
+      if (v[j] >= 0) {
+        m[j] = mailbox[v[j]];
+        cv[j] = val[v[j]];
+      }
+    }
     unsigned long long mine = 0;
-    uint32_t rem = word;
-    while (rem) {  // batches of up to 4 flagged vertices, independent loads
-      int vb[4];
-      uint32_t m[4], cv[4];
 #pragma unroll
-      for (int j = 0; j < 4; j++) {
-        vb[j] = rem ? __ffs(rem) - 1 : -1;
-        if (rem) rem &= rem - 1;
-      }
-#pragma unroll
-      for (int j = 0; j < 4; j++) {
-        if (vb[j] >= 0) {
-          const int v = (wi << 5) + vb[j];
-          m[j] = mailbox[v];
-          cv[j] = val[v];
+    for (int j = 0; j < kApplyItems; j++) {
+      deg[j] = 0;
+      if (v[j] >= 0) {
+        mailbox[v[j]] = kNeutralMin;  // consume (mailbox.py:112-117)
+        if (m[j] < cv[j]) {
+          val[v[j]] = m[j];
+          bcast++;
+          rs[j] = row_ptr[v[j]];
+          deg[j] = -1;  // improved; degree resolved below
         }
       }
+    }
 #pragma unroll
-      for (int j = 0; j < 4; j++) {
-        if (vb[j] >= 0) {
-          const int v = (wi << 5) + vb[j];
-          mailbox[v] = kNeutralMin;  // consume (mailbox.py:112-117)
-          if (m[j] < cv[j]) {
-            val[v] = m[j];
-            imp |= 1u << vb[j];
-            bcast++;
-            const int deg = row_ptr[v + 1] - row_ptr[v];
-            if (deg > 0) mine += (1ull << 32) | (unsigned long long)deg;
-          }
-        }
+    for (int j = 0; j < kApplyItems; j++) {
+      if (deg[j] == -1) {
+        deg[j] = row_ptr[v[j] + 1] - rs[j];
+        if (deg[j] > 0) mine += (1ull << 32) | (unsigned long long)deg[j];
       }
     }
     unsigned long long total;
     unsigned long long run = block_excl_scan_u64(mine, s_w, &total);
-    if (total == 0) continue;  // block-uniform
-    if (threadIdx.x == 0) s_gbase = atomicAdd(&ctr->packed, total);
-    __syncthreads();
-    run += s_gbase;
-    while (imp) {
-      const int b = __ffs(imp) - 1;
-      imp &= imp - 1;
-      const int v = (wi << 5) + b;
-      const int rs = row_ptr[v];
-      const int deg = row_ptr[v + 1] - rs;
-      if (deg > 0) {
-        const unsigned pos = (unsigned)(run >> 32);
-        const int eb = (int)(run & 0xFFFFFFFFull);
-        const uint32_t mv = val[v];
-        ws.f_eb[pos] = eb;
-        ws.f_rs[pos] = rs;
-        f_msg[pos] = (APP == PGX_APP_SSSP) ? mv + 1u : mv;
-        for (int64_t t = ((int64_t)eb + kTile - 1) / kTile; t * kTile < (int64_t)eb + deg; t++)
-          ws.tile_src[t] = (int)pos;
-        run += (1ull << 32) | (unsigned long long)deg;
+    if (total != 0) {  // block-uniform
+      if (threadIdx.x == 0) s_gbase = atomicAdd(&ctr->packed, total);
+      __syncthreads();
+      run += s_gbase;
+#pragma unroll
+      for (int j = 0; j < kApplyItems; j++) {
+        if (deg[j] > 0) {
+          const unsigned pos = (unsigned)(run >> 32);
+          const int eb = (int)(run & 0xFFFFFFFFull);
+          ws.f_eb[pos] = eb;
+          ws.f_rs[pos] = rs[j];
+          f_msg[pos] = (APP == PGX_APP_SSSP) ? m[j] + 1u : m[j];
+          for (int64_t t = ((int64_t)eb + kTile - 1) / kTile; t * kTile < (int64_t)eb + deg[j]; t++)
+            ws.tile_src[t] = (int)pos;
+          run += (1ull << 32) | (unsigned long long)deg[j];
+        }
       }
     }
-    __syncthreads();
+    __syncthreads();  // s_list / s_gbase reuse
   }
   return bcast;
 }
@@ -529,7 +559,7 @@ struct MinRunParams {
 };
 
 template <int APP>
-__global__ void __launch_bounds__(kBlock, 2) min_run_kernel(MinRunParams p) {
+__global__ void __launch_bounds__(kBlock, PGX_MIN_BLOCKS) min_run_kernel(MinRunParams p) {
   extern __shared__ __align__(16) char smem[];
   __shared__ unsigned s_red[32];
   unsigned gen = 0;
@@ -626,7 +656,7 @@ __global__ void __launch_bounds__(kBlock, 2) min_run_kernel(MinRunParams p) {
     if (nrecip == 0 || s + 1 == p.max_steps) break;
 
     // ---- apply(s+1): consume + compute + frontier build ----
-    unsigned bc = apply_min_phase<APP>(p.row_ptr, p.val, mailbox, p.n, p.ws, &p.ws.ctr[s + 1]);
+    unsigned bc = apply_min_phase<APP>(p.row_ptr, p.val, mailbox, p.n, p.ws, &p.ws.ctr[s + 1], smem);
     bc = block_sum<unsigned>(bc, s_red);
     if (threadIdx.x == 0 && bc) atomicAdd(&p.ws.ctr[s + 1].bcast, bc);
     grid_sync(p.ws.bar, gen);
@@ -649,7 +679,7 @@ struct PrRunParams {
   int64_t *stats;
 };
 
-__global__ void __launch_bounds__(kBlock, 2) pagerank_run_kernel(PrRunParams p) {
+__global__ void __launch_bounds__(kBlock, PGX_MIN_BLOCKS) pagerank_run_kernel(PrRunParams p) {
   extern __shared__ __align__(16) char smem[];
   __shared__ double s_red[32];
   __shared__ unsigned long long s_ured[32];
