@@ -44,6 +44,7 @@ extern "C" {
 #define PGX_APP_PAGERANK 0
 #define PGX_APP_CC 1
 #define PGX_APP_SSSP 2
+#define PGX_APP_PAGERANK_PULL 3   /* pagerank in the reference's pull mode */
 
 /* combine operators (mailbox.py:58-70 min_combine / sum_combine) */
 #define PGX_OP_MIN_U32 0
@@ -131,6 +132,19 @@ int pgx_pagerank_run(int32_t n, int64_t m, const int32_t *row_ptr,
                      double r0, int32_t max_supersteps, double *rank,
                      void *run_ws, size_t run_ws_bytes, int64_t *stats,
                      uintptr_t stream);
+
+/* pagerank(iterations, damping) in pull mode -- the reference's own comm
+ * mode for PR (algorithms.py:80; fold engine.py:425-457): every vertex
+ * folds its in-neighbours' shares, no atomics.  Needs the in-CSR
+ * (in_row_ptr / in_col, rows sorted by source id) and its graph workspace
+ * from pgx_graph_prepare(in_row_ptr); row_ptr gives the out-degrees. */
+int pgx_pagerank_pull_run(int32_t n, int64_t m, const int32_t *row_ptr,
+                          const int32_t *in_row_ptr, const int32_t *in_col,
+                          const void *in_graph_ws, int32_t iterations,
+                          double damping, double base, double r0,
+                          int32_t max_supersteps, double *rank, void *run_ws,
+                          size_t run_ws_bytes, int64_t *stats,
+                          uintptr_t stream);
 
 /* ---------------------------------------------------------------- */
 /* R-MAT input generator; input construction only.    */

@@ -18,7 +18,7 @@ LIB_PATH = os.environ.get("PGX_LIB") or os.path.join(PKG_DIR, "libpgx.so")
 
 PGX_ABI_VERSION = 1
 PGX_OK, PGX_EINVAL, PGX_ECUDA, PGX_ENOMEM = 0, -1, -2, -3
-PGX_APP_PAGERANK, PGX_APP_CC, PGX_APP_SSSP = 0, 1, 2
+PGX_APP_PAGERANK, PGX_APP_CC, PGX_APP_SSSP, PGX_APP_PAGERANK_PULL = 0, 1, 2, 3
 PGX_OP_MIN_U32, PGX_OP_SUM_F64 = 0, 1
 PGX_STAT_HDR, PGX_STAT_FIELDS = 4, 8
 PGX_OPT_READ_FILTER, PGX_OPT_CTAS_PER_SM = 0, 1
@@ -33,7 +33,7 @@ EXPORTS = (
     "pgx_abi_version", "pgx_last_error", "pgx_set_option", "pgx_device_sm_count",
     "pgx_offsets_to_i32", "pgx_graph_workspace_bytes", "pgx_graph_prepare",
     "pgx_run_workspace_bytes", "pgx_sssp_run", "pgx_cc_run",
-    "pgx_pagerank_run", "pgx_rmat_keys",
+    "pgx_pagerank_run", "pgx_pagerank_pull_run", "pgx_rmat_keys",
 )
 
 _lib = None
@@ -59,6 +59,8 @@ _SIGS = {
     "pgx_cc_run": (ctypes.c_int, [_i32, _i64, _p, _p, _p, _i32, _p, _p, _sz, _p, _up]),
     "pgx_pagerank_run": (ctypes.c_int, [_i32, _i64, _p, _p, _p, _i32, _f64, _f64, _f64,
                                         _i32, _p, _p, _sz, _p, _up]),
+    "pgx_pagerank_pull_run": (ctypes.c_int, [_i32, _i64, _p, _p, _p, _p, _i32, _f64, _f64,
+                                             _f64, _i32, _p, _p, _sz, _p, _up]),
     "pgx_rmat_keys": (ctypes.c_int, [_i32, _i64, _i64, _f64, _f64, _f64, _u64, _i32,
                                      _i64, _i64, _p, _i64, _p, _up]),
 }

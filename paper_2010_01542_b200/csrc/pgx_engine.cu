@@ -113,6 +113,14 @@ __device__ __forceinline__ uint64_t evict_first_policy() {
 
 __device__ __forceinline__ unsigned lane_id() { return threadIdx.x & 31u; }
 
+__device__ __forceinline__ void red_min_u32(uint32_t *p, uint32_t v) {
+  asm volatile("red.relaxed.gpu.global.min.u32 [%0], %1;" :: "l"(p), "r"(v) : "memory");
+}
+
+__device__ __forceinline__ void red_or_b32(uint32_t *p, uint32_t v) {
+  asm volatile("red.relaxed.gpu.global.or.b32 [%0], %1;" :: "l"(p), "r"(v) : "memory");
+}
+
 __device__ __forceinline__ unsigned lanemask_lt() {
   unsigned m;
   asm("mov.u32 %0, %%lanemask_lt;" : "=r"(m));
@@ -220,7 +228,9 @@ struct RunWs {
   void *f_msg;             // [n]   frontier: message (u32) / PR share (f64)
   uint32_t *has;           // [n/32+1] has-message bitmask (first publishers)
   int32_t *tile_src;       // [ceil(m/kTile)+2] sparse tile map
-  void *mailbox;           // [n]   u32 (min) or f64 (sum)
+  void *mailbox;           // [n]   u32 (min) or f64 (sum); pull PR: folded sums
+  double *share2;          // pull PR: second share buffer
+  double *head, *tail;     // pull PR: per-tile partials of tile-spanning rows
 };
 
 size_t run_ws_layout(int app, int64_t n, int64_t m, int32_t max_steps, RunWs *ws,
@@ -231,7 +241,8 @@ size_t run_ws_layout(int app, int64_t n, int64_t m, int32_t max_steps, RunWs *ws
     off += align_up(bytes);
     return p;
   };
-  const size_t W = app == PGX_APP_PAGERANK ? 8 : 4;
+  const bool pr = app == PGX_APP_PAGERANK || app == PGX_APP_PAGERANK_PULL;
+  const size_t W = pr ? 8 : 4;
   RunWs w;
   w.bar = (GridBarrier *)take(64);
   w.ctr = (StepCounters *)take(sizeof(StepCounters) * (size_t)(max_steps + 2));
@@ -239,7 +250,13 @@ size_t run_ws_layout(int app, int64_t n, int64_t m, int32_t max_steps, RunWs *ws
   w.misc = (unsigned long long *)take(64);
   w.f_msg = take(W * (size_t)(n + 1));
   w.mailbox = take(W * (size_t)(n + 1));
-  if (app != PGX_APP_PAGERANK) {
+  w.share2 = w.head = w.tail = nullptr;
+  if (app == PGX_APP_PAGERANK_PULL) {
+    w.share2 = (double *)take(sizeof(double) * (size_t)(n + 1));
+    w.head = (double *)take(sizeof(double) * (size_t)(ceil_div(m, kTile) + 2));
+    w.tail = (double *)take(sizeof(double) * (size_t)(ceil_div(m, kTile) + 2));
+  }
+  if (!pr) {
     w.f_eb = (int32_t *)take(sizeof(int32_t) * (size_t)(n + 1));
     w.f_rs = (int32_t *)take(sizeof(int32_t) * (size_t)(n + 1));
     w.has = (uint32_t *)take(sizeof(uint32_t) * (size_t)(n / 32 + 2));
@@ -289,9 +306,8 @@ __host__ __device__ constexpr size_t scatter_smem(int op) {
 //   3. the 8 neighbour ids are streamed (L1::no_allocate, L2 evict_first),
 //      then combined (min: read-filter + atomicMin, first publisher sets
 //      the has-message bit; sum: red.add.f64).
-// Returns the number of first publications made by this thread.
 template <int OP, MsgSrc MS>
-__device__ unsigned scatter_phase(const ScatterArgs &a, char *smem, bool read_filter = true) {
+__device__ void scatter_phase(const ScatterArgs &a, char *smem, bool read_filter = true) {
   using Msg = typename std::conditional<OP == PGX_OP_SUM_F64, double, uint32_t>::type;
   constexpr bool kDense = MS != MsgSrc::kFrontier;
   const int lane = (int)lane_id();
@@ -305,7 +321,6 @@ __device__ unsigned scatter_phase(const ScatterArgs &a, char *smem, bool read_fi
   const unsigned upto = (lane == 31) ? 0xFFFFFFFFu : ((2u << lane) - 1u);
   const int64_t gwarp = (int64_t)blockIdx.x * kWarps + warp;
   const int64_t nwarps = (int64_t)gridDim.x * kWarps;
-  unsigned published = 0;
 
   for (int64_t t = gwarp; t < ntiles; t += nwarps) {
     const int64_t e0 = t * kTile;
@@ -358,9 +373,12 @@ __device__ unsigned scatter_phase(const ScatterArgs &a, char *smem, bool read_fi
         }
       }
       if (OP == PGX_OP_MIN_U32) {
-        // hybrid combiner: read-filter (mailbox.py:159 short-circuit), then
-        // one atomicMin; the unique lane that sees NEUTRAL come back is the
-        // first publisher (mailbox.py:190-199) and sets the has-message bit.
+        // hybrid combiner, fire-and-forget: read-filter (the mailbox.py:159
+        // short-circuit), then one red.min.u32.  Publication (mailbox.py:
+        // 190-199) becomes an idempotent has-message bit set by every lane
+        // whose filter read saw NEUTRAL: the lane whose atomic lands first
+        // on an empty slot necessarily read NEUTRAL, so no recipient is
+        // lost, and nothing waits on an atomic's return value.
         uint32_t *mb = reinterpret_cast<uint32_t *>(a.mailbox);
         uint32_t old[kPass];
 #pragma unroll
@@ -368,16 +386,9 @@ __device__ unsigned scatter_phase(const ScatterArgs &a, char *smem, bool read_fi
           old[r] = (w[r] >= 0) ? (read_filter ? mb[w[r]] : kNeutralMin) : 0u;
 #pragma unroll
         for (int r = 0; r < kPass; r++) {
-          if (w[r] >= 0 && (uint32_t)mv[r] < old[r])
-            old[r] = atomicMin(mb + w[r], (uint32_t)mv[r]);
-          else
-            old[r] = 0u;
-        }
-#pragma unroll
-        for (int r = 0; r < kPass; r++) {
-          if (old[r] == kNeutralMin) {
-            atomicOr(a.has + (w[r] >> 5), 1u << (w[r] & 31));
-            published++;
+          if (w[r] >= 0 && (uint32_t)mv[r] < old[r]) {
+            red_min_u32(mb + w[r], (uint32_t)mv[r]);
+            if (old[r] == kNeutralMin) red_or_b32(a.has + (w[r] >> 5), 1u << (w[r] & 31));
           }
         }
       } else {
@@ -388,7 +399,6 @@ __device__ unsigned scatter_phase(const ScatterArgs &a, char *smem, bool read_fi
       }
     }
   }
-  return published;
 }
 
 // ------------------------------------------------------------------
@@ -433,16 +443,24 @@ __device__ __forceinline__ unsigned long long block_excl_scan_u64(unsigned long 
 constexpr int kApplyWords = 64;
 constexpr int kApplyItems = kApplyWords * 32 / kBlock;  // 4
 
+// Returns (recipients counted) << 32 | (broadcasts) for this thread.  With
+// `count_only` the bitmask is only counted (superstep cap reached: the
+// pending messages must stay unconsumed, engine.py:299-300).
 template <int APP>
-__device__ unsigned apply_min_phase(const int32_t *__restrict__ row_ptr, uint32_t *val,
-                                    uint32_t *mailbox, int32_t n, const RunWs &ws,
-                                    StepCounters *ctr, char *smem) {
+__device__ unsigned long long apply_min_phase(const int32_t *__restrict__ row_ptr, uint32_t *val,
+                                              uint32_t *mailbox, int32_t n, const RunWs &ws,
+                                              StepCounters *ctr, char *smem, bool count_only) {
   __shared__ unsigned long long s_w[33];
   __shared__ unsigned long long s_gbase;
   int32_t *s_list = reinterpret_cast<int32_t *>(smem);  // kApplyWords * 32 ids
   uint32_t *f_msg = reinterpret_cast<uint32_t *>(ws.f_msg);
   const int words = (n + 31) >> 5;
-  unsigned bcast = 0;
+  unsigned bcast = 0, recips = 0;
+  if (count_only) {
+    for (int wi = blockIdx.x * kBlock + threadIdx.x; wi < words; wi += gridDim.x * kBlock)
+      recips += __popc(ws.has[wi]);
+    return ((unsigned long long)recips << 32);
+  }
   for (int base = blockIdx.x * kApplyWords; base < words; base += gridDim.x * kApplyWords) {
     // ---- expand the chunk's set bits into s_list (vertex order) ----
     uint32_t word = 0;
@@ -451,6 +469,7 @@ __device__ unsigned apply_min_phase(const int32_t *__restrict__ row_ptr, uint32_
       word = ws.has[wi];
       if (word) ws.has[wi] = 0u;
     }
+    recips += __popc(word);
     unsigned long long tot64;
     const int off = (int)block_excl_scan_u64((unsigned long long)__popc(word), s_w, &tot64);
     const int T = (int)tot64;
@@ -524,7 +543,7 @@ __device__ unsigned apply_min_phase(const int32_t *__restrict__ row_ptr, uint32_
     }
     __syncthreads();  // s_list / s_gbase reuse
   }
-  return bcast;
+  return ((unsigned long long)recips << 32) | bcast;
 }
 
 __device__ __forceinline__ void record_step(int64_t *stats, int s, int64_t active,
@@ -601,12 +620,11 @@ __global__ void __launch_bounds__(kBlock, PGX_MIN_BLOCKS) min_run_kernel(MinRunP
   if (gtid == 0) p.stats[PGX_STAT_HDR + 7] = (int64_t)globaltimer();
 
   for (int s = 0;; s++) {
-    // ---- scatter(s) ----
+    // ---- scatter(s): senders push along out-edges into the mailbox ----
     ScatterArgs a;
     a.col = p.col;
     a.mailbox = mailbox;
     a.has = p.ws.has;
-    unsigned pub;
     if (APP == PGX_APP_CC && s == 0) {
       a.eb = p.g.nz_eb;
       a.rs = nullptr;
@@ -615,7 +633,7 @@ __global__ void __launch_bounds__(kBlock, PGX_MIN_BLOCKS) min_run_kernel(MinRunP
       a.tile_src = p.g.tile_src;
       a.nsrc = p.g.hdr[0];
       a.E = p.m;
-      pub = scatter_phase<PGX_OP_MIN_U32, MsgSrc::kSourceId>(a, smem, p.read_filter);
+      scatter_phase<PGX_OP_MIN_U32, MsgSrc::kSourceId>(a, smem, p.read_filter);
     } else {
       const unsigned long long packed = p.ws.ctr[s].packed;
       a.eb = p.ws.f_eb;
@@ -625,17 +643,29 @@ __global__ void __launch_bounds__(kBlock, PGX_MIN_BLOCKS) min_run_kernel(MinRunP
       a.tile_src = p.ws.tile_src;
       a.nsrc = (int32_t)(packed >> 32);
       a.E = (int64_t)(packed & 0xFFFFFFFFull);
-      pub = scatter_phase<PGX_OP_MIN_U32, MsgSrc::kFrontier>(a, smem, p.read_filter);
+      scatter_phase<PGX_OP_MIN_U32, MsgSrc::kFrontier>(a, smem, p.read_filter);
     }
-    pub = block_sum<unsigned>(pub, s_red);
-    if (threadIdx.x == 0 && pub) atomicAdd(&p.ws.ctr[s].recip, pub);
     if (blockIdx.x == 0 && threadIdx.x == 0) {
       StepCounters z = {};
       p.ws.ctr[s + 1] = z;
     }
     grid_sync(p.ws.bar, gen);
+    const uint64_t t_scatter = globaltimer();
 
-    // ---- halt test (engine.py:288-300) ----
+    // ---- apply(s+1): consume + compute + frontier build; at the cap the
+    //      pending messages are only counted (engine.py:299-300) ----
+    const bool at_cap = (s + 1 == p.max_steps);
+    const unsigned long long rb =
+        apply_min_phase<APP>(p.row_ptr, p.val, mailbox, p.n, p.ws, &p.ws.ctr[s + 1], smem, at_cap);
+    const unsigned bc = block_sum<unsigned>((unsigned)(rb & 0xFFFFFFFFull), s_red);
+    const unsigned rc = block_sum<unsigned>((unsigned)(rb >> 32), s_red);
+    if (threadIdx.x == 0) {
+      if (bc) atomicAdd(&p.ws.ctr[s + 1].bcast, bc);
+      if (rc) atomicAdd(&p.ws.ctr[s].recip, rc);
+    }
+    grid_sync(p.ws.bar, gen);
+
+    // ---- stats + halt test (engine.py:284-300) ----
     const unsigned nrecip = p.ws.ctr[s].recip;
     if (blockIdx.x == 0 && threadIdx.x == 0) {
       const StepCounters c = p.ws.ctr[s];
@@ -646,22 +676,18 @@ __global__ void __launch_bounds__(kBlock, PGX_MIN_BLOCKS) min_run_kernel(MinRunP
       record_step(p.stats, s, active, sent, edges,
                   (APP == PGX_APP_CC && s == 0) ? (int64_t)p.g.hdr[0] : senders, nrecip,
                   (int64_t)c.bcast);
+      p.stats[PGX_STAT_HDR + (int64_t)s * PGX_STAT_FIELDS + 5] = (int64_t)t_scatter;
+      // scatter(s+1) starts after this barrier: field 7 of step s+1
+      if (!at_cap)
+        p.stats[PGX_STAT_HDR + (int64_t)(s + 1) * PGX_STAT_FIELDS + 7] = (int64_t)globaltimer();
       if (nrecip == 0) {
         p.stats[0] = s + 1;
-      } else if (s + 1 == p.max_steps) {
+      } else if (at_cap) {
         p.stats[0] = s + 1;
         p.stats[1] = 1;
       }
     }
-    if (nrecip == 0 || s + 1 == p.max_steps) break;
-
-    // ---- apply(s+1): consume + compute + frontier build ----
-    unsigned bc = apply_min_phase<APP>(p.row_ptr, p.val, mailbox, p.n, p.ws, &p.ws.ctr[s + 1], smem);
-    bc = block_sum<unsigned>(bc, s_red);
-    if (threadIdx.x == 0 && bc) atomicAdd(&p.ws.ctr[s + 1].bcast, bc);
-    grid_sync(p.ws.bar, gen);
-    if (blockIdx.x == 0 && threadIdx.x == 0)  // apply(s+1) end = scatter(s+1) start
-      p.stats[PGX_STAT_HDR + (int64_t)(s + 1) * PGX_STAT_FIELDS + 7] = (int64_t)globaltimer();
+    if (nrecip == 0 || at_cap) break;
   }
 }
 
@@ -771,6 +797,238 @@ __global__ void __launch_bounds__(kBlock, PGX_MIN_BLOCKS) pagerank_run_kernel(Pr
     if (s == last || cap) break;
     scatter_phase<PGX_OP_SUM_F64, MsgSrc::kShareById>(a, smem);
     grid_sync(p.ws.bar, gen);
+  }
+}
+
+// ------------------------------------------------------------------
+// pull-mode PageRank: the reference's own communication mode for PR
+// (algorithms.py:80, engine.py:425-457).  A vertex folds the shares of its
+// in-neighbours; no atomics at all.  The in-CSR edge space is walked in
+// the same 256-edge warp tiles as the scatter (exact edge balance), with
+// a segmented warp scan per 32-edge round.  Rows that fit in one tile are
+// summed in-register and stored; rows spanning tiles leave per-tile
+// partials (tail of the first tile, head of every later tile) that the
+// apply combines in tile order -- deterministic for a fixed tiling.
+// ------------------------------------------------------------------
+
+struct GatherArgs {
+  const int32_t *in_col;
+  const int32_t *eb;        // in-row starts of vertices with in-degree > 0
+  const int32_t *ids;       // those vertices
+  const int32_t *tile_src;  // in-edge tile map
+  int32_t nsrc;
+  int64_t E;
+  const double *share;      // shares broadcast last superstep
+  double *folded, *head, *tail;
+};
+
+__device__ void gather_phase(const GatherArgs &a, char *smem) {
+  const int lane = (int)lane_id();
+  const int warp = threadIdx.x >> 5;
+  int32_t *s_eb = reinterpret_cast<int32_t *>(smem) + warp * kSlots;
+  int32_t *s_id = reinterpret_cast<int32_t *>(smem) + kWarps * kSlots + warp * kSlots;
+  const uint64_t pol = evict_first_policy();
+  const int64_t ntiles = (a.E + kTile - 1) / kTile;
+  const unsigned upto = (lane == 31) ? 0xFFFFFFFFu : ((2u << lane) - 1u);
+  const int64_t gwarp = (int64_t)blockIdx.x * kWarps + warp;
+  const int64_t nwarps = (int64_t)gridDim.x * kWarps;
+
+  for (int64_t t = gwarp; t < ntiles; t += nwarps) {
+    const int64_t e0 = t * kTile;
+    const int64_t e1 = min(a.E, e0 + kTile);
+    const int i0 = a.tile_src[t];
+    const int i1 = (t + 1 < ntiles) ? a.tile_src[t + 1] : a.nsrc - 1;
+    const int k = i1 - i0 + 1;
+    __syncwarp();
+    for (int j = lane; j <= k; j += 32) {
+      const int i = i0 + j;
+      if (j < k) {
+        s_eb[j] = a.eb[i];
+        s_id[j] = a.ids[i];
+      } else {
+        s_eb[j] = (i < a.nsrc) ? a.eb[i] : (int32_t)a.E;
+      }
+    }
+    __syncwarp();
+    const bool first_open = (int64_t)s_eb[0] < e0;  // row began in an earlier tile
+    // pass 1: segment of every lane in every round + neighbour ids (8 loads
+    // in flight); pass 2: the 8 share gathers; pass 3: segmented scans.
+    int seg[kItems], col[kItems];
+    int cur = 0;
+#pragma unroll
+    for (int r = 0; r < kItems; r++) {
+      const int64_t base = e0 + r * 32;
+      const int64_t e = base + lane;
+      const int ci = cur + 1 + lane;
+      unsigned bit = 0;
+      if (ci <= k) {
+        const int64_t pp = (int64_t)s_eb[ci] - base;
+        if (pp >= 0 && pp < 32) bit = 1u << pp;
+      }
+      const unsigned bm = __reduce_or_sync(0xFFFFFFFFu, bit);
+      seg[r] = (e < e1) ? cur + __popc(bm & upto) : (1 << 30);
+      cur += __popc(bm);
+      col[r] = (e < e1) ? ld_stream(a.in_col + e, pol) : -1;
+    }
+    double x[kItems];
+#pragma unroll
+    for (int r = 0; r < kItems; r++) x[r] = (col[r] >= 0) ? __ldg(a.share + col[r]) : 0.0;
+    int carry_seg = -1;
+    double carry = 0.0;
+#pragma unroll
+    for (int r = 0; r < kItems; r++) {
+      const int64_t e = e0 + r * 32 + lane;
+      const bool valid = col[r] >= 0;
+      double v = x[r];
+      const int sg = seg[r];
+      // segmented inclusive scan (segments are contiguous lane ranges)
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const double y = __shfl_up_sync(0xFFFFFFFFu, v, o);
+        const int so = __shfl_up_sync(0xFFFFFFFFu, sg, o);
+        if (lane >= o && so == sg) v = __dadd_rn(v, y);
+      }
+      const int seg_next = __shfl_down_sync(0xFFFFFFFFu, sg, 1);
+      const bool is_end = valid && (lane == 31 || seg_next != sg);
+      const double total = (sg == carry_seg) ? __dadd_rn(carry, v) : v;
+      bool cont = false;
+      if (is_end) {
+        const int64_t nb = s_eb[sg + 1];  // first edge of the next row
+        if (e + 1 == nb || e + 1 == e1) {  // row ends here, or the tile does
+          if (sg == 0 && first_open) a.head[t] = total;
+          else if (e + 1 == nb) a.folded[s_id[sg]] = total;
+          else a.tail[t] = total;
+        } else {
+          cont = true;  // lane 31: row continues into the next round
+        }
+      }
+      const unsigned cm = __ballot_sync(0xFFFFFFFFu, cont);
+      carry = __shfl_sync(0xFFFFFFFFu, total, 31);
+      carry_seg = cm ? __shfl_sync(0xFFFFFFFFu, sg, 31) : -1;
+    }
+  }
+}
+
+struct PrPullParams {
+  int32_t n;
+  int64_t m;
+  const int32_t *row_ptr;     // out-CSR offsets (out-degrees)
+  const int32_t *in_row_ptr;  // in-CSR offsets
+  const int32_t *in_col;
+  GraphWs gin;                // tile map / nz list of the in-CSR
+  RunWs ws;
+  double *rank;
+  int32_t iterations;
+  double damping, base, r0;
+  int32_t max_steps;
+  int64_t *stats;
+};
+
+__global__ void __launch_bounds__(kBlock, PGX_MIN_BLOCKS) pagerank_pull_kernel(PrPullParams p) {
+  extern __shared__ __align__(16) char smem[];
+  __shared__ double s_red[32];
+  __shared__ unsigned long long s_ured[32];
+  __shared__ double s_dangling;
+  unsigned gen = 0;
+  double *folded = reinterpret_cast<double *>(p.ws.mailbox);
+  double *share_cur = reinterpret_cast<double *>(p.ws.f_msg);
+  double *share_nxt = p.ws.share2;
+  const unsigned nthreads = gridDim.x * blockDim.x;
+  const unsigned gtid = blockIdx.x * blockDim.x + threadIdx.x;
+  const int last = p.iterations - 1;
+  const double dn_n = (double)p.n;
+
+  // ---- setup (algorithms.py:44-59): rank = r0, seed shares r0/outdeg ----
+  unsigned long long my_dangling = 0;
+  for (unsigned v = gtid; v < (unsigned)p.n; v += nthreads) {
+    const int deg = p.row_ptr[v + 1] - p.row_ptr[v];
+    p.rank[v] = p.r0;
+    share_cur[v] = deg ? __ddiv_rn(p.r0, (double)deg) : 0.0;
+    my_dangling += deg ? 0ull : 1ull;
+  }
+  unsigned long long bd = block_sum<unsigned long long>(my_dangling, s_ured);
+  if (threadIdx.x == 0) {
+    if (bd) atomicAdd(&p.ws.misc[0], bd);
+    if (blockIdx.x == 0) {
+      p.stats[0] = p.stats[1] = 0;
+      p.stats[2] = gridDim.x;
+      p.stats[3] = (int64_t)globaltimer();
+    }
+  }
+  grid_sync(p.ws.bar, gen);
+  const unsigned long long ndangling = p.ws.misc[0];
+  double dangling = __dmul_rn(p.r0, (double)ndangling);  // algorithms.py:55
+  const int64_t nspread = (int64_t)p.n - (int64_t)ndangling;
+
+  GatherArgs g;
+  g.in_col = p.in_col;
+  g.eb = p.gin.nz_eb;
+  g.ids = p.gin.nz_id;
+  g.tile_src = p.gin.tile_src;
+  g.nsrc = p.gin.hdr[0];
+  g.E = p.m;
+  g.folded = folded;
+  g.head = p.ws.head;
+  g.tail = p.ws.tail;
+
+  for (int s = 0;; s++) {
+    if (blockIdx.x == 0 && threadIdx.x == 0)
+      p.stats[PGX_STAT_HDR + (int64_t)s * PGX_STAT_FIELDS + 7] = (int64_t)globaltimer();
+    // ---- fold (engine.py:425-457): in-neighbour shares of last superstep
+    g.share = share_cur;
+    gather_phase(g, smem);
+    grid_sync(p.ws.bar, gen);
+    const uint64_t t_fold = globaltimer();
+
+    // ---- compute (algorithms.py:61-73): rank, next share, dangling mass
+    const double dn = __ddiv_rn(dangling, dn_n);
+    double my_d = 0.0;
+    for (unsigned v = gtid; v < (unsigned)p.n; v += nthreads) {
+      const int es = p.in_row_ptr[v], ee = p.in_row_ptr[v + 1];
+      double f = 0.0;
+      if (ee > es) {
+        const int64_t t0 = es / kTile, t1 = (ee - 1) / kTile;
+        if (t0 == t1) {
+          f = folded[v];
+        } else {
+          f = p.ws.tail[t0];
+          for (int64_t t = t0 + 1; t <= t1; t++) f = __dadd_rn(f, p.ws.head[t]);
+        }
+      }
+      const double r = __dadd_rn(p.base, __dmul_rn(p.damping, __dadd_rn(f, dn)));
+      p.rank[v] = r;
+      const int deg = p.row_ptr[v + 1] - p.row_ptr[v];
+      if (deg == 0) my_d = __dadd_rn(my_d, r);
+      else if (s != last) share_nxt[v] = __ddiv_rn(r, (double)deg);
+    }
+    const double bsum = block_sum<double>(my_d, s_red);
+    if (threadIdx.x == 0) p.ws.partials[blockIdx.x] = bsum;
+    grid_sync(p.ws.bar, gen);
+
+    // ---- on_superstep_end (algorithms.py:75-78): dangling mass ----
+    {
+      double acc = 0.0;
+      for (int b = threadIdx.x; b < (int)gridDim.x; b += kBlock) acc = __dadd_rn(acc, p.ws.partials[b]);
+      const double tot = block_sum<double>(acc, s_red);
+      if (threadIdx.x == 0) s_dangling = tot;
+      __syncthreads();
+      dangling = s_dangling;
+    }
+    const bool cap = (s + 1 == p.max_steps);
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+      record_step(p.stats, s, p.n, (s == last) ? 0 : nspread, p.m, nspread, p.n,
+                  (s == last) ? 0 : nspread);
+      p.stats[PGX_STAT_HDR + (int64_t)s * PGX_STAT_FIELDS + 5] = (int64_t)globaltimer();
+      (void)t_fold;
+      if (s == last || cap) {
+        p.stats[0] = s + 1;
+        p.stats[1] = (s == last) ? 0 : 1;
+      }
+    }
+    if (s == last || cap) break;
+    double *tmp = share_cur;
+    share_cur = share_nxt;
+    share_nxt = tmp;
   }
 }
 
@@ -992,7 +1250,7 @@ int pgx_graph_prepare(int32_t n, int64_t m, const int32_t *row_ptr, void *graph_
 
 int pgx_run_workspace_bytes(int app, int64_t n, int64_t m, int32_t max_supersteps,
                             size_t *bytes) {
-  if (!bytes || n < 0 || m < 0 || max_supersteps < 1 || app < 0 || app > 2)
+  if (!bytes || n < 0 || m < 0 || max_supersteps < 1 || app < 0 || app > 3)
     return fail(PGX_EINVAL, "bad run workspace arguments");
   *bytes = run_ws_layout(app, n, m, max_supersteps, nullptr, nullptr);
   return PGX_OK;
@@ -1087,6 +1345,47 @@ int pgx_pagerank_run(int32_t n, int64_t m, const int32_t *row_ptr, const int32_t
   if (rc) return rc;
   void *args[] = {&p};
   PGX_CUDA(cudaLaunchCooperativeKernel((void *)pagerank_run_kernel, grid, kBlock, args, smem, st));
+  return PGX_OK;
+}
+
+int pgx_pagerank_pull_run(int32_t n, int64_t m, const int32_t *row_ptr,
+                          const int32_t *in_row_ptr, const int32_t *in_col,
+                          const void *in_graph_ws, int32_t iterations, double damping,
+                          double base, double r0, int32_t max_supersteps, double *rank,
+                          void *run_ws, size_t run_ws_bytes, int64_t *stats, uintptr_t stream) {
+  int rc = check_graph(n, m, in_row_ptr, in_col, in_graph_ws);
+  if (rc) return rc;
+  if (!row_ptr) return fail(PGX_EINVAL, "null out-CSR offsets");
+  if (iterations < 1) return fail(PGX_EINVAL, "iterations must be >= 1");
+  if (!(damping >= 0.0 && damping <= 1.0)) return fail(PGX_EINVAL, "damping must be in [0, 1]");
+  if (max_supersteps < 1) return fail(PGX_EINVAL, "superstep cap must be >= 1");
+  if (!rank || !run_ws || !stats) return fail(PGX_EINVAL, "null output pointer");
+  PrPullParams p;
+  p.n = n;
+  p.m = m;
+  p.row_ptr = row_ptr;
+  p.in_row_ptr = in_row_ptr;
+  p.in_col = in_col;
+  graph_ws_layout(n, m, &p.gin, (char *)in_graph_ws);
+  if (run_ws_layout(PGX_APP_PAGERANK_PULL, n, m, max_supersteps, &p.ws, (char *)run_ws) >
+      run_ws_bytes)
+    return fail(PGX_ENOMEM, "run workspace too small");
+  p.rank = rank;
+  p.iterations = iterations;
+  p.damping = damping;
+  p.base = base;
+  p.r0 = r0;
+  p.max_steps = max_supersteps;
+  p.stats = stats;
+  cudaStream_t st = (cudaStream_t)stream;
+  PGX_CUDA(cudaMemsetAsync(p.ws.bar, 0, 64, st));
+  PGX_CUDA(cudaMemsetAsync(p.ws.misc, 0, 64, st));
+  const size_t smem = (size_t)kWarps * kSlots * 8 + 16;
+  int grid = 0;
+  rc = coop_grid(pagerank_pull_kernel, smem, &grid);
+  if (rc) return rc;
+  void *args[] = {&p};
+  PGX_CUDA(cudaLaunchCooperativeKernel((void *)pagerank_pull_kernel, grid, kBlock, args, smem, st));
   return PGX_OK;
 }
 

@@ -72,6 +72,9 @@ class EngineConfig:
     max_supersteps: int = DEFAULT_MAX_SUPERSTEPS
     validate_phases: bool = False
     device: int | None = None
+    #: PageRank lowering: "pull" (the reference's comm mode, algorithms.py:80;
+    #: in-neighbour fold, no atomics) or "push" (scatter with red.add.f64)
+    pagerank_mode: str = "pull"
 
 
 @dataclass(frozen=True)
@@ -150,6 +153,8 @@ def _validate(program: VertexProgram, config: EngineConfig) -> None:
         raise ConfigError(f"bad layout mode: {config.layout!r}")
     if not isinstance(config.combiner, CombinerKind):
         raise ConfigError(f"bad combiner kind: {config.combiner!r}")
+    if config.pagerank_mode not in ("pull", "push"):
+        raise ConfigError(f"bad pagerank_mode: {config.pagerank_mode!r}")
     if program.comm_mode is CommMode.PUSH and program.combine is None:
         raise ConfigError("push-mode programs must declare a combine function")
     if config.combiner is CombinerKind.CAS and program.comm_mode is CommMode.PUSH \
@@ -209,13 +214,25 @@ class LaunchPlan:
     max_steps: int
     low: dict
     stream: Any
+    pull: bool = False
 
     def launch(self) -> None:
         """Enqueue the persistent run kernel (asynchronous)."""
         lib = _lib.load()
         c = self.csr
         sp = self.stream.cuda_stream
-        if self.app == "pagerank":
+        if self.app == "pagerank" and self.pull:
+            it, d = self.low["iterations"], self.low["damping"]
+            base = (1.0 - d) / c.n      # algorithms.py:49 (host float math)
+            r0 = 1.0 / c.n              # algorithms.py:50
+            rc = lib.pgx_pagerank_pull_run(c.n, c.m, c.row_ptr.data_ptr(),
+                                           c.in_row_ptr.data_ptr(), c.in_col.data_ptr(),
+                                           c.in_ws.data_ptr(), it, d, base, r0,
+                                           self.max_steps, self.values.data_ptr(),
+                                           self.ws.data_ptr(), self.ws_bytes,
+                                           self.stats.data_ptr(), sp)
+            _lib.check(rc, "pgx_pagerank_pull_run")
+        elif self.app == "pagerank":
             it, d = self.low["iterations"], self.low["damping"]
             base = (1.0 - d) / c.n      # algorithms.py:49 (host float math)
             r0 = 1.0 / c.n              # algorithms.py:50
@@ -258,16 +275,20 @@ def plan_run(graph: Graph, program: VertexProgram,
     lib = _lib.load()
     app = low["app"]
     max_steps = int(config.max_supersteps)
+    pull = app == "pagerank" and config.pagerank_mode == "pull"
     if app == "pagerank":
         max_steps = min(max_steps, int(low["iterations"]))
-    ws_bytes = _lib.out_size(lib.pgx_run_workspace_bytes, _APP_ID[app], n, m, max_steps)
+    if pull:
+        csr.ensure_transpose(stream)
+    app_id = _lib.PGX_APP_PAGERANK_PULL if pull else _APP_ID[app]
+    ws_bytes = _lib.out_size(lib.pgx_run_workspace_bytes, app_id, n, m, max_steps)
     with torch.cuda.device(dev):
         ws = torch.empty(ws_bytes, dtype=torch.uint8, device=dev)
         stats = torch.zeros(_lib.PGX_STAT_HDR + _lib.PGX_STAT_FIELDS * max_steps,
                             dtype=torch.int64, device=dev)
         vdt = torch.float64 if app == "pagerank" else torch.int32
         values = torch.empty(n, dtype=vdt, device=dev)
-    return LaunchPlan(app, csr, values, stats, ws, ws_bytes, max_steps, low, stream)
+    return LaunchPlan(app, csr, values, stats, ws, ws_bytes, max_steps, low, stream, pull)
 
 
 def collect(plan: LaunchPlan, program: VertexProgram, wall: float | None = None) -> RunReport:

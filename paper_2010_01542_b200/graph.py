@@ -54,6 +54,36 @@ class DeviceCSR:
     col_idx: torch.Tensor   # int32 [m]
     ws: torch.Tensor        # uint8 per-graph workspace (tile map, nz list)
     h2d_bytes: int          # bytes copied host->device to build it
+    in_row_ptr: torch.Tensor | None = None   # int32 [n+1] transpose (pull mode)
+    in_col: torch.Tensor | None = None       # int32 [m], rows sorted by source
+    in_ws: torch.Tensor | None = None        # tile map of the transpose
+
+    def ensure_transpose(self, stream=None) -> None:
+        """Build the in-CSR on the device (sort by (dst, src)), once."""
+        if self.in_row_ptr is not None:
+            return
+        dev = self.row_ptr.device
+        st = torch.cuda.current_stream(dev) if stream is None else stream
+        lib = _lib.load()
+        with torch.cuda.device(dev), torch.cuda.stream(st):
+            n, m = self.n, self.m
+            deg = torch.diff(self.row_ptr.to(torch.int64))
+            src = torch.repeat_interleave(torch.arange(n, device=dev, dtype=torch.int64),
+                                          deg, output_size=m)
+            key = (self.col_idx.to(torch.int64) << 32) | src
+            del src
+            key, _ = torch.sort(key)
+            dst = key >> 32
+            in_row_ptr = torch.zeros(n + 1, dtype=torch.int32, device=dev)
+            in_row_ptr[1:] = torch.cumsum(torch.bincount(dst, minlength=n), 0).to(torch.int32)
+            del dst
+            in_col = (key & 0xFFFFFFFF).to(torch.int32)
+            del key
+            ws_bytes = _lib.out_size(lib.pgx_graph_workspace_bytes, n, m)
+            ws = torch.empty(ws_bytes, dtype=torch.uint8, device=dev)
+            _lib.check(lib.pgx_graph_prepare(n, m, in_row_ptr.data_ptr(), ws.data_ptr(),
+                                             ws_bytes, st.cuda_stream), "pgx_graph_prepare")
+        self.in_row_ptr, self.in_col, self.in_ws = in_row_ptr, in_col, ws
 
 
 class Graph:

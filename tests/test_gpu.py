@@ -49,11 +49,15 @@ def rel_err(got, want):
     return float(np.max(np.abs(got - want) / np.abs(want)))
 
 
+@pytest.mark.parametrize("mode", ["pull", "push"])
 @pytest.mark.parametrize("r", RUNS, ids=lambda r: r.id)
-def test_golden_reference_runs(r):
+def test_golden_reference_runs(r, mode):
+    if mode == "push" and r.app != "pagerank":
+        pytest.skip("pagerank_mode only changes the PageRank lowering")
     g = pgx.from_edges(r.src, r.dst, r.n, undirected=r.undirected, device="cuda")
     cap = r.kwargs.get("max_supersteps")
-    cfg = pgx.EngineConfig(max_supersteps=cap) if cap else pgx.EngineConfig()
+    cfg = pgx.EngineConfig(max_supersteps=cap if cap else pgx.DEFAULT_MAX_SUPERSTEPS,
+                           pagerank_mode=mode)
     rep = pgx.run(g, program(r.app, r.kwargs), cfg)
     if r.app == "pagerank":
         assert rep.values.dtype == np.float64
@@ -139,6 +143,8 @@ def test_repeat_runs_deterministic():
             [s.active_count for s in b.supersteps]
     p = pgx.run(g, pgx.pagerank()).values
     q = pgx.run(g, pgx.pagerank()).values
+    assert np.array_equal(p, q)  # pull mode: no atomics, fixed fold order
+    q = pgx.run(g, pgx.pagerank(), pgx.EngineConfig(pagerank_mode="push")).values
     assert rel_err(p, q) <= 1e-12
 
 
@@ -178,12 +184,13 @@ def test_gpu_rmat_matches_baseline_hashes(graphs, name):
     assert sha(g.out_targets, "<i4") == CSR_HASHES[name][1]
 
 
-def test_c1_pagerank_vs_oracle(graphs):
+@pytest.mark.parametrize("mode", ["pull", "push"])
+def test_c1_pagerank_vs_oracle(graphs, mode):
     g = graphs("C1")
     off = g.out_offsets.cpu().numpy()
     tgt = g.out_targets.cpu().numpy()
     want = O.run_pagerank(g.vertex_count, off, tgt)
-    rep = pgx.run(g, pgx.pagerank())
+    rep = pgx.run(g, pgx.pagerank(), pgx.EngineConfig(pagerank_mode=mode))
     assert rel_err(rep.values, want.values) <= PR_RTOL
     assert rep.superstep_count == 10
     assert [s.messages_sent for s in rep.supersteps] == [40_445] * 9 + [0]
@@ -218,9 +225,10 @@ def test_c3_sssp_known_answer(graphs):
         [97364, 36379100, 27861844, 339319, 2142, 6, 0]
 
 
-def test_c4_pagerank_vs_oracle(graphs):
+@pytest.mark.parametrize("mode", ["pull", "push"])
+def test_c4_pagerank_vs_oracle(graphs, mode):
     g = graphs("C4")
-    rep = pgx.run(g, pgx.pagerank())
+    rep = pgx.run(g, pgx.pagerank(), pgx.EngineConfig(pagerank_mode=mode))
     off = g.out_offsets.cpu().numpy()
     tgt = g.out_targets.cpu().numpy()
     want = O.run_pagerank(g.vertex_count, off, tgt)

@@ -20,7 +20,8 @@ for c in cfgs:
     app = {"C1": "pagerank", "C2": "components", "C3": "sssp", "C4": "pagerank", "C5": "components"}[c]
     prog = pgx.pagerank() if app == "pagerank" else pgx.connected_components() if app == "components" \
         else pgx.sssp(int(torch.argmax(g.out_degrees)))
-    plan = pgx.plan_run(g, prog)
+    mode = os.environ.get("PR_MODE", "pull")
+    plan = pgx.plan_run(g, prog, pgx.EngineConfig(pagerank_mode=mode))
     best = None
     for r in range(reps):
         s = torch.cuda.Event(enable_timing=True); e = torch.cuda.Event(enable_timing=True)
