@@ -105,6 +105,13 @@ __device__ __forceinline__ int ld_stream(const int *p, uint64_t pol) {
   return v;
 }
 
+__device__ __forceinline__ int4 ld_stream4(const int4 *p, uint64_t pol) {
+  int4 v;
+  asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.v4.s32 {%0, %1, %2, %3}, [%4], %5;"
+               : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "l"(p), "l"(pol));
+  return v;
+}
+
 __device__ __forceinline__ uint64_t evict_first_policy() {
   uint64_t pol;
   asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
@@ -851,60 +858,78 @@ __device__ void gather_phase(const GatherArgs &a, char *smem) {
     }
     __syncwarp();
     const bool first_open = (int64_t)s_eb[0] < e0;  // row began in an earlier tile
-    // pass 1: segment of every lane in every round + neighbour ids (8 loads
-    // in flight); pass 2: the 8 share gathers; pass 3: segmented scans.
-    int seg[kItems], col[kItems];
-    int cur = 0;
+    // Each lane owns 8 contiguous in-edges [a0, a1): two 16-byte id loads,
+    // 8 independent share gathers, a sequential per-row sum; one segmented
+    // warp scan per tile carries partial rows across lanes.
+    const int64_t a0 = e0 + 8 * lane;
+    const int64_t a1 = min(e1, a0 + 8);
+    const bool active = a0 < e1;
+    int col[8];
+    if (active && a1 - a0 == 8) {
+      const int4 c0 = ld_stream4(reinterpret_cast<const int4 *>(a.in_col + a0), pol);
+      const int4 c1 = ld_stream4(reinterpret_cast<const int4 *>(a.in_col + a0) + 1, pol);
+      col[0] = c0.x; col[1] = c0.y; col[2] = c0.z; col[3] = c0.w;
+      col[4] = c1.x; col[5] = c1.y; col[6] = c1.z; col[7] = c1.w;
+    } else {
 #pragma unroll
-    for (int r = 0; r < kItems; r++) {
-      const int64_t base = e0 + r * 32;
-      const int64_t e = base + lane;
-      const int ci = cur + 1 + lane;
-      unsigned bit = 0;
-      if (ci <= k) {
-        const int64_t pp = (int64_t)s_eb[ci] - base;
-        if (pp >= 0 && pp < 32) bit = 1u << pp;
-      }
-      const unsigned bm = __reduce_or_sync(0xFFFFFFFFu, bit);
-      seg[r] = (e < e1) ? cur + __popc(bm & upto) : (1 << 30);
-      cur += __popc(bm);
-      col[r] = (e < e1) ? ld_stream(a.in_col + e, pol) : -1;
+      for (int j = 0; j < 8; j++) col[j] = (a0 + j < a1) ? ld_stream(a.in_col + a0 + j, pol) : -1;
     }
-    double x[kItems];
+    double x[8];
 #pragma unroll
-    for (int r = 0; r < kItems; r++) x[r] = (col[r] >= 0) ? __ldg(a.share + col[r]) : 0.0;
-    int carry_seg = -1;
-    double carry = 0.0;
-#pragma unroll
-    for (int r = 0; r < kItems; r++) {
-      const int64_t e = e0 + r * 32 + lane;
-      const bool valid = col[r] >= 0;
-      double v = x[r];
-      const int sg = seg[r];
-      // segmented inclusive scan (segments are contiguous lane ranges)
-#pragma unroll
-      for (int o = 1; o < 32; o <<= 1) {
-        const double y = __shfl_up_sync(0xFFFFFFFFu, v, o);
-        const int so = __shfl_up_sync(0xFFFFFFFFu, sg, o);
-        if (lane >= o && so == sg) v = __dadd_rn(v, y);
+    for (int j = 0; j < 8; j++) x[j] = (col[j] >= 0) ? __ldg(a.share + col[j]) : 0.0;
+    // row holding a0: largest idx with s_eb[idx] <= a0
+    int cur = 0;
+    if (active) {
+      int hi = k;
+      while (hi - cur > 1) {
+        const int mid = (cur + hi) >> 1;
+        if ((int64_t)s_eb[mid] <= a0) cur = mid; else hi = mid;
       }
-      const int seg_next = __shfl_down_sync(0xFFFFFFFFu, sg, 1);
-      const bool is_end = valid && (lane == 31 || seg_next != sg);
-      const double total = (sg == carry_seg) ? __dadd_rn(carry, v) : v;
-      bool cont = false;
-      if (is_end) {
-        const int64_t nb = s_eb[sg + 1];  // first edge of the next row
-        if (e + 1 == nb || e + 1 == e1) {  // row ends here, or the tile does
-          if (sg == 0 && first_open) a.head[t] = total;
-          else if (e + 1 == nb) a.folded[s_id[sg]] = total;
-          else a.tail[t] = total;
+    }
+    const int first_seg = cur;
+    bool first_closed = false;
+    double first_part = 0.0, acc = 0.0;
+#pragma unroll
+    for (int j = 0; j <= 8; j++) {
+      const int64_t e = a0 + j;
+      if (!active || e > a1) break;
+      // close the current row if the next row starts at e (e == a1: range end)
+      if (cur + 1 <= k && (int64_t)s_eb[cur + 1] <= e) {
+        if (cur == first_seg) {
+          first_closed = true;
+          first_part = acc;
         } else {
-          cont = true;  // lane 31: row continues into the next round
+          a.folded[s_id[cur]] = acc;  // row lies inside this lane's range
         }
+        cur++;
+        acc = 0.0;
       }
-      const unsigned cm = __ballot_sync(0xFFFFFFFFu, cont);
-      carry = __shfl_sync(0xFFFFFFFFu, total, 31);
-      carry_seg = cm ? __shfl_sync(0xFFFFFFFFu, sg, 31) : -1;
+      if (e < a1) acc = __dadd_rn(acc, x[j]);
+    }
+    // segmented inclusive scan of the open-row partials, keyed by row
+    const int key = active ? cur : (1 << 30);
+    double v = active ? acc : 0.0;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const double y = __shfl_up_sync(0xFFFFFFFFu, v, o);
+      const int ko = __shfl_up_sync(0xFFFFFFFFu, key, o);
+      if (lane >= o && ko == key) v = __dadd_rn(y, v);
+    }
+    const double prev_v = __shfl_up_sync(0xFFFFFFFFu, v, 1);
+    const int prev_key = __shfl_up_sync(0xFFFFFFFFu, key, 1);
+    const double carry_in = (lane > 0 && prev_key == first_seg) ? prev_v : 0.0;
+    if (active) {
+      if (first_closed) {  // this lane ends a row that began to its left
+        const double tot = __dadd_rn(carry_in, first_part);
+        if (first_seg == 0 && first_open) a.head[t] = tot;
+        else a.folded[s_id[first_seg]] = tot;
+      }
+      if (a1 == e1 && cur < k && (int64_t)s_eb[cur] < e1) {
+        // the tile ends inside row `cur`, which continues into the next tile
+        const double tot = (cur == first_seg) ? __dadd_rn(carry_in, acc) : acc;
+        if (cur == 0 && first_open) a.head[t] = tot;
+        else a.tail[t] = tot;
+      }
     }
   }
 }
