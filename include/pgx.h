@@ -160,6 +160,20 @@ int pgx_rmat_keys(int32_t scale, int64_t first_draw, int64_t num_draws,
                   uint64_t *keys, int64_t capacity, int64_t *count,
                   uintptr_t stream);
 
+/* ---------------------------------------------------------------- */
+/* scattered-access ceilings (SURVEY.md 8(d) secondary roofline):      */
+/* n_ops accesses of one kind to uniformly random slots of `buf`       */
+/* (n_elems, a power of two), timed with CUDA events; host `ms` out,   */
+/* syncs.                                                              */
+/* ---------------------------------------------------------------- */
+#define PGX_MB_LOAD_U32 0      /* read-filter: ld.global u32 */
+#define PGX_MB_LOAD_F64 1      /* pull gather: ld.global.nc f64 */
+#define PGX_MB_RED_MIN_U32 2   /* min combine: red.min.u32 */
+#define PGX_MB_RED_ADD_F64 3   /* sum combine: red.add.f64 */
+#define PGX_MB_ATOM_MIN_U32 4  /* atomicMin.u32 with return value */
+int pgx_microbench(int kind, void *buf, int64_t n_elems, int64_t n_ops,
+                   uint64_t seed, float *ms, uintptr_t stream);
+
 #ifdef __cplusplus
 }
 #endif

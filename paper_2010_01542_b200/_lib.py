@@ -33,7 +33,7 @@ EXPORTS = (
     "pgx_abi_version", "pgx_last_error", "pgx_set_option", "pgx_device_sm_count",
     "pgx_offsets_to_i32", "pgx_graph_workspace_bytes", "pgx_graph_prepare",
     "pgx_run_workspace_bytes", "pgx_sssp_run", "pgx_cc_run",
-    "pgx_pagerank_run", "pgx_pagerank_pull_run", "pgx_rmat_keys",
+    "pgx_pagerank_run", "pgx_pagerank_pull_run", "pgx_rmat_keys", "pgx_microbench",
 )
 
 _lib = None
@@ -61,6 +61,7 @@ _SIGS = {
                                         _i32, _p, _p, _sz, _p, _up]),
     "pgx_pagerank_pull_run": (ctypes.c_int, [_i32, _i64, _p, _p, _p, _p, _i32, _f64, _f64,
                                              _f64, _i32, _p, _p, _sz, _p, _up]),
+    "pgx_microbench": (ctypes.c_int, [ctypes.c_int, _p, _i64, _i64, _u64, _p, _up]),
     "pgx_rmat_keys": (ctypes.c_int, [_i32, _i64, _i64, _f64, _f64, _f64, _u64, _i32,
                                      _i64, _i64, _p, _i64, _p, _up]),
 }

@@ -128,7 +128,7 @@ __device__ __forceinline__ void red_or_b32(uint32_t *p, uint32_t v) {
   asm volatile("red.relaxed.gpu.global.or.b32 [%0], %1;" :: "l"(p), "r"(v) : "memory");
 }
 
-__device__ __forceinline__ unsigned lanemask_lt() {
+__device__ __forceinline__ __attribute__((unused)) unsigned lanemask_lt() {
   unsigned m;
   asm("mov.u32 %0, %%lanemask_lt;" : "=r"(m));
   return m;
@@ -160,18 +160,6 @@ __device__ __forceinline__ void grid_sync(GridBarrier *bar, unsigned &gen) {
   }
   gen += 1;
   __syncthreads();
-}
-
-// warp-aggregated append of `flag` lanes' `value` to list[*counter ...]
-__device__ __forceinline__ void warp_append(bool flag, int value, int *list,
-                                            unsigned *counter) {
-  unsigned mask = __ballot_sync(0xFFFFFFFFu, flag);
-  if (mask == 0) return;
-  int leader = __ffs(mask) - 1;
-  unsigned base = 0;
-  if ((int)lane_id() == leader) base = atomicAdd(counter, (unsigned)__popc(mask));
-  base = __shfl_sync(0xFFFFFFFFu, base, leader);
-  if (flag) list[base + __popc(mask & lanemask_lt())] = value;
 }
 
 template <typename T>
@@ -836,7 +824,6 @@ __device__ void gather_phase(const GatherArgs &a, char *smem) {
   int32_t *s_id = reinterpret_cast<int32_t *>(smem) + kWarps * kSlots + warp * kSlots;
   const uint64_t pol = evict_first_policy();
   const int64_t ntiles = (a.E + kTile - 1) / kTile;
-  const unsigned upto = (lane == 31) ? 0xFFFFFFFFu : ((2u << lane) - 1u);
   const int64_t gwarp = (int64_t)blockIdx.x * kWarps + warp;
   const int64_t nwarps = (int64_t)gridDim.x * kWarps;
 
