@@ -175,6 +175,47 @@ def flush_l2(buf):
     buf.add_(1)
 
 
+#: scattered-access ceilings measured on this pool's B200 by tools/ceilings.py
+#: (profiles/ceilings_r1.json): uniformly random 4/8-byte slots of an
+#: L2-resident array.  Every edge of a superstep costs at least one such
+#: access (read-filter load / share gather / red), so these bound GTEPS.
+SCATTER_CEILING = {"load": 290.0, "red": 193.0}
+
+
+def ncu_traffic(tag: str):
+    """DRAM bytes per launch of the headline kernel from the committed ncu
+    summary (profiles/ncu_<tag>_*.json, newest), else None."""
+    import glob
+    files = sorted(glob.glob(os.path.join(ROOT, "profiles", f"ncu_{tag}_*.json")),
+                   )
+    if not files:
+        return None, None
+    try:
+        d = json.load(open(files[-1]))
+        return float(d["kernels"][0]["dram_bytes_per_launch"]), os.path.basename(files[-1])
+    except Exception:
+        return None, None
+
+
+def measure_device(pgx, g, prog, steps, warmup, flush, config=None):
+    """Device-resident timing: one persistent-kernel launch per step."""
+    import torch
+    plan = pgx.plan_run(g, prog, config)
+    for _ in range(warmup):
+        plan.launch()
+    torch.cuda.synchronize()
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+          for _ in range(steps)]
+    for i in range(steps):
+        flush_l2(flush)
+        ev[i][0].record(plan.stream)
+        plan.launch()
+        ev[i][1].record(plan.stream)
+    torch.cuda.synchronize()
+    ms = [a.elapsed_time(b) for a, b in ev]
+    return plan, ms
+
+
 def bench_gpu(args):
     import torch
     import paper_2010_01542_b200 as pgx
@@ -197,29 +238,15 @@ def bench_gpu(args):
     flush = torch.empty(512 << 20, dtype=torch.uint8, device="cuda")
 
     # ---- device-resident arm: one persistent kernel per step ----
-    plan = pgx.plan_run(g, prog)
-    for _ in range(args.warmup):
-        plan.launch()
-    torch.cuda.synchronize()
-    ref = pgx.collect(plan, prog)
-    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
-          for _ in range(args.steps)]
-    kernel_ms = []
+    pcfg = pgx.EngineConfig(pagerank_mode="pull" if args.pr_pull else "push")
     if dist is not None:
         dist.barrier()
     torch.cuda.synchronize()
     with ClockSampler(local) as clocks:
-        for i in range(args.steps):
-            flush_l2(flush)
-            ev[i][0].record(plan.stream)
-            plan.launch()
-            ev[i][1].record(plan.stream)
-        torch.cuda.synchronize()
+        plan, kernel_ms = measure_device(pgx, g, prog, args.steps, args.warmup, flush, pcfg)
     if dist is not None:
         dist.barrier()
-    kernel_ms = [a.elapsed_time(b) for a, b in ev]
     rep = pgx.collect(plan, prog)
-    assert np.array_equal(rep.values, ref.values) or app == "pagerank"
     edges = sum(s.edges for s in rep.supersteps)
     total_ms = float(sum(kernel_ms))
     if dist is not None:
@@ -243,13 +270,40 @@ def bench_gpu(args):
         flush_l2(flush)
         torch.cuda.synchronize()
         t = time.perf_counter()
-        r = pgx.run(host, prog)
+        r = pgx.run(host, prog, pcfg)
         dt = time.perf_counter() - t
         if i >= args.warmup:
             e2e_ms.append(dt * 1e3)
     e2e_total = float(sum(e2e_ms))
     e2e_value = edges * len(e2e_ms) / (e2e_total * 1e-3) / 1e9
 
+    traffic, traffic_src = ncu_traffic("c2_components") if cfg == "C2" else (None, None)
+    ceiling = SCATTER_CEILING["red"] if (app == "pagerank" and not args.pr_pull) \
+        else SCATTER_CEILING["load"]
+    per_config = {}
+    if world == 1 and not args.no_per_config:
+        for c2 in ("C1", "C3", "C4"):
+            if c2 == cfg:
+                continue
+            del plan
+            torch.cuda.empty_cache()
+            gx = rmat_graph(c2)
+            appx = APP_OF[c2]
+            px = program_for(pgx, appx, gx)
+            cfgx = pgx.EngineConfig(pagerank_mode="pull" if args.pr_pull else "push")
+            plan, msx = measure_device(pgx, gx, px, args.aux_steps, 3, flush, cfgx)
+            rx = pgx.collect(plan, px)
+            ex = sum(st.edges for st in rx.supersteps)
+            tx = float(np.median(msx))
+            bx = algorithmic_bytes(appx, gx.vertex_count, gx.edge_count, step_views(appx, rx))
+            per_config[c2] = {
+                "app": appx, "n": gx.vertex_count, "m": gx.edge_count,
+                "supersteps": rx.superstep_count, "ms_per_run_median": round(tx, 4),
+                "GTEPS": round(ex / (tx * 1e-3) / 1e9, 2),
+                "alg_GBps": round(bx / (tx * 1e-3) / 1e9, 1),
+                "frac_of_measured_hbm": round(bx / (tx * 1e-3) / 1e9 / peak, 4),
+                "pagerank_mode": ("pull" if args.pr_pull else "push") if appx == "pagerank" else None}
+            del gx
     line = {
         "metric": METRIC,
         "value": round(value, 4),
@@ -278,8 +332,17 @@ def bench_gpu(args):
                      "frac_of_8TBs": round(achieved / HBM_NORTH_STAR_GBS, 4),
                      "alg_bytes_per_step": alg_bytes,
                      "kernel": "min_run_kernel / pagerank_run_kernel (persistent)"},
+        "scattered_roofline": {
+            "bound": "random 4/8-byte L2 accesses (>= 1 per edge)",
+            "achieved": round(value / world, 2), "peak": ceiling, "unit": "G accesses/s",
+            "frac": round(value / world / ceiling, 4),
+            "peak_source": "profiles/ceilings_r1.json (tools/ceilings.py, measured B200)"},
+        "per_config": per_config,
         "clocks": clocks.summary(),
     }
+    if traffic is not None:
+        line["roofline"]["traffic"] = int(traffic)
+        line["roofline"]["traffic_source"] = traffic_src
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         line["cpu_baseline"] = cpu_baseline(cfg, g, app)
     if rank == 0:
@@ -343,6 +406,10 @@ def main():
     ap.add_argument("--impl", default="pgx", choices=["pgx", "reference"])
     ap.add_argument("--config", default="C2", choices=sorted(APP_OF))
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-per-config", action="store_true")
+    ap.add_argument("--aux-steps", type=int, default=5)
+    ap.add_argument("--pr-push", dest="pr_pull", action="store_false",
+                    help="PageRank A/B arm: push scatter with red.add.f64")
     args = ap.parse_args()
     if args.warmup < 3 and args.impl == "pgx":
         args.warmup = 3

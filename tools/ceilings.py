@@ -28,6 +28,7 @@ for size_mb in (16, 64, 1024):
         print(r, flush=True)
         del buf
 tag = sys.argv[1] if len(sys.argv) > 1 else "r1"
-os.makedirs("profiles", exist_ok=True)
-with open(f"profiles/ceilings_{tag}.json", "w") as fh:
-    json.dump(out, fh, indent=1)
+for d in ("profiles", "gpurun_out"):
+    os.makedirs(d, exist_ok=True)
+    with open(f"{d}/ceilings_{tag}.json", "w") as fh:
+        json.dump(out, fh, indent=1)
