@@ -147,6 +147,58 @@ int pgx_pagerank_pull_run(int32_t n, int64_t m, const int32_t *row_ptr,
                           uintptr_t stream);
 
 /* ---------------------------------------------------------------- */
+/* phases of the partitioned multi-GPU superstep.     */
+/* A rank owns the out-edges of vertices [lo, lo+len) (a local CSR     */
+/* with GLOBAL destination ids) and that slice of the mailbox.  Per    */
+/* superstep the host calls pgx_scatter (into a full-width local       */
+/* mailbox), reduces the slices onto their owners (NCCL min / sum via  */
+/* torch.distributed), then pgx_apply_slice / pgx_pr_apply_slice.      */
+/* Replaces the same reference functions as the *_run entry points,    */
+/* one phase at a time.                                                */
+/* ---------------------------------------------------------------- */
+
+/* value / rank / share initialisation of an owned slice (setup,
+ * algorithms.py:44-59, 96-97, 129-134); `val` is u32 labels/distances or
+ * f64 ranks; `share`/`row_ptr` for PageRank only */
+int pgx_slice_init(int app, int32_t len, int32_t lo, void *val,
+                   const int32_t *row_ptr, double *share, double r0,
+                   uintptr_t stream);
+
+/* K1 alone: senders push along out-edges into `mailbox` (global ids).
+ * dense != 0: senders are a graph workspace's non-zero-degree list
+ * (src_eb = its row starts, src_ids = its local ids; min: message =
+ * id + id_offset; sum: message = ((double*)src_msg)[id]);
+ * dense == 0: a frontier built by pgx_apply_slice (src_eb/src_rs/src_msg).
+ * has_bits may be NULL. */
+int pgx_scatter(int op, int dense, const int32_t *col_idx,
+                const int32_t *src_eb, const int32_t *src_rs,
+                const int32_t *src_ids, int32_t id_offset, const void *src_msg,
+                const int32_t *tile_src, int32_t nsrc, int64_t edges,
+                void *mailbox, uint32_t *has_bits, uintptr_t stream);
+
+/* size of the device counter block used by pgx_apply_slice (host out) */
+int pgx_slice_counters_bytes(size_t *bytes);
+
+/* K2 on an owned slice (min programs): recipients are the slots that are
+ * not `neutral` after the reduction; consume (reset to `neutral`), adopt,
+ * build the next frontier (edge prefix + tile map) and count.  count_only:
+ * cap reached, only count recipients.  The partitioned path uses
+ * neutral = INT32_MAX so that a signed int32 MIN reduction (NCCL / gloo)
+ * is exact: every message is < n <= 2^31 - 1. */
+int pgx_apply_slice(int app, int32_t len, const int32_t *row_ptr,
+                    uint32_t *val, uint32_t *mailbox_slice, int32_t *f_eb,
+                    int32_t *f_rs, uint32_t *f_msg, int32_t *tile_src,
+                    void *counters, int32_t count_only, uint32_t neutral,
+                    uintptr_t stream);
+
+/* PageRank apply on an owned slice: rank, next share, per-CTA dangling
+ * partials (partials[ceil(len/512)]) */
+int pgx_pr_apply_slice(int32_t len, const int32_t *row_ptr, double *rank,
+                       double *mailbox_slice, double *share, double base,
+                       double damping, double dangling_over_n, int32_t last,
+                       double *partials, uintptr_t stream);
+
+/* ---------------------------------------------------------------- */
 /* R-MAT input generator; input construction only.    */
 /* Writes src << 32 | dst keys of the non-loop draws in                */
 /* [first_draw, first_draw + num_draws) whose source lies in           */

@@ -34,6 +34,8 @@ EXPORTS = (
     "pgx_offsets_to_i32", "pgx_graph_workspace_bytes", "pgx_graph_prepare",
     "pgx_run_workspace_bytes", "pgx_sssp_run", "pgx_cc_run",
     "pgx_pagerank_run", "pgx_pagerank_pull_run", "pgx_rmat_keys", "pgx_microbench",
+    "pgx_slice_init", "pgx_scatter", "pgx_slice_counters_bytes", "pgx_apply_slice",
+    "pgx_pr_apply_slice",
 )
 
 _lib = None
@@ -61,6 +63,14 @@ _SIGS = {
                                         _i32, _p, _p, _sz, _p, _up]),
     "pgx_pagerank_pull_run": (ctypes.c_int, [_i32, _i64, _p, _p, _p, _p, _i32, _f64, _f64,
                                              _f64, _i32, _p, _p, _sz, _p, _up]),
+    "pgx_slice_init": (ctypes.c_int, [ctypes.c_int, _i32, _i32, _p, _p, _p, _f64, _up]),
+    "pgx_scatter": (ctypes.c_int, [ctypes.c_int, ctypes.c_int, _p, _p, _p, _p, _i32, _p, _p,
+                                   _i32, _i64, _p, _p, _up]),
+    "pgx_slice_counters_bytes": (ctypes.c_int, [_p]),
+    "pgx_apply_slice": (ctypes.c_int, [ctypes.c_int, _i32, _p, _p, _p, _p, _p, _p, _p, _p,
+                                       _i32, ctypes.c_uint32, _up]),
+    "pgx_pr_apply_slice": (ctypes.c_int, [_i32, _p, _p, _p, _p, _f64, _f64, _f64, _i32, _p,
+                                          _up]),
     "pgx_microbench": (ctypes.c_int, [ctypes.c_int, _p, _i64, _i64, _u64, _p, _up]),
     "pgx_rmat_keys": (ctypes.c_int, [_i32, _i64, _i64, _f64, _f64, _f64, _u64, _i32,
                                      _i64, _i64, _p, _i64, _p, _up]),

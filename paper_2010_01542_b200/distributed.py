@@ -1,12 +1,49 @@
-"""Multi-GPU superstep (placeholder until the partitioned path lands)."""
+"""Partitioned multi-GPU superstep, one process per GPU.
+
+The reference has no distributed mode (SPEC.md:420 non-goal); this is the
+B200 build's scale-out of the same superstep, with results identical to
+one GPU (CC labels / SSSP distances bit-exact, PageRank within 1e-9):
+
+* **partition**: 1-D by source vertex.  Rank r owns the contiguous vertex
+  range ``[lo_r, hi_r)`` -- its out-edges (a local CSR with GLOBAL
+  destination ids) and that slice of the mailbox.  Ranges follow the
+  reference's exact integer edge-balance rule (``edge_balanced_partition``,
+  scheduler.py:91-116) over ``out_degree + 1`` (edges + vertex work);
+* **per superstep**: every rank scatters its senders into a full-width
+  local mailbox (``pgx_scatter``); one reduction per owner delivers the
+  combined slice (``min`` for CC/SSSP, ``sum`` for PageRank) -- issued as
+  ``len(world)`` ``reduce`` calls, which NCCL runs over NVLink/NVSwitch;
+  the owner applies on its slice (``pgx_apply_slice`` /
+  ``pgx_pr_apply_slice``); an ``all_reduce`` of the counters (recipients,
+  broadcasts, senders, edges, dangling mass) drives the halt test.  No
+  all-gather is needed: a sender is always local to its owner.
+* has-message after the reduction is ``mailbox != neutral``: CC / SSSP
+  messages are < n <= 2^31 and never equal UINT32_MAX, and PageRank needs
+  no flag (the paper's neutral-value caveat).
+
+The orchestration below is backend-agnostic: ``CudaBackend`` drives
+libpgx.so on the rank's GPU (NCCL process group); tests/ drive the same
+``PartitionedRun`` with a CPU test backend over a gloo process group.
+"""
 
 from __future__ import annotations
 
-import os
+import time
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+
+from .errors import ConfigError
+from .scheduler import edge_balanced_partition
+
+#: min neutral of the exchanged mailbox: INT32_MAX, so that the signed
+#: int32 MIN reduction of NCCL / gloo is exact (messages are < n < 2^31 - 1)
+EXCHANGE_NEUTRAL = 2 ** 31 - 1
 
 
 def distributed_context():
-    """Active torch.distributed world with >1 rank, else None."""
+    """The active torch.distributed module when world_size > 1, else None."""
     try:
         import torch.distributed as dist
     except Exception:  # pragma: no cover
@@ -18,5 +55,326 @@ def distributed_context():
     return dist
 
 
-def run_partitioned(graph, program, low, config, ctx):  # pragma: no cover
-    raise NotImplementedError
+def partition_bounds(out_degrees, world: int) -> np.ndarray:
+    """Owner ranges ``bounds[r]..bounds[r+1]`` (edge + vertex balanced)."""
+    deg = np.asarray(out_degrees, dtype=np.int64)
+    return edge_balanced_partition(deg + 1, world).boundaries.astype(np.int64)
+
+
+@dataclass
+class StepCounts:
+    recipients: int
+    broadcasts: int
+    senders: int
+    edges: int
+    dangling: float = 0.0
+
+
+class PartitionedRun:
+    """Backend-agnostic driver of one partitioned run on this rank."""
+
+    def __init__(self, backend, dist, bounds, n: int, m: int):
+        self.b = backend
+        self.dist = dist
+        self.bounds = np.asarray(bounds, dtype=np.int64)
+        self.rank = dist.get_rank()
+        self.world = dist.get_world_size()
+        self.n, self.m = n, m
+        self.lo = int(self.bounds[self.rank])
+        self.hi = int(self.bounds[self.rank + 1])
+
+    # ---- collectives --------------------------------------------------
+
+    def _reduce_slices(self, op):
+        full = self.b.mailbox
+        for r in range(self.world):
+            lo, hi = int(self.bounds[r]), int(self.bounds[r + 1])
+            if hi > lo:
+                self.dist.reduce(full[lo:hi], dst=r, op=op)
+
+    def _allreduce_counts(self, c: StepCounts) -> StepCounts:
+        t = torch.tensor([c.recipients, c.broadcasts, c.senders, c.edges],
+                         dtype=torch.int64, device=self.b.device)
+        self.dist.all_reduce(t)
+        d = torch.tensor([c.dangling], dtype=torch.float64, device=self.b.device)
+        self.dist.all_reduce(d)
+        v = t.tolist()
+        return StepCounts(v[0], v[1], v[2], v[3], float(d.item()))
+
+    def _gather_values(self):
+        local = self.b.values()
+        sizes = np.diff(self.bounds)
+        mx = int(sizes.max())
+        pad = torch.zeros(mx, dtype=local.dtype, device=local.device)
+        pad[:local.numel()] = local
+        parts = [torch.empty_like(pad) for _ in range(self.world)]
+        self.dist.all_gather(parts, pad)
+        return torch.cat([parts[r][:int(sizes[r])] for r in range(self.world)])
+
+    # ---- min programs: CC / SSSP -------------------------------------
+
+    def run_min(self, app: str, source: int, max_steps: int):
+        op = self.dist.ReduceOp.MIN
+        n = self.n
+        self.b.init_min(app, self.lo, self.hi)
+        stats = []
+        if app == "sssp":
+            own = self.lo <= source < self.hi
+            deg = self.b.global_out_degree(source)
+            if own:
+                self.b.seed_source(source - self.lo)
+            nxt = StepCounts(0, 1, 1 if deg > 0 else 0, deg)
+        else:
+            nxt = StepCounts(0, n, self.b.global_nonzero_degree(), self.m)
+        hit_cap = False
+        t0 = time.perf_counter()
+        active = n  # superstep 0 runs every vertex
+        for s in range(max_steps):
+            ts = time.perf_counter()
+            cur = nxt
+            self.b.reset_mailbox()
+            self.b.scatter_min(dense=(app == "components" and s == 0),
+                               id_offset=self.lo)
+            self._reduce_slices(op)
+            at_cap = s + 1 == max_steps
+            local = self.b.apply_min(app, count_only=at_cap)
+            nxt = self._allreduce_counts(local)
+            sent = cur.edges if app == "sssp" else cur.broadcasts
+            stats.append(dict(index=s, active_count=active,
+                              messages_sent=sent, edges=cur.edges,
+                              senders=cur.senders, recipients=nxt.recipients,
+                              broadcasters=cur.broadcasts,
+                              seconds=time.perf_counter() - ts))
+            active = nxt.recipients
+            if nxt.recipients == 0:
+                break
+            if at_cap:
+                hit_cap = True
+                break
+        values = self._gather_values()
+        return values, stats, hit_cap, time.perf_counter() - t0
+
+    # ---- PageRank -------------------------------------------------------
+
+    def run_pagerank(self, iterations: int, damping: float, max_steps: int):
+        op = self.dist.ReduceOp.SUM
+        n = self.n
+        base = (1.0 - damping) / n      # algorithms.py:49
+        r0 = 1.0 / n                    # algorithms.py:50
+        last = iterations - 1
+        ndangling = self.b.init_pagerank(self.lo, self.hi, r0)
+        t = torch.tensor([ndangling], dtype=torch.int64, device=self.b.device)
+        self.dist.all_reduce(t)
+        ndangling = int(t.item())
+        dangling = r0 * ndangling       # algorithms.py:55
+        nspread = n - ndangling
+        stats = []
+        t0 = time.perf_counter()
+        steps = min(max_steps, iterations)
+        for s in range(steps):
+            ts = time.perf_counter()
+            # the fold of superstep s: shares broadcast at s-1 (or the seed)
+            self.b.reset_mailbox()
+            self.b.scatter_sum()
+            self._reduce_slices(op)
+            local_d = self.b.apply_pagerank(base, damping, dangling / n, s == last)
+            d = torch.tensor([local_d], dtype=torch.float64, device=self.b.device)
+            self.dist.all_reduce(d)
+            dangling = float(d.item())
+            stats.append(dict(index=s, active_count=n,
+                              messages_sent=0 if s == last else nspread,
+                              edges=self.m, senders=nspread, recipients=n,
+                              broadcasters=0 if s == last else nspread,
+                              seconds=time.perf_counter() - ts))
+        hit_cap = steps < iterations  # engine.py:299-300
+        values = self._gather_values()
+        return values, stats, hit_cap, time.perf_counter() - t0
+
+
+# ----------------------------------------------------------------------
+# CUDA backend (libpgx phase kernels on this rank's GPU)
+# ----------------------------------------------------------------------
+
+class CudaBackend:
+    """Owns the rank's local CSR, full-width mailbox and owned-slice state."""
+
+    def __init__(self, graph, lo: int, hi: int, device):
+        from . import _lib
+        self._lib = _lib
+        self.lib = _lib.load()
+        self.device = torch.device(device)
+        self.stream = torch.cuda.current_stream(self.device)
+        dev = self.device
+        off = graph.out_offsets.to(dev)
+        tgt = graph.out_targets.to(dev)
+        self.n = graph.vertex_count
+        self.glob_deg = torch.diff(off)
+        base = int(off[lo])
+        self.row_ptr = (off[lo:hi + 1] - base).to(torch.int32).contiguous()
+        self.col = tgt[base:int(off[hi])].to(torch.int32).contiguous()
+        self.len = hi - lo
+        self.m_local = int(self.col.numel())
+        st = self.stream.cuda_stream
+        ws_bytes = _lib.out_size(self.lib.pgx_graph_workspace_bytes, max(self.len, 1),
+                                 self.m_local)
+        self.gws = torch.empty(ws_bytes, dtype=torch.uint8, device=dev)
+        if self.len > 0:
+            _lib.check(self.lib.pgx_graph_prepare(self.len, self.m_local,
+                                                  self.row_ptr.data_ptr(),
+                                                  self.gws.data_ptr(), ws_bytes, st),
+                       "pgx_graph_prepare")
+        # graph workspace layout (pgx_engine.cu graph_ws_layout): hdr, nz_id,
+        # nz_eb, tile_src, blk -- 256-byte aligned chunks
+        al = lambda x: (x + 255) // 256 * 256
+        o_id = al(16)
+        o_eb = o_id + al(4 * (self.len + 1))
+        o_tile = o_eb + al(4 * (self.len + 1))
+        self._g_hdr = self.gws[:16].view(torch.int32)
+        self._g_nz_id = self.gws[o_id:o_id + 4 * (self.len + 1)].view(torch.int32)
+        self._g_nz_eb = self.gws[o_eb:o_eb + 4 * (self.len + 1)].view(torch.int32)
+        ntile = (self.m_local + 255) // 256 + 2
+        self._g_tile = self.gws[o_tile:o_tile + 4 * ntile].view(torch.int32)
+        cb = _lib.out_size(self.lib.pgx_slice_counters_bytes)
+        self.ctr = torch.zeros(cb, dtype=torch.uint8, device=dev)
+        self.f_eb = torch.empty(self.len + 1, dtype=torch.int32, device=dev)
+        self.f_rs = torch.empty(self.len + 1, dtype=torch.int32, device=dev)
+        self.f_msg = torch.empty(self.len + 1, dtype=torch.int32, device=dev)
+        self.f_tile = torch.empty(ntile, dtype=torch.int32, device=dev)
+        self.nsrc, self.E = 0, 0
+
+    # ---- helpers ----
+    def global_out_degree(self, v: int) -> int:
+        return int(self.glob_deg[v])
+
+    def global_nonzero_degree(self) -> int:
+        return int((self.glob_deg > 0).sum())
+
+    def _counters(self):
+        c = self.ctr[:32].view(torch.int64).tolist()
+        d = float(self.ctr[24:32].view(torch.float64).item())
+        return c, d
+
+    # ---- min programs ----
+    def init_min(self, app, lo, hi):
+        self.app = app
+        self.lo = lo
+        self.mailbox = torch.empty(self.n, dtype=torch.int32, device=self.device)
+        self.val = torch.empty(max(self.len, 1), dtype=torch.int32, device=self.device)
+        app_id = self._lib.PGX_APP_CC if app == "components" else self._lib.PGX_APP_SSSP
+        self._lib.check(self.lib.pgx_slice_init(app_id, self.len, lo, self.val.data_ptr(),
+                                                self.row_ptr.data_ptr(), None, 0.0,
+                                                self.stream.cuda_stream), "pgx_slice_init")
+        self.nsrc, self.E = 0, 0
+
+    def seed_source(self, local_v: int):
+        rs = int(self.row_ptr[local_v])
+        deg = int(self.row_ptr[local_v + 1]) - rs
+        self.val[local_v] = 0
+        if deg > 0:
+            self.f_eb[0] = 0
+            self.f_rs[0] = rs
+            self.f_msg[0] = 1
+            ntiles = (deg + 255) // 256
+            self.f_tile[:ntiles] = 0
+            self.nsrc, self.E = 1, deg
+
+    def reset_mailbox(self):
+        if self.app == "pagerank":
+            self.mailbox.zero_()
+        else:
+            self.mailbox.fill_(EXCHANGE_NEUTRAL)
+
+    def scatter_min(self, dense: bool, id_offset: int):
+        L, st = self.lib, self.stream.cuda_stream
+        op = self._lib.PGX_OP_MIN_U32
+        if dense:
+            nnz = int(self._g_hdr[0])
+            rc = L.pgx_scatter(op, 1, self.col.data_ptr(), self._g_nz_eb.data_ptr(), None,
+                               self._g_nz_id.data_ptr(), id_offset, None,
+                               self._g_tile.data_ptr(), nnz, self.m_local,
+                               self.mailbox.data_ptr(), None, st)
+        else:
+            rc = L.pgx_scatter(op, 0, self.col.data_ptr(), self.f_eb.data_ptr(),
+                               self.f_rs.data_ptr(), None, 0, self.f_msg.data_ptr(),
+                               self.f_tile.data_ptr(), self.nsrc, self.E,
+                               self.mailbox.data_ptr(), None, st)
+        self._lib.check(rc, "pgx_scatter")
+
+    def apply_min(self, app, count_only: bool) -> StepCounts:
+        self.ctr.zero_()
+        app_id = self._lib.PGX_APP_CC if app == "components" else self._lib.PGX_APP_SSSP
+        sl = self.mailbox[self.lo:self.lo + self.len]
+        self._lib.check(self.lib.pgx_apply_slice(
+            app_id, self.len, self.row_ptr.data_ptr(), self.val.data_ptr(), sl.data_ptr(),
+            self.f_eb.data_ptr(), self.f_rs.data_ptr(), self.f_msg.data_ptr(),
+            self.f_tile.data_ptr(), self.ctr.data_ptr(), int(count_only), EXCHANGE_NEUTRAL,
+            self.stream.cuda_stream), "pgx_apply_slice")
+        c, _ = self._counters()
+        packed = c[0] & 0xFFFFFFFFFFFFFFFF
+        self.nsrc, self.E = packed >> 32, packed & 0xFFFFFFFF
+        return StepCounts(c[1], c[2], self.nsrc, self.E)
+
+    # ---- PageRank ----
+    def init_pagerank(self, lo, hi, r0) -> int:
+        self.app = "pagerank"
+        self.lo = lo
+        self.mailbox = torch.zeros(self.n, dtype=torch.float64, device=self.device)
+        self.rank = torch.empty(max(self.len, 1), dtype=torch.float64, device=self.device)
+        self.share = torch.empty(max(self.len, 1), dtype=torch.float64, device=self.device)
+        self._lib.check(self.lib.pgx_slice_init(self._lib.PGX_APP_PAGERANK, self.len, lo,
+                                                self.rank.data_ptr(), self.row_ptr.data_ptr(),
+                                                self.share.data_ptr(), r0,
+                                                self.stream.cuda_stream), "pgx_slice_init")
+        self.partials = torch.zeros((self.len + 511) // 512 + 1, dtype=torch.float64,
+                                    device=self.device)
+        deg = torch.diff(self.row_ptr)
+        return int((deg == 0).sum())
+
+    def scatter_sum(self):
+        nnz = int(self._g_hdr[0])
+        self._lib.check(self.lib.pgx_scatter(
+            self._lib.PGX_OP_SUM_F64, 1, self.col.data_ptr(), self._g_nz_eb.data_ptr(), None,
+            self._g_nz_id.data_ptr(), 0, self.share.data_ptr(), self._g_tile.data_ptr(), nnz,
+            self.m_local, self.mailbox.data_ptr(), None, self.stream.cuda_stream),
+            "pgx_scatter")
+
+    def apply_pagerank(self, base, damping, dn, last: bool) -> float:
+        sl = self.mailbox[self.lo:self.lo + self.len]
+        self._lib.check(self.lib.pgx_pr_apply_slice(
+            self.len, self.row_ptr.data_ptr(), self.rank.data_ptr(), sl.data_ptr(),
+            self.share.data_ptr(), base, damping, dn, int(last), self.partials.data_ptr(),
+            self.stream.cuda_stream), "pgx_pr_apply_slice")
+        return float(self.partials[:(self.len + 511) // 512].sum().item())
+
+    def values(self):
+        if self.app == "pagerank":
+            return self.rank[:self.len]
+        return self.val[:self.len]
+
+
+def run_partitioned(graph, program, low, config, dist):
+    """engine.run() under torchrun: every rank calls run() with the graph."""
+    from .engine import RunReport, SuperstepStats
+    rank, world = dist.get_rank(), dist.get_world_size()
+    n, m = graph.vertex_count, graph.edge_count
+    deg = torch.diff(graph.out_offsets.cpu()).numpy()
+    bounds = partition_bounds(deg, world)
+    dev = torch.device("cuda", torch.cuda.current_device())
+    backend = CudaBackend(graph, int(bounds[rank]), int(bounds[rank + 1]), dev)
+    runner = PartitionedRun(backend, dist, bounds, n, m)
+    app = low["app"]
+    if app == "pagerank":
+        vals, stats, cap, wall = runner.run_pagerank(low["iterations"], low["damping"],
+                                                     config.max_supersteps)
+        values = vals.cpu().numpy()
+    else:
+        vals, stats, cap, wall = runner.run_min(app, low.get("source", 0),
+                                                config.max_supersteps)
+        v = vals.cpu().numpy().view(np.uint32)
+        values = v.astype(np.int64) if app == "components" else v
+    steps = [SuperstepStats(**s) for s in stats]
+    if program.extract is not None:
+        from types import SimpleNamespace
+        values = program.extract(SimpleNamespace(state=values,
+                                                 halted=np.ones(values.shape[0], bool)))
+    return RunReport(values, len(steps), steps, wall, cap, device_values=vals)

@@ -1,0 +1,103 @@
+"""Thread-based stand-in for torch.distributed -- TEST INFRASTRUCTURE ONLY.
+
+Runs W "ranks" as threads of one process so the partitioned driver and the
+CUDA phase kernels (pgx_scatter / pgx_apply_slice / pgx_pr_apply_slice)
+can be exercised on ONE GPU.  Collectives are implemented with a barrier
+and torch ops on the participants' tensors; no kernel waits on another
+rank, so nothing spins on the device.
+"""
+
+from __future__ import annotations
+
+import threading
+
+import torch
+import torch.distributed as _d
+
+
+class ThreadDist:
+    ReduceOp = _d.ReduceOp
+
+    def __init__(self, world: int):
+        self.world = world
+        self._bar = threading.Barrier(world)
+        self._slots = [None] * world
+        self._tls = threading.local()
+
+    def bind(self, rank: int):
+        self._tls.rank = rank
+
+    def get_rank(self):
+        return self._tls.rank
+
+    def get_world_size(self):
+        return self.world
+
+    def _combine(self, op):
+        ts = self._slots
+        out = ts[0].clone()
+        for t in ts[1:]:
+            if op == _d.ReduceOp.MIN:
+                out = torch.minimum(out, t)
+            elif op == _d.ReduceOp.MAX:
+                out = torch.maximum(out, t)
+            else:
+                out = out + t
+        return out
+
+    def reduce(self, tensor, dst, op=_d.ReduceOp.SUM):
+        r = self.get_rank()
+        torch.cuda.synchronize() if tensor.is_cuda else None
+        self._slots[r] = tensor
+        self._bar.wait()
+        if r == dst:
+            res = self._combine(op)
+        self._bar.wait()
+        if r == dst:
+            tensor.copy_(res)
+            torch.cuda.synchronize() if tensor.is_cuda else None
+        self._bar.wait()
+
+    def all_reduce(self, tensor, op=_d.ReduceOp.SUM):
+        r = self.get_rank()
+        torch.cuda.synchronize() if tensor.is_cuda else None
+        self._slots[r] = tensor
+        self._bar.wait()
+        res = self._combine(op)
+        self._bar.wait()
+        tensor.copy_(res)
+        torch.cuda.synchronize() if tensor.is_cuda else None
+        self._bar.wait()
+
+    def all_gather(self, parts, tensor):
+        r = self.get_rank()
+        torch.cuda.synchronize() if tensor.is_cuda else None
+        self._slots[r] = tensor
+        self._bar.wait()
+        for i in range(self.world):
+            parts[i].copy_(self._slots[i])
+        self._bar.wait()
+
+
+def run_ranks(world, fn):
+    """Run fn(rank, dist) on `world` threads; returns the per-rank results."""
+    d = ThreadDist(world)
+    out = [None] * world
+    err = []
+
+    def body(r):
+        d.bind(r)
+        try:
+            out[r] = fn(r, d)
+        except BaseException as e:  # pragma: no cover
+            err.append(e)
+            d._bar.abort()
+
+    ts = [threading.Thread(target=body, args=(r,)) for r in range(world)]
+    for t in ts:
+        t.start()
+    for t in ts:
+        t.join()
+    if err:
+        raise err[0]
+    return out
