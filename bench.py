@@ -351,6 +351,94 @@ def bench_gpu(args):
         dist.destroy_process_group()
 
 
+def bench_multi(args):
+    """N > 1 under torchrun: the partitioned superstep of the
+    same workload on every rank's GPU, NCCL reductions over NVLink; strong
+    scaling (the graph is fixed).  Timed with CUDA events around each run,
+    max over ranks."""
+    import torch
+    import torch.distributed as dist
+    import paper_2010_01542_b200 as pgx
+    from paper_2010_01542_b200.rmat import rmat_graph
+
+    world = int(os.environ["WORLD_SIZE"])
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+    dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    cfg = args.config
+    app = APP_OF[cfg]
+    g = rmat_graph(cfg)
+    n, m = g.vertex_count, g.edge_count
+    prog = program_for(pgx, app, g)
+    flush = torch.empty(512 << 20, dtype=torch.uint8, device="cuda")
+    for _ in range(args.warmup):
+        rep = pgx.run(g, prog)
+    ms = []
+    with ClockSampler(local) as clocks:
+        for _ in range(args.steps):
+            flush_l2(flush)
+            dist.barrier()
+            torch.cuda.synchronize()
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record()
+            rep = pgx.run(g, prog)
+            b.record()
+            torch.cuda.synchronize()
+            ms.append(a.elapsed_time(b))
+    t = torch.tensor([sum(ms)], device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    total_ms = float(t.item())
+    edges = sum(s.edges for s in rep.supersteps)
+    value = edges * args.steps / (total_ms * 1e-3) / 1e9
+    peak, peak_src = measured_peaks()
+    alg = algorithmic_bytes(app, n, m, step_views(app, rep))
+    achieved = alg / (total_ms / args.steps * 1e-3) / 1e9
+    # e2e: the public run() from pinned host memory (local slice upload inside)
+    host = g.pin_memory()
+    e2e = []
+    for i in range(2 + args.e2e_steps):
+        dist.barrier()
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        pgx.run(host, prog)
+        torch.cuda.synchronize()
+        dt = time.perf_counter() - t0
+        host.drop_device_cache()
+        if i >= 2:
+            e2e.append(dt * 1e3)
+    te = torch.tensor([sum(e2e)], device="cuda")
+    dist.all_reduce(te, op=dist.ReduceOp.MAX)
+    e2e_ms = float(te.item()) / len(e2e)
+    line = {
+        "metric": METRIC, "value": round(value, 4), "unit": "GTEPS", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": round(total_ms / args.steps, 4), "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None,
+        "dtype": "u32" if app != "pagerank" else "f64",
+        "data": "synthetic R-MAT (SURVEY 8(d) generator, BASELINE.md CSR sha256-pinned)",
+        "config": {"workload": f"{cfg}: {app} on R-MAT, n={n}, m={m}, 1-D source partition "
+                               f"over {world} GPUs (edge-balanced ranges)",
+                   "n": n, "m": m, "supersteps": rep.superstep_count,
+                   "l2": "flushed (512 MiB write) between timed steps",
+                   "parallelism": f"partitioned x{world}, NCCL reduce per owner + allreduce"},
+        "e2e": {"value": round(edges / (e2e_ms * 1e-3) / 1e9, 4), "unit": "GTEPS",
+                "h2d_bytes_per_step": (n + 1) * 8 + m * 4,
+                "d2h_bytes_per_step": n * (8 if app == "pagerank" else 4),
+                "ms_per_step": round(e2e_ms, 3)},
+        # our kernels per timed step: pgx_scatter + pgx_apply_slice per superstep
+        "gpu_launches": 2 * rep.superstep_count * args.steps,
+        "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak * world,
+                     "unit": "GB/s", "frac": round(achieved / (peak * world), 4),
+                     "traffic": None, "peak_source": peak_src + f" x {world} GPUs"},
+        "clocks": clocks.summary(),
+    }
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    dist.destroy_process_group()
+
+
 def bench_reference(args):
     """--impl reference: the oracle port of pregelite's engine on host cores."""
     rank = int(os.environ.get("RANK", "0"))
@@ -415,6 +503,8 @@ def main():
         args.warmup = 3
     if args.impl == "reference":
         bench_reference(args)
+    elif int(os.environ.get("WORLD_SIZE", "1")) > 1:
+        bench_multi(args)
     else:
         bench_gpu(args)
 

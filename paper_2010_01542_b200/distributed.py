@@ -357,10 +357,15 @@ def run_partitioned(graph, program, low, config, dist):
     from .engine import RunReport, SuperstepStats
     rank, world = dist.get_rank(), dist.get_world_size()
     n, m = graph.vertex_count, graph.edge_count
-    deg = torch.diff(graph.out_offsets.cpu()).numpy()
-    bounds = partition_bounds(deg, world)
     dev = torch.device("cuda", torch.cuda.current_device())
-    backend = CudaBackend(graph, int(bounds[rank]), int(bounds[rank + 1]), dev)
+    key = ("partitioned", world, rank, dev.index)
+    cached = graph._device.get(key)
+    if cached is None:  # local CSR slice + its tile map, built once per graph
+        deg = torch.diff(graph.out_offsets.cpu()).numpy()
+        bounds = partition_bounds(deg, world)
+        backend = CudaBackend(graph, int(bounds[rank]), int(bounds[rank + 1]), dev)
+        cached = graph._device[key] = (bounds, backend)
+    bounds, backend = cached
     runner = PartitionedRun(backend, dist, bounds, n, m)
     app = low["app"]
     if app == "pagerank":
