@@ -48,7 +48,10 @@ constexpr int kBlock = 512;          // threads per CTA
 constexpr int kWarps = kBlock / 32;
 constexpr int kItems = 8;            // 32-edge rounds per warp tile
 constexpr int kTile = 32 * kItems;   // 256 edges per warp tile
-constexpr int kPass = 4;             // rounds in flight per pass
+#ifndef PGX_PASS
+#define PGX_PASS 4
+#endif
+constexpr int kPass = PGX_PASS;      // rounds in flight per pass
 constexpr int kSlots = kTile + 2;    // sources per warp tile (+ sentinel)
 constexpr uint32_t kNeutralMin = 0xFFFFFFFFu;
 constexpr int kMaxCtas = 4096;
@@ -465,6 +468,7 @@ __device__ unsigned long long apply_min_phase(const int32_t *__restrict__ row_pt
       word = ws.has[wi];
       if (word) ws.has[wi] = 0u;
     }
+    if (!__syncthreads_or(word != 0)) continue;  // empty chunk: one barrier
     recips += __popc(word);
     unsigned long long tot64;
     const int off = (int)block_excl_scan_u64((unsigned long long)__popc(word), s_w, &tot64);

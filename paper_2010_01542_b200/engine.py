@@ -308,12 +308,16 @@ def collect(plan: LaunchPlan, program: VertexProgram, wall: float | None = None)
     dev_seconds = max(int(rows[k - 1, 5]) - t0, 0) * 1e-9
     app = plan.app
     dv = plan.values
-    if app == "pagerank":
-        values = dv.cpu().numpy()
-    elif app == "components":
-        values = dv.to(torch.int64).cpu().numpy()       # algorithms.py:111 int64
-    else:
-        values = dv.cpu().numpy().view(np.uint32)        # algorithms.py:150 uint32
+    if app == "components":
+        dv = dv.to(torch.int64)                          # algorithms.py:111 int64
+    # read back through page-locked memory (torch's caching host allocator):
+    # a pageable .cpu() of a C2-sized result costs ~20x more
+    host = torch.empty(dv.shape, dtype=dv.dtype, pin_memory=True)
+    host.copy_(dv, non_blocking=True)
+    plan.stream.synchronize()
+    values = host.numpy()
+    if app == "sssp":
+        values = values.view(np.uint32)                  # algorithms.py:150 uint32
     if program.extract is not None:
         values = program.extract(SimpleNamespace(state=values,
                                                  halted=np.ones(values.shape[0], bool)))
