@@ -33,7 +33,7 @@
 extern "C" {
 #endif
 
-#define PGX_ABI_VERSION 1
+#define PGX_ABI_VERSION 2
 
 #define PGX_OK 0
 #define PGX_EINVAL (-1)   /* bad argument / unsupported configuration */
@@ -110,9 +110,18 @@ int pgx_graph_prepare(int32_t n, int64_t m, const int32_t *row_ptr,
 int pgx_run_workspace_bytes(int app, int64_t n, int64_t m,
                             int32_t max_supersteps, size_t *bytes);
 
+/* Hub recipients (the paper's hybrid combiner split by recipient class):
+ * optionally, col_idx may be an ENCODED copy in which every edge into one
+ * of `nhubs` hub vertices holds (0x80000000 | slot), hub_ids[slot] being
+ * the vertex; those edges are read-filtered and pre-combined in a per-CTA
+ * shared-memory copy of the hub mailboxes.  nhubs = 0: plain col_idx.
+ * nhubs <= pgx_hub_capacity(). */
+int pgx_hub_capacity(int32_t *capacity);
+
 /* sssp(source) -- algorithms.py:116-152 (push, min, uint32 hops) */
 int pgx_sssp_run(int32_t n, int64_t m, const int32_t *row_ptr,
                  const int32_t *col_idx, const void *graph_ws,
+                 const int32_t *hub_ids, int32_t nhubs,
                  int32_t source, int32_t max_supersteps, uint32_t *dist,
                  void *run_ws, size_t run_ws_bytes, int64_t *stats,
                  uintptr_t stream);
@@ -120,6 +129,7 @@ int pgx_sssp_run(int32_t n, int64_t m, const int32_t *row_ptr,
 /* connected_components() -- algorithms.py:87-113 (Hashmin, min) */
 int pgx_cc_run(int32_t n, int64_t m, const int32_t *row_ptr,
                const int32_t *col_idx, const void *graph_ws,
+               const int32_t *hub_ids, int32_t nhubs,
                int32_t max_supersteps, uint32_t *labels, void *run_ws,
                size_t run_ws_bytes, int64_t *stats, uintptr_t stream);
 

@@ -16,7 +16,7 @@ from .errors import ConfigError, ExecutionError
 PKG_DIR = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.environ.get("PGX_LIB") or os.path.join(PKG_DIR, "libpgx.so")
 
-PGX_ABI_VERSION = 1
+PGX_ABI_VERSION = 2
 PGX_OK, PGX_EINVAL, PGX_ECUDA, PGX_ENOMEM = 0, -1, -2, -3
 PGX_APP_PAGERANK, PGX_APP_CC, PGX_APP_SSSP, PGX_APP_PAGERANK_PULL = 0, 1, 2, 3
 PGX_OP_MIN_U32, PGX_OP_SUM_F64 = 0, 1
@@ -32,7 +32,7 @@ def set_option(key: int, value: int) -> None:
 EXPORTS = (
     "pgx_abi_version", "pgx_last_error", "pgx_set_option", "pgx_device_sm_count",
     "pgx_offsets_to_i32", "pgx_graph_workspace_bytes", "pgx_graph_prepare",
-    "pgx_run_workspace_bytes", "pgx_sssp_run", "pgx_cc_run",
+    "pgx_run_workspace_bytes", "pgx_hub_capacity", "pgx_sssp_run", "pgx_cc_run",
     "pgx_pagerank_run", "pgx_pagerank_pull_run", "pgx_rmat_keys", "pgx_microbench",
     "pgx_slice_init", "pgx_scatter", "pgx_slice_counters_bytes", "pgx_apply_slice",
     "pgx_pr_apply_slice",
@@ -57,8 +57,11 @@ _SIGS = {
     "pgx_graph_workspace_bytes": (ctypes.c_int, [_i64, _i64, _p]),
     "pgx_graph_prepare": (ctypes.c_int, [_i32, _i64, _p, _p, _sz, _up]),
     "pgx_run_workspace_bytes": (ctypes.c_int, [ctypes.c_int, _i64, _i64, _i32, _p]),
-    "pgx_sssp_run": (ctypes.c_int, [_i32, _i64, _p, _p, _p, _i32, _i32, _p, _p, _sz, _p, _up]),
-    "pgx_cc_run": (ctypes.c_int, [_i32, _i64, _p, _p, _p, _i32, _p, _p, _sz, _p, _up]),
+    "pgx_hub_capacity": (ctypes.c_int, [_p]),
+    "pgx_sssp_run": (ctypes.c_int, [_i32, _i64, _p, _p, _p, _p, _i32, _i32, _i32, _p, _p, _sz,
+                                    _p, _up]),
+    "pgx_cc_run": (ctypes.c_int, [_i32, _i64, _p, _p, _p, _p, _i32, _i32, _p, _p, _sz, _p,
+                                  _up]),
     "pgx_pagerank_run": (ctypes.c_int, [_i32, _i64, _p, _p, _p, _i32, _f64, _f64, _f64,
                                         _i32, _p, _p, _sz, _p, _up]),
     "pgx_pagerank_pull_run": (ctypes.c_int, [_i32, _i64, _p, _p, _p, _p, _i32, _f64, _f64,

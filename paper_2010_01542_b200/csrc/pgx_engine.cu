@@ -54,6 +54,8 @@ constexpr int kTile = 32 * kItems;   // 256 edges per warp tile
 constexpr int kPass = PGX_PASS;      // rounds in flight per pass
 constexpr int kSlots = kTile + 2;    // sources per warp tile (+ sentinel)
 constexpr uint32_t kNeutralMin = 0xFFFFFFFFu;
+constexpr int kHubs = 12288;         // hub recipients cached per CTA (48 KB smem)
+constexpr int kInvalidEdge = 0x7FFFFFFF;  // never a vertex id (n < 2^31 - 1)
 constexpr int kMaxCtas = 4096;
 constexpr int kCompactBlock = 1024;
 
@@ -286,11 +288,17 @@ struct ScatterArgs {
   void *mailbox;
   uint32_t *has;          // has-message bitmask (min only; nullptr: none)
   int32_t id_offset;      // kSourceId: message = ids[i] + id_offset
+  const int32_t *hub_ids; // hub slot -> vertex; col_idx entries of hubs are
+  int32_t nhubs;          // (sign bit | slot).  nhubs == 0: no hub cache
 };
 
-// shared memory of the scatter: one source window per warp
+// shared memory of the scatter: one source window per warp (+ the hub
+// cache of the min combiner, right after the windows)
+__host__ __device__ constexpr size_t scatter_windows_smem(int op) {
+  return (size_t)kWarps * kSlots * (sizeof(int32_t) * 2 + (op == PGX_OP_SUM_F64 ? 8 : 4));
+}
 __host__ __device__ constexpr size_t scatter_smem(int op) {
-  return (size_t)kWarps * kSlots * (sizeof(int32_t) * 2 + (op == PGX_OP_SUM_F64 ? 8 : 4)) + 16;
+  return scatter_windows_smem(op) + (op == PGX_OP_MIN_U32 ? sizeof(uint32_t) * kHubs : 0) + 16;
 }
 
 // One superstep's scatter.  Every warp owns whole 256-edge tiles of the
@@ -303,8 +311,16 @@ __host__ __device__ constexpr size_t scatter_smem(int op) {
 //      bits that fall in the window gives every lane its source with one
 //      popc (sources have >= 1 edge, so <= 32 boundaries per window);
 //   3. the 8 neighbour ids are streamed (L1::no_allocate, L2 evict_first),
-//      then combined (min: read-filter + atomicMin, first publisher sets
-//      the has-message bit; sum: red.add.f64).
+//      then combined (min: read-filter + red.min, first publisher sets the
+//      has-message bit; sum: red.add.f64).
+// Hybrid combiner for hub recipients (the paper's split by recipient
+// class): the top in-degree vertices are flagged in the encoded col_idx
+// and filtered against a per-CTA shared-memory copy of their mailbox;
+// only a CTA-local improvement goes to the global red.min.
+#ifdef PGX_COUNT_OPS
+__device__ unsigned long long g_dbg_reds, g_dbg_bits, g_dbg_edges;
+#endif
+
 template <int OP, MsgSrc MS>
 __device__ void scatter_phase(const ScatterArgs &a, char *smem, bool read_filter = true) {
   using Msg = typename std::conditional<OP == PGX_OP_SUM_F64, double, uint32_t>::type;
@@ -320,6 +336,11 @@ __device__ void scatter_phase(const ScatterArgs &a, char *smem, bool read_filter
   const unsigned upto = (lane == 31) ? 0xFFFFFFFFu : ((2u << lane) - 1u);
   const int64_t gwarp = (int64_t)blockIdx.x * kWarps + warp;
   const int64_t nwarps = (int64_t)gridDim.x * kWarps;
+  uint32_t *s_hub = reinterpret_cast<uint32_t *>(smem + scatter_windows_smem(OP));
+  if (OP == PGX_OP_MIN_U32 && a.nhubs > 0) {  // block-uniform
+    for (int i = threadIdx.x; i < a.nhubs; i += blockDim.x) s_hub[i] = kNeutralMin;
+    __syncthreads();
+  }
 
   for (int64_t t = gwarp; t < ntiles; t += nwarps) {
     const int64_t e0 = t * kTile;
@@ -364,7 +385,7 @@ __device__ void scatter_phase(const ScatterArgs &a, char *smem, bool read_filter
         const unsigned bm = __reduce_or_sync(0xFFFFFFFFu, bit);
         const int src = cur + __popc(bm & upto);
         cur += __popc(bm);
-        w[r] = -1;
+        w[r] = kInvalidEdge;
         if (e < e1) {
           const int64_t pos = kDense ? e : (int64_t)s_rs[src] + (e - s_eb[src]);
           w[r] = ld_stream(a.col + pos, pol);
@@ -381,20 +402,42 @@ __device__ void scatter_phase(const ScatterArgs &a, char *smem, bool read_filter
         uint32_t *mb = reinterpret_cast<uint32_t *>(a.mailbox);
         uint32_t old[kPass];
 #pragma unroll
-        for (int r = 0; r < kPass; r++)
-          old[r] = (w[r] >= 0) ? (read_filter ? mb[w[r]] : kNeutralMin) : 0u;
+        for (int r = 0; r < kPass; r++) {
+          const int x = w[r];
+          old[r] = (x == kInvalidEdge) ? 0u
+                   : (x < 0) ? s_hub[x & 0x7FFFFFFF]  // hub: CTA-local filter
+                   : (read_filter ? mb[x] : kNeutralMin);
+        }
 #pragma unroll
         for (int r = 0; r < kPass; r++) {
-          if (w[r] >= 0 && (uint32_t)mv[r] < old[r]) {
-            red_min_u32(mb + w[r], (uint32_t)mv[r]);
-            if (a.has && old[r] == kNeutralMin) red_or_b32(a.has + (w[r] >> 5), 1u << (w[r] & 31));
+          const int x = w[r];
+          const uint32_t msg = (uint32_t)mv[r];
+          if (x != kInvalidEdge && msg < old[r]) {
+            int v = x;
+            uint32_t prev = old[r];
+            if (x < 0) {
+              const int slot = x & 0x7FFFFFFF;
+              prev = atomicMin(s_hub + slot, msg);
+              v = (msg < prev) ? a.hub_ids[slot] : -1;
+            }
+            if (v >= 0) {
+              red_min_u32(mb + v, msg);
+              if (a.has && prev == kNeutralMin) red_or_b32(a.has + (v >> 5), 1u << (v & 31));
+#ifdef PGX_COUNT_OPS
+              atomicAdd(&g_dbg_reds, 1ull);
+              if (prev == kNeutralMin) atomicAdd(&g_dbg_bits, 1ull);
+#endif
+            }
           }
+#ifdef PGX_COUNT_OPS
+          if (x != kInvalidEdge) atomicAdd(&g_dbg_edges, 1ull);
+#endif
         }
       } else {
         double *mb = reinterpret_cast<double *>(a.mailbox);
 #pragma unroll
         for (int r = 0; r < kPass; r++)
-          if (w[r] >= 0) atomicAdd(mb + w[r], (double)mv[r]);
+          if (w[r] != kInvalidEdge) atomicAdd(mb + w[r], (double)mv[r]);
       }
     }
   }
@@ -574,6 +617,8 @@ struct MinRunParams {
   int32_t source;  // SSSP only
   int32_t max_steps;
   int32_t read_filter;
+  const int32_t *hub_ids;
+  int32_t nhubs;
   int64_t *stats;
 };
 
@@ -626,6 +671,8 @@ __global__ void __launch_bounds__(kBlock, PGX_MIN_BLOCKS) min_run_kernel(MinRunP
     a.mailbox = mailbox;
     a.has = p.ws.has;
     a.id_offset = 0;
+    a.hub_ids = p.hub_ids;
+    a.nhubs = p.nhubs;
     if (APP == PGX_APP_CC && s == 0) {
       a.eb = p.g.nz_eb;
       a.rs = nullptr;
@@ -752,6 +799,8 @@ __global__ void __launch_bounds__(kBlock, PGX_MIN_BLOCKS) pagerank_run_kernel(Pr
   a.mailbox = mailbox;
   a.has = nullptr;
   a.id_offset = 0;
+  a.hub_ids = nullptr;
+  a.nhubs = 0;
   const unsigned long long ndangling = p.ws.misc[0];
   double dangling = __dmul_rn(p.r0, (double)ndangling);  // algorithms.py:55
   const int64_t nspread = (int64_t)p.n - (int64_t)ndangling;
@@ -1334,6 +1383,19 @@ int pgx_abi_version(void) { return PGX_ABI_VERSION; }
 
 const char *pgx_last_error(void) { return g_last_error.c_str(); }
 
+#ifdef PGX_COUNT_OPS
+extern "C" int pgx_debug_counts(unsigned long long *out3) {
+  cudaMemcpyFromSymbol(out3, g_dbg_reds, 8, 0);
+  cudaMemcpyFromSymbol(out3 + 1, g_dbg_bits, 8, 0);
+  cudaMemcpyFromSymbol(out3 + 2, g_dbg_edges, 8, 0);
+  unsigned long long z = 0;
+  cudaMemcpyToSymbol(g_dbg_reds, &z, 8, 0);
+  cudaMemcpyToSymbol(g_dbg_bits, &z, 8, 0);
+  cudaMemcpyToSymbol(g_dbg_edges, &z, 8, 0);
+  return 0;
+}
+#endif
+
 int pgx_set_option(int key, int value) {
   if (key < 0 || key >= PGX_OPT_COUNT) return fail(PGX_EINVAL, "unknown option");
   g_opt[key] = value;
@@ -1392,8 +1454,11 @@ int pgx_run_workspace_bytes(int app, int64_t n, int64_t m, int32_t max_superstep
 }
 
 static int min_run(int app, int32_t n, int64_t m, const int32_t *row_ptr, const int32_t *col_idx,
-                   const void *graph_ws, int32_t source, int32_t max_supersteps, uint32_t *val,
+                   const void *graph_ws, const int32_t *hub_ids, int32_t nhubs,
+                   int32_t source, int32_t max_supersteps, uint32_t *val,
                    void *run_ws, size_t run_ws_bytes, int64_t *stats, uintptr_t stream) {
+  if (nhubs < 0 || nhubs > kHubs || (nhubs > 0 && !hub_ids))
+    return fail(PGX_EINVAL, "hub count must be in [0, pgx_hub_capacity()]");
   int rc = check_graph(n, m, row_ptr, col_idx, graph_ws);
   if (rc) return rc;
   if (max_supersteps < 1) return fail(PGX_EINVAL, "superstep cap must be >= 1");
@@ -1412,6 +1477,8 @@ static int min_run(int app, int32_t n, int64_t m, const int32_t *row_ptr, const 
   p.source = source;
   p.max_steps = max_supersteps;
   p.read_filter = g_opt[PGX_OPT_READ_FILTER];
+  p.hub_ids = hub_ids;
+  p.nhubs = nhubs;
   p.stats = stats;
   cudaStream_t st = (cudaStream_t)stream;
   PGX_CUDA(cudaMemsetAsync(p.ws.bar, 0, 64, st));
@@ -1433,17 +1500,25 @@ static int min_run(int app, int32_t n, int64_t m, const int32_t *row_ptr, const 
 }
 
 int pgx_sssp_run(int32_t n, int64_t m, const int32_t *row_ptr, const int32_t *col_idx,
-                 const void *graph_ws, int32_t source, int32_t max_supersteps, uint32_t *dist,
-                 void *run_ws, size_t run_ws_bytes, int64_t *stats, uintptr_t stream) {
-  return min_run(PGX_APP_SSSP, n, m, row_ptr, col_idx, graph_ws, source, max_supersteps, dist,
-                 run_ws, run_ws_bytes, stats, stream);
+                 const void *graph_ws, const int32_t *hub_ids, int32_t nhubs, int32_t source,
+                 int32_t max_supersteps, uint32_t *dist, void *run_ws, size_t run_ws_bytes,
+                 int64_t *stats, uintptr_t stream) {
+  return min_run(PGX_APP_SSSP, n, m, row_ptr, col_idx, graph_ws, hub_ids, nhubs, source,
+                 max_supersteps, dist, run_ws, run_ws_bytes, stats, stream);
 }
 
 int pgx_cc_run(int32_t n, int64_t m, const int32_t *row_ptr, const int32_t *col_idx,
-               const void *graph_ws, int32_t max_supersteps, uint32_t *labels, void *run_ws,
-               size_t run_ws_bytes, int64_t *stats, uintptr_t stream) {
-  return min_run(PGX_APP_CC, n, m, row_ptr, col_idx, graph_ws, 0, max_supersteps, labels, run_ws,
-                 run_ws_bytes, stats, stream);
+               const void *graph_ws, const int32_t *hub_ids, int32_t nhubs,
+               int32_t max_supersteps, uint32_t *labels, void *run_ws, size_t run_ws_bytes,
+               int64_t *stats, uintptr_t stream) {
+  return min_run(PGX_APP_CC, n, m, row_ptr, col_idx, graph_ws, hub_ids, nhubs, 0,
+                 max_supersteps, labels, run_ws, run_ws_bytes, stats, stream);
+}
+
+int pgx_hub_capacity(int32_t *capacity) {
+  if (!capacity) return fail(PGX_EINVAL, "null out pointer");
+  *capacity = kHubs;
+  return PGX_OK;
 }
 
 int pgx_pagerank_run(int32_t n, int64_t m, const int32_t *row_ptr, const int32_t *col_idx,
@@ -1558,6 +1633,8 @@ int pgx_scatter(int op, int dense, const int32_t *col_idx, const int32_t *src_eb
   a.mailbox = mailbox;
   a.has = has_bits;
   a.id_offset = id_offset;
+  a.hub_ids = nullptr;
+  a.nhubs = 0;
   const int64_t tiles = ceil_div(edges, kTile);
   int sms = 148, dev = 0;
   if (cudaGetDevice(&dev) == cudaSuccess)

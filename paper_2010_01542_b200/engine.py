@@ -75,6 +75,10 @@ class EngineConfig:
     #: PageRank lowering: "pull" (the reference's comm mode, algorithms.py:80;
     #: in-neighbour fold, no atomics) or "push" (scatter with red.add.f64)
     pagerank_mode: str = "pull"
+    #: shared-memory combiner for hub recipients (CC / SSSP): "auto" builds
+    #: the hub encoding from the second run on a device CSR (amortised graph
+    #: preprocessing), "on" always, "off" never
+    hub_cache: str = "auto"
 
 
 @dataclass(frozen=True)
@@ -155,6 +159,8 @@ def _validate(program: VertexProgram, config: EngineConfig) -> None:
         raise ConfigError(f"bad combiner kind: {config.combiner!r}")
     if config.pagerank_mode not in ("pull", "push"):
         raise ConfigError(f"bad pagerank_mode: {config.pagerank_mode!r}")
+    if config.hub_cache not in ("auto", "on", "off"):
+        raise ConfigError(f"bad hub_cache: {config.hub_cache!r}")
     if program.comm_mode is CommMode.PUSH and program.combine is None:
         raise ConfigError("push-mode programs must declare a combine function")
     if config.combiner is CombinerKind.CAS and program.comm_mode is CommMode.PUSH \
@@ -215,6 +221,13 @@ class LaunchPlan:
     low: dict
     stream: Any
     pull: bool = False
+    hubs: bool = False
+
+    def _hub_args(self):
+        c = self.csr
+        if self.hubs:
+            return c.hub_col.data_ptr(), c.hub_ids.data_ptr(), int(c.hub_ids.numel())
+        return c.col_idx.data_ptr(), None, 0
 
     def launch(self) -> None:
         """Enqueue the persistent run kernel (asynchronous)."""
@@ -243,14 +256,16 @@ class LaunchPlan:
                                       self.ws_bytes, self.stats.data_ptr(), sp)
             _lib.check(rc, "pgx_pagerank_run")
         elif self.app == "components":
-            rc = lib.pgx_cc_run(c.n, c.m, c.row_ptr.data_ptr(), c.col_idx.data_ptr(),
-                                c.ws.data_ptr(), self.max_steps,
+            col, hub_ids, nh = self._hub_args()
+            rc = lib.pgx_cc_run(c.n, c.m, c.row_ptr.data_ptr(), col, c.ws.data_ptr(),
+                                hub_ids, nh, self.max_steps,
                                 self.values.data_ptr(), self.ws.data_ptr(),
                                 self.ws_bytes, self.stats.data_ptr(), sp)
             _lib.check(rc, "pgx_cc_run")
         else:
-            rc = lib.pgx_sssp_run(c.n, c.m, c.row_ptr.data_ptr(), c.col_idx.data_ptr(),
-                                  c.ws.data_ptr(), self.low["source"], self.max_steps,
+            col, hub_ids, nh = self._hub_args()
+            rc = lib.pgx_sssp_run(c.n, c.m, c.row_ptr.data_ptr(), col, c.ws.data_ptr(),
+                                  hub_ids, nh, self.low["source"], self.max_steps,
                                   self.values.data_ptr(), self.ws.data_ptr(),
                                   self.ws_bytes, self.stats.data_ptr(), sp)
             _lib.check(rc, "pgx_sssp_run")
@@ -280,6 +295,11 @@ def plan_run(graph: Graph, program: VertexProgram,
         max_steps = min(max_steps, int(low["iterations"]))
     if pull:
         csr.ensure_transpose(stream)
+    hubs = app != "pagerank" and (config.hub_cache == "on" or
+                                  (config.hub_cache == "auto" and csr.runs >= 1))
+    if hubs:
+        csr.ensure_hubs(stream)
+    csr.runs += 1
     app_id = _lib.PGX_APP_PAGERANK_PULL if pull else _APP_ID[app]
     ws_bytes = _lib.out_size(lib.pgx_run_workspace_bytes, app_id, n, m, max_steps)
     with torch.cuda.device(dev):
@@ -288,7 +308,7 @@ def plan_run(graph: Graph, program: VertexProgram,
                             dtype=torch.int64, device=dev)
         vdt = torch.float64 if app == "pagerank" else torch.int32
         values = torch.empty(n, dtype=vdt, device=dev)
-    return LaunchPlan(app, csr, values, stats, ws, ws_bytes, max_steps, low, stream, pull)
+    return LaunchPlan(app, csr, values, stats, ws, ws_bytes, max_steps, low, stream, pull, hubs)
 
 
 def collect(plan: LaunchPlan, program: VertexProgram, wall: float | None = None) -> RunReport:

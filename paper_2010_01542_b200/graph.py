@@ -21,6 +21,7 @@ byte-compatible with the reference (``PGLCSR1`` format, graph.py:298-373).
 
 from __future__ import annotations
 
+import ctypes
 import io
 import os
 from dataclasses import dataclass
@@ -57,6 +58,38 @@ class DeviceCSR:
     in_row_ptr: torch.Tensor | None = None   # int32 [n+1] transpose (pull mode)
     in_col: torch.Tensor | None = None       # int32 [m], rows sorted by source
     in_ws: torch.Tensor | None = None        # tile map of the transpose
+    hub_col: torch.Tensor | None = None      # col_idx with hub edges encoded
+    hub_ids: torch.Tensor | None = None      # hub slot -> vertex
+    runs: int = 0                            # device runs on this CSR
+
+    def ensure_hubs(self, stream=None) -> None:
+        """Encode the hub recipients for the scatter's shared-memory combiner.
+
+        Hubs are the (at most pgx_hub_capacity) highest in-degree vertices;
+        an edge into hub h is stored as (0x80000000 | slot(h)).  Graph
+        preprocessing, amortised over repeated runs (engine: from the
+        second run on a device CSR when ``hub_cache="auto"``).
+        """
+        if self.hub_col is not None:
+            return
+        dev = self.row_ptr.device
+        st = torch.cuda.current_stream(dev) if stream is None else stream
+        lib = _lib.load()
+        cap = ctypes.c_int32(0)
+        _lib.check(lib.pgx_hub_capacity(ctypes.byref(cap)), "pgx_hub_capacity")
+        with torch.cuda.device(dev), torch.cuda.stream(st):
+            col = self.col_idx.to(torch.int64)
+            indeg = torch.bincount(col, minlength=self.n)
+            h = min(int(cap.value), self.n)
+            vals, idx = torch.topk(indeg, h, sorted=True)
+            idx = idx[vals >= 2]          # a hub must receive >= 2 edges
+            slot = torch.full((self.n,), -1, dtype=torch.int32, device=dev)
+            slot[idx] = torch.arange(idx.numel(), dtype=torch.int32, device=dev)
+            s = slot[col]
+            del col
+            enc = torch.where(s >= 0, s | torch.tensor(-2 ** 31, dtype=torch.int32, device=dev),
+                              self.col_idx)
+            self.hub_col, self.hub_ids = enc.contiguous(), idx.to(torch.int32).contiguous()
 
     def ensure_transpose(self, stream=None) -> None:
         """Build the in-CSR on the device (sort by (dst, src)), once."""

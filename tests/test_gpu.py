@@ -49,15 +49,18 @@ def rel_err(got, want):
     return float(np.max(np.abs(got - want) / np.abs(want)))
 
 
-@pytest.mark.parametrize("mode", ["pull", "push"])
+@pytest.mark.parametrize("mode", ["pull", "push", "hubs"])
 @pytest.mark.parametrize("r", RUNS, ids=lambda r: r.id)
 def test_golden_reference_runs(r, mode):
     if mode == "push" and r.app != "pagerank":
         pytest.skip("pagerank_mode only changes the PageRank lowering")
+    if mode == "hubs" and r.app == "pagerank":
+        pytest.skip("hub_cache only changes the min combiner")
     g = pgx.from_edges(r.src, r.dst, r.n, undirected=r.undirected, device="cuda")
     cap = r.kwargs.get("max_supersteps")
     cfg = pgx.EngineConfig(max_supersteps=cap if cap else pgx.DEFAULT_MAX_SUPERSTEPS,
-                           pagerank_mode=mode)
+                           pagerank_mode="push" if mode == "push" else "pull",
+                           hub_cache="on" if mode == "hubs" else "off")
     rep = pgx.run(g, program(r.app, r.kwargs), cfg)
     if r.app == "pagerank":
         assert rep.values.dtype == np.float64
@@ -198,9 +201,10 @@ def test_c1_pagerank_vs_oracle(graphs, mode):
     assert abs(rep.values[0] - 0.005883584525755893) / 0.005883584525755893 <= PR_RTOL
 
 
-def test_c2_components_known_answer(graphs):
+@pytest.mark.parametrize("hubs", ["off", "on"])
+def test_c2_components_known_answer(graphs, hubs):
     g = graphs("C2")
-    rep = pgx.run(g, pgx.connected_components())
+    rep = pgx.run(g, pgx.connected_components(), pgx.EngineConfig(hub_cache=hubs))
     assert sha(rep.values.astype(np.uint32), "<u4") == \
         "c4e2cc1d7b5db62b9818e1cd41611649a294c5623d7e29804c175f904c40bf98"
     assert [s.active_count for s in rep.supersteps] == \
@@ -212,11 +216,12 @@ def test_c2_components_known_answer(graphs):
     assert len(np.unique(rep.values)) == 2_186_257
 
 
-def test_c3_sssp_known_answer(graphs):
+@pytest.mark.parametrize("hubs", ["off", "on"])
+def test_c3_sssp_known_answer(graphs, hubs):
     g = graphs("C3")
     src = int(torch.argmax(g.out_degrees))
     assert src == 0
-    rep = pgx.run(g, pgx.sssp(src))
+    rep = pgx.run(g, pgx.sssp(src), pgx.EngineConfig(hub_cache=hubs))
     assert sha(rep.values, "<u4") == \
         "bd08774026f70bbd29b80c977187f880654c0d8cbd2b42ba0988fed279ffa1e2"
     assert [s.active_count for s in rep.supersteps] == \
