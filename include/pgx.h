@@ -233,6 +233,9 @@ int pgx_rmat_keys(int32_t scale, int64_t first_draw, int64_t num_draws,
 #define PGX_MB_RED_MIN_U32 2   /* min combine: red.min.u32 */
 #define PGX_MB_RED_ADD_F64 3   /* sum combine: red.add.f64 */
 #define PGX_MB_ATOM_MIN_U32 4  /* atomicMin.u32 with return value */
+#define PGX_MB_LOAD_U32_CG 5   /* ld.global.cg u32 (L2 only) */
+#define PGX_MB_LOAD_U32_NA 6   /* ld.global.L1::no_allocate u32 */
+#define PGX_MB_LOAD_U32_RELAXED 7  /* ld.relaxed.gpu u32 */
 int pgx_microbench(int kind, void *buf, int64_t n_elems, int64_t n_ops,
                    uint64_t seed, float *ms, uintptr_t stream);
 

@@ -297,8 +297,8 @@ struct ScatterArgs {
 __host__ __device__ constexpr size_t scatter_windows_smem(int op) {
   return (size_t)kWarps * kSlots * (sizeof(int32_t) * 2 + (op == PGX_OP_SUM_F64 ? 8 : 4));
 }
-__host__ __device__ constexpr size_t scatter_smem(int op) {
-  return scatter_windows_smem(op) + (op == PGX_OP_MIN_U32 ? sizeof(uint32_t) * kHubs : 0) + 16;
+__host__ __device__ constexpr size_t scatter_smem(int op, int nhubs = 0) {
+  return scatter_windows_smem(op) + (op == PGX_OP_MIN_U32 ? sizeof(uint32_t) * nhubs : 0) + 16;
 }
 
 // One superstep's scatter.  Every warp owns whole 256-edge tiles of the
@@ -415,10 +415,13 @@ __device__ void scatter_phase(const ScatterArgs &a, char *smem, bool read_filter
           if (x != kInvalidEdge && msg < old[r]) {
             int v = x;
             uint32_t prev = old[r];
-            if (x < 0) {
+            if (x < 0) {  // hub: the CTA-local copy let it through; consult
+                          // the global slot (the shared filter) before the red
               const int slot = x & 0x7FFFFFFF;
-              prev = atomicMin(s_hub + slot, msg);
-              v = (msg < prev) ? a.hub_ids[slot] : -1;
+              v = a.hub_ids[slot];
+              prev = mb[v];
+              s_hub[slot] = min(prev, msg);  // racy store: only weakens the filter
+              if (msg >= prev) v = -1;
             }
             if (v >= 0) {
               red_min_u32(mb + v, msg);
@@ -1482,7 +1485,7 @@ static int min_run(int app, int32_t n, int64_t m, const int32_t *row_ptr, const 
   p.stats = stats;
   cudaStream_t st = (cudaStream_t)stream;
   PGX_CUDA(cudaMemsetAsync(p.ws.bar, 0, 64, st));
-  const size_t smem = scatter_smem_bytes(PGX_OP_MIN_U32);
+  const size_t smem = scatter_smem(PGX_OP_MIN_U32, nhubs);
   int grid = 0;
   void *args[] = {&p};
   if (app == PGX_APP_SSSP) {

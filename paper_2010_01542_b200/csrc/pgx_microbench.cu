@@ -50,6 +50,20 @@ __global__ void __launch_bounds__(256) random_access_kernel(void *buf, uint64_t 
       for (int j = 0; j < 8; j++) v[j] = __ldg(d + idx[j]);
 #pragma unroll
       for (int j = 0; j < 8; j++) dacc += v[j];
+    } else if (KIND == PGX_MB_LOAD_U32_CG || KIND == PGX_MB_LOAD_U32_NA ||
+               KIND == PGX_MB_LOAD_U32_RELAXED) {
+      uint32_t v[8];
+#pragma unroll
+      for (int j = 0; j < 8; j++) {
+        if (KIND == PGX_MB_LOAD_U32_CG)
+          asm volatile("ld.global.cg.u32 %0, [%1];" : "=r"(v[j]) : "l"(u + idx[j]));
+        else if (KIND == PGX_MB_LOAD_U32_NA)
+          asm volatile("ld.global.L1::no_allocate.u32 %0, [%1];" : "=r"(v[j]) : "l"(u + idx[j]));
+        else
+          asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v[j]) : "l"(u + idx[j]));
+      }
+#pragma unroll
+      for (int j = 0; j < 8; j++) acc += v[j];
     } else if (KIND == PGX_MB_RED_MIN_U32) {
 #pragma unroll
       for (int j = 0; j < 8; j++)
@@ -105,6 +119,9 @@ extern "C" int pgx_microbench(int kind, void *buf, int64_t n_elems, int64_t n_op
       case PGX_MB_RED_MIN_U32: e = launch<PGX_MB_RED_MIN_U32>(buf, mask, per_thread, seed, sink, grid, st); break;
       case PGX_MB_RED_ADD_F64: e = launch<PGX_MB_RED_ADD_F64>(buf, mask, per_thread, seed, sink, grid, st); break;
       case PGX_MB_ATOM_MIN_U32: e = launch<PGX_MB_ATOM_MIN_U32>(buf, mask, per_thread, seed, sink, grid, st); break;
+      case PGX_MB_LOAD_U32_CG: e = launch<PGX_MB_LOAD_U32_CG>(buf, mask, per_thread, seed, sink, grid, st); break;
+      case PGX_MB_LOAD_U32_NA: e = launch<PGX_MB_LOAD_U32_NA>(buf, mask, per_thread, seed, sink, grid, st); break;
+      case PGX_MB_LOAD_U32_RELAXED: e = launch<PGX_MB_LOAD_U32_RELAXED>(buf, mask, per_thread, seed, sink, grid, st); break;
       default: e = cudaErrorInvalidValue;
     }
     cudaEventRecord(b, st);

@@ -75,10 +75,11 @@ class EngineConfig:
     #: PageRank lowering: "pull" (the reference's comm mode, algorithms.py:80;
     #: in-neighbour fold, no atomics) or "push" (scatter with red.add.f64)
     pagerank_mode: str = "pull"
-    #: shared-memory combiner for hub recipients (CC / SSSP): "auto" builds
+    #: shared-memory combiner for hub recipients (CC / SSSP, ablation arm;
+    #: measured slower on B200): "auto" builds
     #: the hub encoding from the second run on a device CSR (amortised graph
     #: preprocessing), "on" always, "off" never
-    hub_cache: str = "auto"
+    hub_cache: str = "off"
 
 
 @dataclass(frozen=True)

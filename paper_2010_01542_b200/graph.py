@@ -80,7 +80,7 @@ class DeviceCSR:
         with torch.cuda.device(dev), torch.cuda.stream(st):
             col = self.col_idx.to(torch.int64)
             indeg = torch.bincount(col, minlength=self.n)
-            h = min(int(cap.value), self.n)
+            h = min(int(cap.value), self.n, int(os.environ.get("PGX_HUBS", cap.value)))
             vals, idx = torch.topk(indeg, h, sorted=True)
             idx = idx[vals >= 2]          # a hub must receive >= 2 edges
             slot = torch.full((self.n,), -1, dtype=torch.int32, device=dev)

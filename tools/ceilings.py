@@ -6,12 +6,15 @@ import torch
 from paper_2010_01542_b200 import _lib
 
 lib = _lib.load()
-kinds = {"load_u32": 0, "load_f64": 1, "red_min_u32": 2, "red_add_f64": 3, "atom_min_u32": 4}
+kinds = {"load_u32": 0, "load_f64": 1, "red_min_u32": 2, "red_add_f64": 3, "atom_min_u32": 4,
+         "load_u32_cg": 5, "load_u32_l1_no_allocate": 6, "load_u32_relaxed_gpu": 7}
+if len(sys.argv) > 2:
+    kinds = {k: v for k, v in kinds.items() if k in sys.argv[2].split(",")}
 out = {"gpu": torch.cuda.get_device_name(0), "when": time.strftime("%Y-%m-%dT%H:%M:%SZ", time.gmtime()),
        "how": "pgx_microbench: uniformly random slots (counter hash), 8 in flight/thread, "
               "148x8 CTAs x 256 threads, second launch timed with CUDA events", "results": []}
 ops = 1 << 30
-for size_mb in (16, 64, 1024):
+for size_mb in ((16,) if len(sys.argv) > 2 else (16, 64, 1024)):
     for name, k in kinds.items():
         elem = 8 if "f64" in name else 4
         n = (size_mb << 20) // elem

@@ -21,7 +21,7 @@ for c in cfgs:
     prog = pgx.pagerank() if app == "pagerank" else pgx.connected_components() if app == "components" \
         else pgx.sssp(int(torch.argmax(g.out_degrees)))
     mode = os.environ.get("PR_MODE", "pull")
-    plan = pgx.plan_run(g, prog, pgx.EngineConfig(pagerank_mode=mode, hub_cache=os.environ.get("HUBS", "on")))
+    plan = pgx.plan_run(g, prog, pgx.EngineConfig(pagerank_mode=mode, hub_cache=os.environ.get("HUBS", "off")))
     best = None
     for r in range(reps):
         s = torch.cuda.Event(enable_timing=True); e = torch.cuda.Event(enable_timing=True)
