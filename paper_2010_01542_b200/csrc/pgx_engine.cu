@@ -41,6 +41,9 @@
 #ifndef PGX_MIN_BLOCKS
 #define PGX_MIN_BLOCKS 2
 #endif
+#ifndef PGX_SCATTER_SMEM
+#define PGX_SCATTER_SMEM 1   // stage each warp tile's sources in shared memory
+#endif
 
 namespace {
 
@@ -56,6 +59,7 @@ constexpr int kSlots = kTile + 2;    // sources per warp tile (+ sentinel)
 constexpr uint32_t kNeutralMin = 0xFFFFFFFFu;
 constexpr int kHubs = 12288;         // hub recipients cached per CTA (48 KB smem)
 constexpr int kInvalidEdge = 0x7FFFFFFF;  // never a vertex id (n < 2^31 - 1)
+constexpr int kApplyListBytes = 64 * 32 * 4;  // apply: kApplyWords * 32 vertex ids
 constexpr int kMaxCtas = 4096;
 constexpr int kCompactBlock = 1024;
 
@@ -110,11 +114,16 @@ __device__ __forceinline__ int ld_stream(const int *p, uint64_t pol) {
   return v;
 }
 
-__device__ __forceinline__ int4 ld_stream4(const int4 *p, uint64_t pol) {
-  int4 v;
-  asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.v4.s32 {%0, %1, %2, %3}, [%4], %5;"
-               : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "l"(p), "l"(pol));
-  return v;
+
+// 32-byte streamed load (sm_100: LDG.E.NA.ENL2.256) -- a warp reading
+// 32 consecutive 32-byte chunks touches exactly 32 fully used sectors
+__device__ __forceinline__ void ld_stream8(const int *p, uint64_t pol, int (&v)[8]) {
+  asm volatile(
+      "ld.global.nc.L1::no_allocate.L2::cache_hint.v8.b32 {%0, %1, %2, %3, %4, %5, %6, %7}, "
+      "[%8], %9;"
+      : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]),
+        "=r"(v[7])
+      : "l"(p), "l"(pol));
 }
 
 __device__ __forceinline__ uint64_t evict_first_policy() {
@@ -295,7 +304,9 @@ struct ScatterArgs {
 // shared memory of the scatter: one source window per warp (+ the hub
 // cache of the min combiner, right after the windows)
 __host__ __device__ constexpr size_t scatter_windows_smem(int op) {
-  return (size_t)kWarps * kSlots * (sizeof(int32_t) * 2 + (op == PGX_OP_SUM_F64 ? 8 : 4));
+  return PGX_SCATTER_SMEM
+             ? (size_t)kWarps * kSlots * (sizeof(int32_t) * 2 + (op == PGX_OP_SUM_F64 ? 8 : 4))
+             : (size_t)kApplyListBytes;  // the apply's recipient list still needs smem
 }
 __host__ __device__ constexpr size_t scatter_smem(int op, int nhubs = 0) {
   return scatter_windows_smem(op) + (op == PGX_OP_MIN_U32 ? sizeof(uint32_t) * nhubs : 0) + 16;
@@ -348,6 +359,7 @@ __device__ void scatter_phase(const ScatterArgs &a, char *smem, bool read_filter
     const int i0 = a.tile_src[t];
     const int i1 = (t + 1 < ntiles) ? a.tile_src[t + 1] : a.nsrc - 1;
     const int k = i1 - i0 + 1;  // <= kTile + 1
+#if PGX_SCATTER_SMEM
     __syncwarp();
     for (int j = lane; j <= k; j += 32) {
       const int i = i0 + j;
@@ -366,8 +378,24 @@ __device__ void scatter_phase(const ScatterArgs &a, char *smem, bool read_filter
       }
     }
     __syncwarp();
+#define PGX_EB(j) s_eb[j]
+#define PGX_RS(j) s_rs[j]
+#define PGX_MSG(j) s_msg[j]
+#else
+    // no staging: boundary candidates are 32 consecutive ints (one or two
+    // sectors per round) and per-source data are broadcast loads, both
+    // L1 hits after the first round -- all of shared memory stays L1
+    const int32_t *g_eb = a.eb + i0;
+    const int nrem = a.nsrc - i0;
+#define PGX_EB(j) ((j) < nrem ? __ldg(g_eb + (j)) : (int32_t)a.E)
+#define PGX_RS(j) __ldg(a.rs + i0 + (j))
+#define PGX_MSG(j)                                                              \
+  (MS == MsgSrc::kFrontier ? __ldg(reinterpret_cast<const Msg *>(a.msg) + i0 + (j)) \
+   : MS == MsgSrc::kSourceId ? (Msg)(__ldg(a.ids + i0 + (j)) + a.id_offset)       \
+   : __ldg(reinterpret_cast<const Msg *>(a.msg) + __ldg(a.ids + i0 + (j))))
+#endif
 
-    int cur = 0;  // s_eb[0] <= e0: tile_src names the source holding e0
+    int cur = 0;  // eb[0] <= e0: tile_src names the source holding e0
 #pragma unroll 1
     for (int pass = 0; pass < kItems / kPass; pass++) {
       int w[kPass];
@@ -379,7 +407,7 @@ __device__ void scatter_phase(const ScatterArgs &a, char *smem, bool read_filter
         const int ci = cur + 1 + lane;
         unsigned bit = 0;
         if (ci <= k) {
-          const int64_t pp = (int64_t)s_eb[ci] - base;
+          const int64_t pp = (int64_t)PGX_EB(ci) - base;
           if (pp >= 0 && pp < 32) bit = 1u << pp;
         }
         const unsigned bm = __reduce_or_sync(0xFFFFFFFFu, bit);
@@ -387,9 +415,9 @@ __device__ void scatter_phase(const ScatterArgs &a, char *smem, bool read_filter
         cur += __popc(bm);
         w[r] = kInvalidEdge;
         if (e < e1) {
-          const int64_t pos = kDense ? e : (int64_t)s_rs[src] + (e - s_eb[src]);
+          const int64_t pos = kDense ? e : (int64_t)PGX_RS(src) + (e - PGX_EB(src));
           w[r] = ld_stream(a.col + pos, pol);
-          mv[r] = s_msg[src];
+          mv[r] = PGX_MSG(src);
         }
       }
       if (OP == PGX_OP_MIN_U32) {
@@ -443,6 +471,9 @@ __device__ void scatter_phase(const ScatterArgs &a, char *smem, bool read_filter
           if (w[r] != kInvalidEdge) atomicAdd(mb + w[r], (double)mv[r]);
       }
     }
+#undef PGX_EB
+#undef PGX_RS
+#undef PGX_MSG
   }
 }
 
@@ -912,10 +943,7 @@ __device__ void gather_phase(const GatherArgs &a, char *smem) {
     const bool active = a0 < e1;
     int col[8];
     if (active && a1 - a0 == 8) {
-      const int4 c0 = ld_stream4(reinterpret_cast<const int4 *>(a.in_col + a0), pol);
-      const int4 c1 = ld_stream4(reinterpret_cast<const int4 *>(a.in_col + a0) + 1, pol);
-      col[0] = c0.x; col[1] = c0.y; col[2] = c0.z; col[3] = c0.w;
-      col[4] = c1.x; col[5] = c1.y; col[6] = c1.z; col[7] = c1.w;
+      ld_stream8(a.in_col + a0, pol, col);
     } else {
 #pragma unroll
       for (int j = 0; j < 8; j++) col[j] = (a0 + j < a1) ? ld_stream(a.in_col + a0 + j, pol) : -1;
@@ -1121,8 +1149,12 @@ struct SliceCounters {       // device counters of one partitioned superstep
   double dangling;           // PageRank: rank mass of owned dangling vertices
 };
 
+#ifndef PGX_SCATTER_MIN_BLOCKS
+#define PGX_SCATTER_MIN_BLOCKS PGX_MIN_BLOCKS
+#endif
+
 template <int OP, MsgSrc MS>
-__global__ void __launch_bounds__(kBlock, PGX_MIN_BLOCKS) scatter_kernel(ScatterArgs a,
+__global__ void __launch_bounds__(kBlock, PGX_SCATTER_MIN_BLOCKS) scatter_kernel(ScatterArgs a,
                                                                           int read_filter) {
   extern __shared__ __align__(16) char smem[];
   scatter_phase<OP, MS>(a, smem, read_filter != 0);
@@ -1643,7 +1675,7 @@ int pgx_scatter(int op, int dense, const int32_t *col_idx, const int32_t *src_eb
   if (cudaGetDevice(&dev) == cudaSuccess)
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(ceil_div(tiles, kWarps),
-                                                               (int64_t)sms * PGX_MIN_BLOCKS));
+                                                               (int64_t)sms * PGX_SCATTER_MIN_BLOCKS));
   cudaStream_t st = (cudaStream_t)stream;
   const size_t smem = scatter_smem(op);
   const int rf = g_opt[PGX_OPT_READ_FILTER];
