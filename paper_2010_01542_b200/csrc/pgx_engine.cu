@@ -951,13 +951,24 @@ __device__ void gather_phase(const GatherArgs &a, char *smem) {
     double x[8];
 #pragma unroll
     for (int j = 0; j < 8; j++) x[j] = (col[j] >= 0) ? __ldg(a.share + col[j]) : 0.0;
-    // row holding a0: largest idx with s_eb[idx] <= a0
+    // row holding a0: largest idx with s_eb[idx] <= a0 (binary search over
+    // the <= 258 staged row starts), then the starts of the next 8 rows as
+    // a boundary bitmask over the lane's 9 positions a0..a0+8, so the walk
+    // below runs on registers only
     int cur = 0;
+    unsigned bmask = 0;
     if (active) {
       int hi = k;
       while (hi - cur > 1) {
         const int mid = (cur + hi) >> 1;
         if ((int64_t)s_eb[mid] <= a0) cur = mid; else hi = mid;
+      }
+#pragma unroll
+      for (int i = 1; i <= 8; i++) {
+        if (cur + i <= k) {
+          const int64_t p = (int64_t)s_eb[cur + i] - a0;  // > 0 by construction
+          if (p <= 8) bmask |= 1u << p;
+        }
       }
     }
     const int first_seg = cur;
@@ -967,8 +978,7 @@ __device__ void gather_phase(const GatherArgs &a, char *smem) {
     for (int j = 0; j <= 8; j++) {
       const int64_t e = a0 + j;
       if (!active || e > a1) break;
-      // close the current row if the next row starts at e (e == a1: range end)
-      if (cur + 1 <= k && (int64_t)s_eb[cur + 1] <= e) {
+      if ((bmask >> j) & 1u) {  // the next row starts at e (e == a1: range end)
         if (cur == first_seg) {
           first_closed = true;
           first_part = acc;
