@@ -1,0 +1,45 @@
+"""C5 at full size on one B200 (n = 2^26, m = 1.84e9): BASELINE.md section 3.
+
+The reference cannot run C5 (~200 GB for its Python engine);
+BASELINE.md's answers come from the survey's C++ restatement, validated
+against the reference on C2.  Needs ~85 GiB of HBM for input generation.
+"""
+
+import hashlib
+
+import numpy as np
+import pytest
+import torch
+
+import paper_2010_01542_b200 as pgx
+from paper_2010_01542_b200.rmat import rmat_graph
+
+pytestmark = [pytest.mark.gpu, pytest.mark.slow]
+
+
+def sha(a, dt):
+    a = a.cpu().numpy() if isinstance(a, torch.Tensor) else a
+    return hashlib.sha256(np.ascontiguousarray(a.astype(dt, copy=False)).tobytes()).hexdigest()
+
+
+def test_c5_components_known_answer():
+    if torch.cuda.get_device_properties(0).total_memory < 120 * 2 ** 30:
+        pytest.skip("needs a 180 GB B200")
+    torch.cuda.empty_cache()
+    g = rmat_graph("C5")
+    assert (g.vertex_count, g.edge_count) == (67_108_864, 1_844_208_942)
+    assert sha(g.out_offsets, "<i8") == \
+        "f614c1f95e1a3306eb010a577c7da219b35785190bacf6375eb96f4532514738"
+    assert sha(g.out_targets, "<i4") == \
+        "7809334f406f147b22e18001f03fd95659dd863d8a4d96636ee0025d7d761880"
+    rep = pgx.run(g, pgx.connected_components())
+    assert sha(rep.values, "<u4") == \
+        "2667f2ecc3e6e7cb00c5c53f2b8af394b2802cbd19de2a9e1b8122490b4b1154"
+    assert [s.active_count for s in rep.supersteps] == \
+        [67108864, 31691446, 31654625, 24001955, 2770014, 15744, 43]
+    assert [s.messages_sent for s in rep.supersteps] == \
+        [67108864, 28808188, 30736448, 3973129, 15743, 43, 0]
+    assert [s.edges for s in rep.supersteps] == \
+        [1844208942, 1838211760, 801105854, 5102558, 15802, 43, 0]
+    del g, rep
+    torch.cuda.empty_cache()
