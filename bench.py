@@ -452,13 +452,17 @@ def bench_reference(args):
     in_off, in_tgt = (None, None) if app == "sssp" else O.transpose(n, off, tgt)
     threads = O.max_threads()
     src = int(np.argmax(np.diff(off)))
+    # C5 (1.8e9 edges): a bounded sample -- the first 2 supersteps (2/3 of
+    # the run's edges); every other config runs to completion
+    cap = 2 if cfg == "C5" else 10_000
 
     def once():
         if app == "pagerank":
-            return O.run_pagerank(n, off, tgt, 10, 0.85, in_off, in_tgt, threads=threads)
+            return O.run_pagerank(n, off, tgt, 10, 0.85, in_off, in_tgt, max_steps=cap,
+                                  threads=threads)
         if app == "components":
-            return O.run_cc(n, off, tgt, in_off, in_tgt, threads=threads)
-        return O.run_sssp(n, off, tgt, src, threads=threads)
+            return O.run_cc(n, off, tgt, in_off, in_tgt, max_steps=cap, threads=threads)
+        return O.run_sssp(n, off, tgt, src, max_steps=cap, threads=threads)
 
     for _ in range(min(args.warmup, 1)):
         once()
@@ -470,12 +474,15 @@ def bench_reference(args):
         secs += time.perf_counter() - t
         edges += sum(r.edges)
     v = edges / secs / 1e9
-    sample = (f"{steps} full {cfg} {app} run(s) of the oracle port of pregelite's "
+    what = "full" if cap > 100 else f"first-{cap}-superstep"
+    sample = (f"{steps} {what} {cfg} {app} run(s) of the oracle port of pregelite's "
               f"engine (oracle/pregel_oracle.c), {threads} OpenMP threads")
     line = {"metric": METRIC, "value": round(v, 5), "unit": "GTEPS", "impl": "reference",
             "n_gpus": int(os.environ.get("WORLD_SIZE", "1")), "steps": steps,
             "warmup": min(args.warmup, 1), "ms_per_step": round(secs / steps * 1e3, 3),
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "higher_is_better": True,
+            "scaling": "strong" if int(os.environ.get("WORLD_SIZE", "1")) > 1 else "weak",
+            "vs_baseline": None,
             "dtype": "u32" if app != "pagerank" else "f64", "data": "synthetic R-MAT",
             "config": {"workload": f"{cfg}: {app}, n={n}, m={tgt.size}"},
             "cpu_baseline": {"value": round(v, 5), "unit": "GTEPS", "cores": threads,
@@ -492,13 +499,18 @@ def main():
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--e2e-steps", type=int, default=5)
     ap.add_argument("--impl", default="pgx", choices=["pgx", "reference"])
-    ap.add_argument("--config", default="C2", choices=sorted(APP_OF))
+    ap.add_argument("--config", default=None, choices=sorted(APP_OF),
+                    help="BASELINE config; default C2 (configs[1]) at N=1, "
+                         "C5 (the 1/2/4/8-GPU config) under torchrun N>1")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-per-config", action="store_true")
     ap.add_argument("--aux-steps", type=int, default=5)
     ap.add_argument("--pr-push", dest="pr_pull", action="store_false",
                     help="PageRank A/B arm: push scatter with red.add.f64")
     args = ap.parse_args()
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    if args.config is None:
+        args.config = "C5" if world > 1 else "C2"
     if args.warmup < 3 and args.impl == "pgx":
         args.warmup = 3
     if args.impl == "reference":
