@@ -59,7 +59,7 @@ constexpr int kSlots = kTile + 2;    // sources per warp tile (+ sentinel)
 constexpr uint32_t kNeutralMin = 0xFFFFFFFFu;
 constexpr int kHubs = 12288;         // hub recipients cached per CTA (48 KB smem)
 constexpr int kInvalidEdge = 0x7FFFFFFF;  // never a vertex id (n < 2^31 - 1)
-constexpr int kApplyListBytes = 64 * 32 * 4;  // apply: kApplyWords * 32 vertex ids
+constexpr int kApplyListBytes = 128 * 32 * 4;  // apply: up to 128 words * 32 vertex ids
 constexpr int kMaxCtas = 4096;
 constexpr int kCompactBlock = 1024;
 
@@ -516,7 +516,10 @@ __device__ __forceinline__ unsigned long long block_excl_scan_u64(unsigned long 
 // bits are first compacted into a shared-memory vertex list (block scan
 // of popcounts), then every thread consumes up to kApplyItems recipients
 // with independent loads -- no per-word serial chains.
-constexpr int kApplyWords = 64;
+#ifndef PGX_APPLY_WORDS
+#define PGX_APPLY_WORDS 64
+#endif
+constexpr int kApplyWords = PGX_APPLY_WORDS;
 constexpr int kApplyItems = kApplyWords * 32 / kBlock;  // 4
 
 // Returns (recipients counted) << 32 | (broadcasts) for this thread.  With
