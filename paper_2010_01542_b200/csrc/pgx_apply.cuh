@@ -1,0 +1,175 @@
+// pgx_apply.cuh -- K2, the superstep's apply for the min programs: consume
+// the mailbox, compute (adopt an improvement), vote to halt, build the next
+// frontier.  Reference: _chunk_push (engine.py:402-414), the computes of
+// connected_components / sssp (algorithms.py:99-108, 136-147),
+// _next_frontier (engine.py:349-365).
+#pragma once
+
+#include "pgx_common.cuh"
+
+namespace pgx {
+
+// ------------------------------------------------------------------
+// sparse apply for the min programs (SSSP / CC), driven by the
+// has-message bitmask: consume every flagged mailbox (vertex order),
+// adopt an improvement, append improved vertices to the next frontier
+// with their edge prefix.  One 64-bit atomic per block chunk reserves
+// (frontier slots, edge range); the tile map is written as a side effect.
+// ------------------------------------------------------------------
+
+__device__ __forceinline__ unsigned long long block_excl_scan_u64(unsigned long long x,
+                                                                  unsigned long long *s_w,
+                                                                  unsigned long long *total) {
+  unsigned long long incl = x;
+  for (int o = 1; o < 32; o <<= 1) {
+    const unsigned long long y = __shfl_up_sync(0xFFFFFFFFu, incl, o);
+    if ((int)lane_id() >= o) incl += y;
+  }
+  if (lane_id() == 31) s_w[threadIdx.x >> 5] = incl;
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    const unsigned long long w = (threadIdx.x < kWarps) ? s_w[threadIdx.x] : 0ull;
+    unsigned long long wi = w;
+    for (int o = 1; o < 32; o <<= 1) {
+      const unsigned long long y = __shfl_up_sync(0xFFFFFFFFu, wi, o);
+      if ((int)threadIdx.x >= o) wi += y;
+    }
+    if (threadIdx.x < kWarps) s_w[threadIdx.x] = wi - w;
+    if (threadIdx.x == 31) s_w[32] = wi;
+  }
+  __syncthreads();
+  const unsigned long long r = s_w[threadIdx.x >> 5] + incl - x;
+  *total = s_w[32];
+  __syncthreads();
+  return r;
+}
+
+// Apply chunk: kApplyWords bitmask words per block iteration.  The set
+// bits are first compacted into a shared-memory vertex list (block scan
+// of popcounts), then every thread consumes up to kApplyItems recipients
+// with independent loads -- no per-word serial chains.
+#ifndef PGX_APPLY_WORDS
+#define PGX_APPLY_WORDS 64
+#endif
+constexpr int kApplyWords = PGX_APPLY_WORDS;
+constexpr int kApplyItems = kApplyWords * 32 / kBlock;  // 4
+
+// Returns (recipients counted) << 32 | (broadcasts) for this thread.  With
+// `count_only` the bitmask is only counted (superstep cap reached: the
+// pending messages must stay unconsumed, engine.py:299-300).
+template <int APP>
+__device__ unsigned long long apply_min_phase(const int32_t *__restrict__ row_ptr, uint32_t *val,
+                                              uint32_t *mailbox, int32_t n, const RunWs &ws,
+                                              StepCounters *ctr, char *smem, bool count_only) {
+  __shared__ unsigned long long s_w[33];
+  __shared__ unsigned long long s_gbase;
+  int32_t *s_list = reinterpret_cast<int32_t *>(smem);  // kApplyWords * 32 ids
+  uint32_t *f_msg = reinterpret_cast<uint32_t *>(ws.f_msg);
+  const int words = (n + 31) >> 5;
+  unsigned bcast = 0, recips = 0;
+  if (count_only) {
+    for (int wi = blockIdx.x * kBlock + threadIdx.x; wi < words; wi += gridDim.x * kBlock)
+      recips += __popc(ws.has[wi]);
+    return ((unsigned long long)recips << 32);
+  }
+  for (int base = blockIdx.x * kApplyWords; base < words; base += gridDim.x * kApplyWords) {
+    // ---- expand the chunk's set bits into s_list (vertex order) ----
+    uint32_t word = 0;
+    const int wi = base + threadIdx.x;
+    if (threadIdx.x < kApplyWords && wi < words) {
+      word = ws.has[wi];
+      if (word) ws.has[wi] = 0u;
+    }
+    if (!__syncthreads_or(word != 0)) continue;  // empty chunk: one barrier
+    recips += __popc(word);
+    unsigned long long tot64;
+    const int off = (int)block_excl_scan_u64((unsigned long long)__popc(word), s_w, &tot64);
+    const int T = (int)tot64;
+    if (T == 0) continue;  // block-uniform
+    {
+      int o = off;
+      uint32_t rem = word;
+      while (rem) {
+        const int b = __ffs(rem) - 1;
+        rem &= rem - 1;
+        s_list[o++] = (wi << 5) + b;
+      }
+    }
+    __syncthreads();
+    // ---- consume + compute, kApplyItems independent recipients / thread ----
+    int v[kApplyItems];
+    uint32_t m[kApplyItems], cv[kApplyItems];
+    int deg[kApplyItems], rs[kApplyItems];
+#pragma unroll
+    for (int j = 0; j < kApplyItems; j++) {
+      const int idx = j * kBlock + threadIdx.x;
+      v[j] = (idx < T) ? s_list[idx] : -1;
+    }
+#pragma unroll
+    for (int j = 0; j < kApplyItems; j++) {
+      if (v[j] >= 0) {
+        m[j] = mailbox[v[j]];
+        cv[j] = val[v[j]];
+      }
+    }
+    unsigned long long mine = 0;
+#pragma unroll
+    for (int j = 0; j < kApplyItems; j++) {
+      deg[j] = 0;
+      if (v[j] >= 0) {
+        mailbox[v[j]] = kNeutralMin;  // consume (mailbox.py:112-117)
+        if (m[j] < cv[j]) {
+          val[v[j]] = m[j];
+          bcast++;
+          rs[j] = row_ptr[v[j]];
+          deg[j] = -1;  // improved; degree resolved below
+        }
+      }
+    }
+#pragma unroll
+    for (int j = 0; j < kApplyItems; j++) {
+      if (deg[j] == -1) {
+        deg[j] = row_ptr[v[j] + 1] - rs[j];
+        if (deg[j] > 0) mine += (1ull << 32) | (unsigned long long)deg[j];
+      }
+    }
+    unsigned long long total;
+    unsigned long long run = block_excl_scan_u64(mine, s_w, &total);
+    if (total != 0) {  // block-uniform
+      if (threadIdx.x == 0) s_gbase = atomicAdd(&ctr->packed, total);
+      __syncthreads();
+      run += s_gbase;
+#pragma unroll
+      for (int j = 0; j < kApplyItems; j++) {
+        if (deg[j] > 0) {
+          const unsigned pos = (unsigned)(run >> 32);
+          const int eb = (int)(run & 0xFFFFFFFFull);
+          ws.f_eb[pos] = eb;
+          ws.f_rs[pos] = rs[j];
+          f_msg[pos] = (APP == PGX_APP_SSSP) ? m[j] + 1u : m[j];
+          for (int64_t t = ((int64_t)eb + kTile - 1) / kTile; t * kTile < (int64_t)eb + deg[j]; t++)
+            ws.tile_src[t] = (int)pos;
+          run += (1ull << 32) | (unsigned long long)deg[j];
+        }
+      }
+    }
+    __syncthreads();  // s_list / s_gbase reuse
+  }
+  return ((unsigned long long)recips << 32) | bcast;
+}
+
+__device__ __forceinline__ void record_step(int64_t *stats, int s, int64_t active,
+                                            int64_t sent, int64_t edges, int64_t senders,
+                                            int64_t recips, int64_t bcast) {
+  int64_t *st = stats + PGX_STAT_HDR + (int64_t)s * PGX_STAT_FIELDS;
+  st[0] = active;
+  st[1] = sent;
+  st[2] = edges;
+  st[3] = senders;
+  st[4] = recips;
+  st[5] = (int64_t)globaltimer();
+  st[6] = bcast;
+}
+
+
+}  // namespace pgx

@@ -1,0 +1,573 @@
+// pgx_run.cu -- whole runs on one GPU: the persistent superstep kernels.
+//
+// One persistent cooperative kernel runs a whole Pregel run: every
+// superstep's scatter (send + combine into the recipient mailbox), apply
+// (consume + compute + vote-to-halt) and the halt test stay on the device,
+// separated by a grid barrier.  Reference semantics:
+//   engine.py:255-316   _Executor.run (BSP loop, stats, quiescence, cap)
+//   engine.py:402-414   _chunk_push (consume, compute)
+//   engine.py:154-162   send_to_out_neighbors (per-edge send)
+//   mailbox.py:180-199  send_hybrid: publish-once + lock-free combine
+//   mailbox.py:147-165  apply_cas: skip the atomic when combine is a no-op
+//   algorithms.py       pagerank 27-84, connected_components 87-113,
+//                       sssp 116-152
+//   scheduler.py:91-116 edge_balanced_partition (edge-space split)
+//
+// Mapping of the paper's three optimisations onto sm_100a:
+//   hybrid combiner  -> read-filter (plain load, skip when min(old,msg)==old)
+//                       + one fire-and-forget red.min.u32 / red.add.f64;
+//                       publication is an idempotent has-message bit set by
+//                       every lane whose filter read saw the neutral
+//                       (pgx_scatter.cuh).
+//   externalisation  -> SoA: value[], mailbox[], has-bitmask, frontier SoA.
+//   edge-centric     -> the frontier is built with its exclusive edge
+//                       prefix (one 64-bit packed atomic per block chunk,
+//                       pgx_apply.cuh); the scatter walks fixed 256-edge warp
+//                       tiles of that edge space -- exact edge balance, hub
+//                       rows split across tiles.
+// PageRank's default lowering is the reference's pull fold (pgx_gather.cuh).
+#include "pgx_apply.cuh"
+#include "pgx_common.cuh"
+#include "pgx_gather.cuh"
+#include "pgx_scatter.cuh"
+
+namespace pgx {
+namespace {
+
+// ------------------------------------------------------------------
+// persistent run kernels
+// ------------------------------------------------------------------
+
+struct MinRunParams {
+  int32_t n;
+  int64_t m;
+  const int32_t *row_ptr;
+  const int32_t *col;
+  GraphWs g;
+  RunWs ws;
+  uint32_t *val;
+  int32_t source;  // SSSP only
+  int32_t max_steps;
+  int32_t read_filter;
+  const int32_t *hub_ids;
+  int32_t nhubs;
+  int64_t *stats;
+};
+
+template <int APP>
+__global__ void __launch_bounds__(kBlock, PGX_MIN_BLOCKS) min_run_kernel(MinRunParams p) {
+  extern __shared__ __align__(16) char smem[];
+  __shared__ unsigned s_red[32];
+  unsigned gen = 0;
+  if (threadIdx.x == 0) gen = ld_acquire(&p.ws.bar->gen);
+  uint32_t *mailbox = reinterpret_cast<uint32_t *>(p.ws.mailbox);
+  const unsigned nthreads = gridDim.x * blockDim.x;
+  const unsigned gtid = blockIdx.x * blockDim.x + threadIdx.x;
+
+  // ---- setup (algorithms.py:96-97 / 129-134) + superstep-0 senders ----
+  for (unsigned v = gtid; v < (unsigned)p.n; v += nthreads) {
+    p.val[v] = (APP == PGX_APP_CC) ? v : kNeutralMin;
+    mailbox[v] = kNeutralMin;
+  }
+  for (unsigned wi = gtid; wi < (unsigned)(p.n / 32 + 2); wi += nthreads) p.ws.has[wi] = 0u;
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    p.stats[0] = p.stats[1] = 0;
+    p.stats[2] = gridDim.x;
+    p.stats[3] = (int64_t)globaltimer();
+    StepCounters z = {};
+    p.ws.ctr[0] = z;
+    p.ws.ctr[1] = z;
+    if (APP == PGX_APP_SSSP) {
+      const int rs = p.row_ptr[p.source];
+      const int deg = p.row_ptr[p.source + 1] - rs;
+      if (deg > 0) {
+        p.ws.f_eb[0] = 0;
+        p.ws.f_rs[0] = rs;
+        reinterpret_cast<uint32_t *>(p.ws.f_msg)[0] = 1u;
+        for (int64_t t = 0; t * kTile < deg; t++) p.ws.tile_src[t] = 0;
+        p.ws.ctr[0].packed = (1ull << 32) | (unsigned long long)deg;
+      }
+      p.ws.ctr[0].bcast = 1u;  // the source computes and sends in superstep 0
+    } else {
+      p.ws.ctr[0].bcast = (unsigned)p.n;  // every vertex broadcasts its id
+    }
+  }
+  grid_sync(p.ws.bar, gen);
+  if (APP == PGX_APP_SSSP && gtid == 0) p.val[p.source] = 0u;
+  if (gtid == 0) p.stats[PGX_STAT_HDR + 7] = (int64_t)globaltimer();
+
+  for (int s = 0;; s++) {
+    // ---- scatter(s): senders push along out-edges into the mailbox ----
+    ScatterArgs a;
+    a.col = p.col;
+    a.mailbox = mailbox;
+    a.has = p.ws.has;
+    a.id_offset = 0;
+    a.hub_ids = p.hub_ids;
+    a.nhubs = p.nhubs;
+    if (APP == PGX_APP_CC && s == 0) {
+      a.eb = p.g.nz_eb;
+      a.rs = nullptr;
+      a.ids = p.g.nz_id;
+      a.msg = nullptr;
+      a.tile_src = p.g.tile_src;
+      a.nsrc = p.g.hdr[0];
+      a.E = p.m;
+      scatter_phase<PGX_OP_MIN_U32, MsgSrc::kSourceId>(a, smem, p.read_filter);
+    } else {
+      const unsigned long long packed = p.ws.ctr[s].packed;
+      a.eb = p.ws.f_eb;
+      a.rs = p.ws.f_rs;
+      a.ids = nullptr;
+      a.msg = p.ws.f_msg;
+      a.tile_src = p.ws.tile_src;
+      a.nsrc = (int32_t)(packed >> 32);
+      a.E = (int64_t)(packed & 0xFFFFFFFFull);
+      scatter_phase<PGX_OP_MIN_U32, MsgSrc::kFrontier>(a, smem, p.read_filter);
+    }
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+      StepCounters z = {};
+      p.ws.ctr[s + 1] = z;
+    }
+    grid_sync(p.ws.bar, gen);
+    const uint64_t t_scatter = globaltimer();
+
+    // ---- apply(s+1): consume + compute + frontier build; at the cap the
+    //      pending messages are only counted (engine.py:299-300) ----
+    const bool at_cap = (s + 1 == p.max_steps);
+    const unsigned long long rb =
+        apply_min_phase<APP>(p.row_ptr, p.val, mailbox, p.n, p.ws, &p.ws.ctr[s + 1], smem, at_cap);
+    const unsigned bc = block_sum<unsigned>((unsigned)(rb & 0xFFFFFFFFull), s_red);
+    const unsigned rc = block_sum<unsigned>((unsigned)(rb >> 32), s_red);
+    if (threadIdx.x == 0) {
+      if (bc) atomicAdd(&p.ws.ctr[s + 1].bcast, bc);
+      if (rc) atomicAdd(&p.ws.ctr[s].recip, rc);
+    }
+    grid_sync(p.ws.bar, gen);
+
+    // ---- stats + halt test (engine.py:284-300) ----
+    const unsigned nrecip = p.ws.ctr[s].recip;
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+      const StepCounters c = p.ws.ctr[s];
+      const int64_t senders = (int64_t)(c.packed >> 32);
+      const int64_t edges = (APP == PGX_APP_CC && s == 0) ? p.m : (int64_t)(c.packed & 0xFFFFFFFFull);
+      const int64_t active = (s == 0) ? p.n : (int64_t)p.ws.ctr[s - 1].recip;
+      const int64_t sent = (APP == PGX_APP_SSSP) ? edges : (int64_t)c.bcast;
+      record_step(p.stats, s, active, sent, edges,
+                  (APP == PGX_APP_CC && s == 0) ? (int64_t)p.g.hdr[0] : senders, nrecip,
+                  (int64_t)c.bcast);
+      p.stats[PGX_STAT_HDR + (int64_t)s * PGX_STAT_FIELDS + 5] = (int64_t)t_scatter;
+      // scatter(s+1) starts after this barrier: field 7 of step s+1
+      if (!at_cap)
+        p.stats[PGX_STAT_HDR + (int64_t)(s + 1) * PGX_STAT_FIELDS + 7] = (int64_t)globaltimer();
+      if (nrecip == 0) {
+        p.stats[0] = s + 1;
+      } else if (at_cap) {
+        p.stats[0] = s + 1;
+        p.stats[1] = 1;
+      }
+    }
+    if (nrecip == 0 || at_cap) break;
+  }
+}
+
+struct PrRunParams {
+  int32_t n;
+  int64_t m;
+  const int32_t *row_ptr;
+  const int32_t *col;
+  GraphWs g;
+  RunWs ws;
+  double *rank;
+  int32_t iterations;
+  double damping, base, r0;
+  int32_t max_steps;
+  int64_t *stats;
+};
+
+__global__ void __launch_bounds__(kBlock, PGX_MIN_BLOCKS) pagerank_run_kernel(PrRunParams p) {
+  extern __shared__ __align__(16) char smem[];
+  __shared__ double s_red[32];
+  __shared__ unsigned long long s_ured[32];
+  __shared__ double s_dangling;
+  unsigned gen = 0;
+  if (threadIdx.x == 0) gen = ld_acquire(&p.ws.bar->gen);
+  double *mailbox = reinterpret_cast<double *>(p.ws.mailbox);
+  double *share = reinterpret_cast<double *>(p.ws.f_msg);
+  const unsigned nthreads = gridDim.x * blockDim.x;
+  const unsigned gtid = blockIdx.x * blockDim.x + threadIdx.x;
+  const int last = p.iterations - 1;
+  const double dn_n = (double)p.n;
+
+  // ---- setup (algorithms.py:44-59): rank = r0, seed shares r0/outdeg ----
+  unsigned long long my_dangling = 0;
+  for (unsigned v = gtid; v < (unsigned)p.n; v += nthreads) {
+    const int deg = p.row_ptr[v + 1] - p.row_ptr[v];
+    p.rank[v] = p.r0;
+    mailbox[v] = 0.0;
+    share[v] = deg ? __ddiv_rn(p.r0, (double)deg) : 0.0;
+    my_dangling += deg ? 0ull : 1ull;
+  }
+  unsigned long long bd = block_sum<unsigned long long>(my_dangling, s_ured);
+  if (threadIdx.x == 0) {
+    if (bd) atomicAdd(&p.ws.misc[0], bd);
+    if (blockIdx.x == 0) {
+      p.stats[0] = p.stats[1] = 0;
+      p.stats[2] = gridDim.x;
+      p.stats[3] = (int64_t)globaltimer();
+    }
+  }
+  grid_sync(p.ws.bar, gen);
+
+  ScatterArgs a;
+  a.col = p.col;
+  a.eb = p.g.nz_eb;
+  a.rs = nullptr;
+  a.ids = p.g.nz_id;
+  a.msg = share;
+  a.tile_src = p.g.tile_src;
+  a.nsrc = p.g.hdr[0];
+  a.E = p.m;
+  a.mailbox = mailbox;
+  a.has = nullptr;
+  a.id_offset = 0;
+  a.hub_ids = nullptr;
+  a.nhubs = 0;
+  const unsigned long long ndangling = p.ws.misc[0];
+  double dangling = __dmul_rn(p.r0, (double)ndangling);  // algorithms.py:55
+  const int64_t nspread = (int64_t)p.n - (int64_t)ndangling;
+
+  // the setup seed is folded in superstep 0 (algorithms.py:56-59)
+  scatter_phase<PGX_OP_SUM_F64, MsgSrc::kShareById>(a, smem);
+  grid_sync(p.ws.bar, gen);
+
+  for (int s = 0;; s++) {
+    // ---- apply(s): rank = base + d * (folded + dangling / n) ----
+    const double dn = __ddiv_rn(dangling, dn_n);
+    double my_d = 0.0;
+    for (unsigned v = gtid; v < (unsigned)p.n; v += nthreads) {
+      const double folded = mailbox[v];
+      mailbox[v] = 0.0;
+      const double r = __dadd_rn(p.base, __dmul_rn(p.damping, __dadd_rn(folded, dn)));
+      p.rank[v] = r;
+      const int deg = p.row_ptr[v + 1] - p.row_ptr[v];
+      if (deg == 0) my_d = __dadd_rn(my_d, r);
+      else if (s != last) share[v] = __ddiv_rn(r, (double)deg);
+    }
+    const double bsum = block_sum<double>(my_d, s_red);
+    if (threadIdx.x == 0) p.ws.partials[blockIdx.x] = bsum;
+    grid_sync(p.ws.bar, gen);
+
+    // ---- on_superstep_end (algorithms.py:75-78): dangling mass ----
+    {
+      double acc = 0.0;
+      for (int b = threadIdx.x; b < (int)gridDim.x; b += kBlock) acc = __dadd_rn(acc, p.ws.partials[b]);
+      const double tot = block_sum<double>(acc, s_red);
+      if (threadIdx.x == 0) s_dangling = tot;
+      __syncthreads();
+      dangling = s_dangling;
+    }
+    const bool cap = (s + 1 == p.max_steps);
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+      p.stats[PGX_STAT_HDR + (int64_t)s * PGX_STAT_FIELDS + 7] = (int64_t)globaltimer();
+      record_step(p.stats, s, p.n, (s == last) ? 0 : nspread, p.m, nspread, p.n,
+                  (s == last) ? 0 : nspread);
+      if (s == last || cap) {
+        p.stats[0] = s + 1;
+        p.stats[1] = (s == last) ? 0 : 1;
+      }
+    }
+    if (s == last || cap) break;
+    scatter_phase<PGX_OP_SUM_F64, MsgSrc::kShareById>(a, smem);
+    grid_sync(p.ws.bar, gen);
+  }
+}
+
+struct PrPullParams {
+  int32_t n;
+  int64_t m;
+  const int32_t *row_ptr;     // out-CSR offsets (out-degrees)
+  const int32_t *in_row_ptr;  // in-CSR offsets
+  const int32_t *in_col;
+  GraphWs gin;                // tile map / nz list of the in-CSR
+  RunWs ws;
+  double *rank;
+  int32_t iterations;
+  double damping, base, r0;
+  int32_t max_steps;
+  int64_t *stats;
+};
+
+__global__ void __launch_bounds__(kBlock, PGX_MIN_BLOCKS) pagerank_pull_kernel(PrPullParams p) {
+  extern __shared__ __align__(16) char smem[];
+  __shared__ double s_red[32];
+  __shared__ unsigned long long s_ured[32];
+  __shared__ double s_dangling;
+  unsigned gen = 0;
+  double *folded = reinterpret_cast<double *>(p.ws.mailbox);
+  double *share_cur = reinterpret_cast<double *>(p.ws.f_msg);
+  double *share_nxt = p.ws.share2;
+  const unsigned nthreads = gridDim.x * blockDim.x;
+  const unsigned gtid = blockIdx.x * blockDim.x + threadIdx.x;
+  const int last = p.iterations - 1;
+  const double dn_n = (double)p.n;
+
+  // ---- setup (algorithms.py:44-59): rank = r0, seed shares r0/outdeg ----
+  unsigned long long my_dangling = 0;
+  for (unsigned v = gtid; v < (unsigned)p.n; v += nthreads) {
+    const int deg = p.row_ptr[v + 1] - p.row_ptr[v];
+    p.rank[v] = p.r0;
+    share_cur[v] = deg ? __ddiv_rn(p.r0, (double)deg) : 0.0;
+    my_dangling += deg ? 0ull : 1ull;
+  }
+  unsigned long long bd = block_sum<unsigned long long>(my_dangling, s_ured);
+  if (threadIdx.x == 0) {
+    if (bd) atomicAdd(&p.ws.misc[0], bd);
+    if (blockIdx.x == 0) {
+      p.stats[0] = p.stats[1] = 0;
+      p.stats[2] = gridDim.x;
+      p.stats[3] = (int64_t)globaltimer();
+    }
+  }
+  grid_sync(p.ws.bar, gen);
+  const unsigned long long ndangling = p.ws.misc[0];
+  double dangling = __dmul_rn(p.r0, (double)ndangling);  // algorithms.py:55
+  const int64_t nspread = (int64_t)p.n - (int64_t)ndangling;
+
+  GatherArgs g;
+  g.in_col = p.in_col;
+  g.eb = p.gin.nz_eb;
+  g.ids = p.gin.nz_id;
+  g.tile_src = p.gin.tile_src;
+  g.nsrc = p.gin.hdr[0];
+  g.E = p.m;
+  g.folded = folded;
+  g.head = p.ws.head;
+  g.tail = p.ws.tail;
+
+  for (int s = 0;; s++) {
+    if (blockIdx.x == 0 && threadIdx.x == 0)
+      p.stats[PGX_STAT_HDR + (int64_t)s * PGX_STAT_FIELDS + 7] = (int64_t)globaltimer();
+    // ---- fold (engine.py:425-457): in-neighbour shares of last superstep
+    g.share = share_cur;
+    gather_phase(g, smem);
+    grid_sync(p.ws.bar, gen);
+    const uint64_t t_fold = globaltimer();
+
+    // ---- compute (algorithms.py:61-73): rank, next share, dangling mass
+    const double dn = __ddiv_rn(dangling, dn_n);
+    double my_d = 0.0;
+    for (unsigned v = gtid; v < (unsigned)p.n; v += nthreads) {
+      const int es = p.in_row_ptr[v], ee = p.in_row_ptr[v + 1];
+      double f = 0.0;
+      if (ee > es) {
+        const int64_t t0 = es / kTile, t1 = (ee - 1) / kTile;
+        if (t0 == t1) {
+          f = folded[v];
+        } else {
+          f = p.ws.tail[t0];
+          for (int64_t t = t0 + 1; t <= t1; t++) f = __dadd_rn(f, p.ws.head[t]);
+        }
+      }
+      const double r = __dadd_rn(p.base, __dmul_rn(p.damping, __dadd_rn(f, dn)));
+      p.rank[v] = r;
+      const int deg = p.row_ptr[v + 1] - p.row_ptr[v];
+      if (deg == 0) my_d = __dadd_rn(my_d, r);
+      else if (s != last) share_nxt[v] = __ddiv_rn(r, (double)deg);
+    }
+    const double bsum = block_sum<double>(my_d, s_red);
+    if (threadIdx.x == 0) p.ws.partials[blockIdx.x] = bsum;
+    grid_sync(p.ws.bar, gen);
+
+    // ---- on_superstep_end (algorithms.py:75-78): dangling mass ----
+    {
+      double acc = 0.0;
+      for (int b = threadIdx.x; b < (int)gridDim.x; b += kBlock) acc = __dadd_rn(acc, p.ws.partials[b]);
+      const double tot = block_sum<double>(acc, s_red);
+      if (threadIdx.x == 0) s_dangling = tot;
+      __syncthreads();
+      dangling = s_dangling;
+    }
+    const bool cap = (s + 1 == p.max_steps);
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+      record_step(p.stats, s, p.n, (s == last) ? 0 : nspread, p.m, nspread, p.n,
+                  (s == last) ? 0 : nspread);
+      p.stats[PGX_STAT_HDR + (int64_t)s * PGX_STAT_FIELDS + 5] = (int64_t)globaltimer();
+      (void)t_fold;
+      if (s == last || cap) {
+        p.stats[0] = s + 1;
+        p.stats[1] = (s == last) ? 0 : 1;
+      }
+    }
+    if (s == last || cap) break;
+    double *tmp = share_cur;
+    share_cur = share_nxt;
+    share_nxt = tmp;
+  }
+}
+
+
+inline size_t scatter_smem_bytes(int op) { return scatter_smem(op); }
+
+}  // namespace
+}  // namespace pgx
+
+using namespace pgx;
+
+extern "C" {
+
+int pgx_run_workspace_bytes(int app, int64_t n, int64_t m, int32_t max_supersteps,
+                            size_t *bytes) {
+  if (!bytes || n < 0 || m < 0 || max_supersteps < 1 || app < 0 || app > 3)
+    return fail(PGX_EINVAL, "bad run workspace arguments");
+  *bytes = run_ws_layout(app, n, m, max_supersteps, nullptr, nullptr);
+  return PGX_OK;
+}
+
+static int min_run(int app, int32_t n, int64_t m, const int32_t *row_ptr, const int32_t *col_idx,
+                   const void *graph_ws, const int32_t *hub_ids, int32_t nhubs,
+                   int32_t source, int32_t max_supersteps, uint32_t *val,
+                   void *run_ws, size_t run_ws_bytes, int64_t *stats, uintptr_t stream) {
+  if (nhubs < 0 || nhubs > kHubs || (nhubs > 0 && !hub_ids))
+    return fail(PGX_EINVAL, "hub count must be in [0, pgx_hub_capacity()]");
+  int rc = check_graph(n, m, row_ptr, col_idx, graph_ws);
+  if (rc) return rc;
+  if (max_supersteps < 1) return fail(PGX_EINVAL, "superstep cap must be >= 1");
+  if (!val || !run_ws || !stats) return fail(PGX_EINVAL, "null output pointer");
+  if (app == PGX_APP_SSSP && (source < 0 || source >= n))
+    return fail(PGX_EINVAL, "source vertex out of range");
+  MinRunParams p;
+  p.n = n;
+  p.m = m;
+  p.row_ptr = row_ptr;
+  p.col = col_idx;
+  graph_ws_layout(n, m, &p.g, (char *)graph_ws);
+  if (run_ws_layout(app, n, m, max_supersteps, &p.ws, (char *)run_ws) > run_ws_bytes)
+    return fail(PGX_ENOMEM, "run workspace too small");
+  p.val = val;
+  p.source = source;
+  p.max_steps = max_supersteps;
+  p.read_filter = g_opt[PGX_OPT_READ_FILTER];
+  p.hub_ids = hub_ids;
+  p.nhubs = nhubs;
+  p.stats = stats;
+  cudaStream_t st = (cudaStream_t)stream;
+  PGX_CUDA(cudaMemsetAsync(p.ws.bar, 0, 64, st));
+  const size_t smem = scatter_smem(PGX_OP_MIN_U32, nhubs);
+  int grid = 0;
+  void *args[] = {&p};
+  if (app == PGX_APP_SSSP) {
+    rc = coop_grid(min_run_kernel<PGX_APP_SSSP>, smem, &grid);
+    if (rc) return rc;
+    PGX_CUDA(cudaLaunchCooperativeKernel((void *)min_run_kernel<PGX_APP_SSSP>, grid, kBlock,
+                                         args, smem, st));
+  } else {
+    rc = coop_grid(min_run_kernel<PGX_APP_CC>, smem, &grid);
+    if (rc) return rc;
+    PGX_CUDA(cudaLaunchCooperativeKernel((void *)min_run_kernel<PGX_APP_CC>, grid, kBlock,
+                                         args, smem, st));
+  }
+  return PGX_OK;
+}
+
+int pgx_sssp_run(int32_t n, int64_t m, const int32_t *row_ptr, const int32_t *col_idx,
+                 const void *graph_ws, const int32_t *hub_ids, int32_t nhubs, int32_t source,
+                 int32_t max_supersteps, uint32_t *dist, void *run_ws, size_t run_ws_bytes,
+                 int64_t *stats, uintptr_t stream) {
+  return min_run(PGX_APP_SSSP, n, m, row_ptr, col_idx, graph_ws, hub_ids, nhubs, source,
+                 max_supersteps, dist, run_ws, run_ws_bytes, stats, stream);
+}
+
+int pgx_cc_run(int32_t n, int64_t m, const int32_t *row_ptr, const int32_t *col_idx,
+               const void *graph_ws, const int32_t *hub_ids, int32_t nhubs,
+               int32_t max_supersteps, uint32_t *labels, void *run_ws, size_t run_ws_bytes,
+               int64_t *stats, uintptr_t stream) {
+  return min_run(PGX_APP_CC, n, m, row_ptr, col_idx, graph_ws, hub_ids, nhubs, 0,
+                 max_supersteps, labels, run_ws, run_ws_bytes, stats, stream);
+}
+
+int pgx_hub_capacity(int32_t *capacity) {
+  if (!capacity) return fail(PGX_EINVAL, "null out pointer");
+  *capacity = kHubs;
+  return PGX_OK;
+}
+
+int pgx_pagerank_run(int32_t n, int64_t m, const int32_t *row_ptr, const int32_t *col_idx,
+                     const void *graph_ws, int32_t iterations, double damping, double base,
+                     double r0, int32_t max_supersteps, double *rank, void *run_ws,
+                     size_t run_ws_bytes, int64_t *stats, uintptr_t stream) {
+  int rc = check_graph(n, m, row_ptr, col_idx, graph_ws);
+  if (rc) return rc;
+  if (iterations < 1) return fail(PGX_EINVAL, "iterations must be >= 1");
+  if (!(damping >= 0.0 && damping <= 1.0)) return fail(PGX_EINVAL, "damping must be in [0, 1]");
+  if (max_supersteps < 1) return fail(PGX_EINVAL, "superstep cap must be >= 1");
+  if (!rank || !run_ws || !stats) return fail(PGX_EINVAL, "null output pointer");
+  PrRunParams p;
+  p.n = n;
+  p.m = m;
+  p.row_ptr = row_ptr;
+  p.col = col_idx;
+  graph_ws_layout(n, m, &p.g, (char *)graph_ws);
+  if (run_ws_layout(PGX_APP_PAGERANK, n, m, max_supersteps, &p.ws, (char *)run_ws) > run_ws_bytes)
+    return fail(PGX_ENOMEM, "run workspace too small");
+  p.rank = rank;
+  p.iterations = iterations;
+  p.damping = damping;
+  p.base = base;
+  p.r0 = r0;
+  p.max_steps = max_supersteps;
+  p.stats = stats;
+  cudaStream_t st = (cudaStream_t)stream;
+  PGX_CUDA(cudaMemsetAsync(p.ws.bar, 0, 64, st));
+  PGX_CUDA(cudaMemsetAsync(p.ws.misc, 0, 64, st));
+  const size_t smem = scatter_smem_bytes(PGX_OP_SUM_F64);
+  int grid = 0;
+  rc = coop_grid(pagerank_run_kernel, smem, &grid);
+  if (rc) return rc;
+  void *args[] = {&p};
+  PGX_CUDA(cudaLaunchCooperativeKernel((void *)pagerank_run_kernel, grid, kBlock, args, smem, st));
+  return PGX_OK;
+}
+
+int pgx_pagerank_pull_run(int32_t n, int64_t m, const int32_t *row_ptr,
+                          const int32_t *in_row_ptr, const int32_t *in_col,
+                          const void *in_graph_ws, int32_t iterations, double damping,
+                          double base, double r0, int32_t max_supersteps, double *rank,
+                          void *run_ws, size_t run_ws_bytes, int64_t *stats, uintptr_t stream) {
+  int rc = check_graph(n, m, in_row_ptr, in_col, in_graph_ws);
+  if (rc) return rc;
+  if (!row_ptr) return fail(PGX_EINVAL, "null out-CSR offsets");
+  if (iterations < 1) return fail(PGX_EINVAL, "iterations must be >= 1");
+  if (!(damping >= 0.0 && damping <= 1.0)) return fail(PGX_EINVAL, "damping must be in [0, 1]");
+  if (max_supersteps < 1) return fail(PGX_EINVAL, "superstep cap must be >= 1");
+  if (!rank || !run_ws || !stats) return fail(PGX_EINVAL, "null output pointer");
+  PrPullParams p;
+  p.n = n;
+  p.m = m;
+  p.row_ptr = row_ptr;
+  p.in_row_ptr = in_row_ptr;
+  p.in_col = in_col;
+  graph_ws_layout(n, m, &p.gin, (char *)in_graph_ws);
+  if (run_ws_layout(PGX_APP_PAGERANK_PULL, n, m, max_supersteps, &p.ws, (char *)run_ws) >
+      run_ws_bytes)
+    return fail(PGX_ENOMEM, "run workspace too small");
+  p.rank = rank;
+  p.iterations = iterations;
+  p.damping = damping;
+  p.base = base;
+  p.r0 = r0;
+  p.max_steps = max_supersteps;
+  p.stats = stats;
+  cudaStream_t st = (cudaStream_t)stream;
+  PGX_CUDA(cudaMemsetAsync(p.ws.bar, 0, 64, st));
+  PGX_CUDA(cudaMemsetAsync(p.ws.misc, 0, 64, st));
+  const size_t smem = (size_t)kWarps * kSlots * 8 + 16;
+  int grid = 0;
+  rc = coop_grid(pagerank_pull_kernel, smem, &grid);
+  if (rc) return rc;
+  void *args[] = {&p};
+  PGX_CUDA(cudaLaunchCooperativeKernel((void *)pagerank_pull_kernel, grid, kBlock, args, smem, st));
+  return PGX_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,168 @@
+// pgx_scatter.cuh -- K1, the superstep's scatter: every sender pushes its
+// message along its out-edges and the messages are combined into each
+// recipient's single mailbox slot.  Reference: send_to_out_neighbors
+// (engine.py:154-162), send_hybrid / apply_cas (mailbox.py:147-199),
+// edge_balanced_partition (scheduler.py:91-116).
+#pragma once
+
+#include "pgx_common.cuh"
+
+namespace pgx {
+
+// One superstep's scatter.  Every warp owns whole 256-edge tiles of the
+// senders' edge space (exact edge balance; a hub row spans many tiles) and
+// runs without block barriers:
+//   1. the tile map gives the source holding the tile's first edge; the
+//      <= 257 sources of the tile are staged in the warp's smem window;
+//   2. per round of 32 consecutive edges, lane j holds the start of
+//      candidate source cur+1+j; the OR-reduction (REDUX) of the boundary
+//      bits that fall in the window gives every lane its source with one
+//      popc (sources have >= 1 edge, so <= 32 boundaries per window);
+//   3. the 8 neighbour ids are streamed (L1::no_allocate, L2 evict_first),
+//      then combined (min: read-filter + red.min, first publisher sets the
+//      has-message bit; sum: red.add.f64).
+// Hybrid combiner for hub recipients (the paper's split by recipient
+// class): the top in-degree vertices are flagged in the encoded col_idx
+// and filtered against a per-CTA shared-memory copy of their mailbox;
+// only a CTA-local improvement goes to the global red.min.
+
+template <int OP, MsgSrc MS>
+__device__ void scatter_phase(const ScatterArgs &a, char *smem, bool read_filter = true) {
+  using Msg = typename std::conditional<OP == PGX_OP_SUM_F64, double, uint32_t>::type;
+  constexpr bool kDense = MS != MsgSrc::kFrontier;
+  const int lane = (int)lane_id();
+  const int warp = threadIdx.x >> 5;
+  int32_t *s_eb = reinterpret_cast<int32_t *>(smem) + warp * kSlots;
+  int32_t *s_rs = reinterpret_cast<int32_t *>(smem) + kWarps * kSlots + warp * kSlots;
+  Msg *s_msg = reinterpret_cast<Msg *>(reinterpret_cast<int32_t *>(smem) + 2 * kWarps * kSlots) +
+               warp * kSlots;
+  const uint64_t pol = evict_first_policy();
+  const int64_t ntiles = (a.E + kTile - 1) / kTile;
+  const unsigned upto = (lane == 31) ? 0xFFFFFFFFu : ((2u << lane) - 1u);
+  const int64_t gwarp = (int64_t)blockIdx.x * kWarps + warp;
+  const int64_t nwarps = (int64_t)gridDim.x * kWarps;
+  uint32_t *s_hub = reinterpret_cast<uint32_t *>(smem + scatter_windows_smem(OP));
+  if (OP == PGX_OP_MIN_U32 && a.nhubs > 0) {  // block-uniform
+    for (int i = threadIdx.x; i < a.nhubs; i += blockDim.x) s_hub[i] = kNeutralMin;
+    __syncthreads();
+  }
+
+  for (int64_t t = gwarp; t < ntiles; t += nwarps) {
+    const int64_t e0 = t * kTile;
+    const int64_t e1 = min(a.E, e0 + kTile);
+    const int i0 = a.tile_src[t];
+    const int i1 = (t + 1 < ntiles) ? a.tile_src[t + 1] : a.nsrc - 1;
+    const int k = i1 - i0 + 1;  // <= kTile + 1
+#if PGX_SCATTER_SMEM
+    __syncwarp();
+    for (int j = lane; j <= k; j += 32) {
+      const int i = i0 + j;
+      if (j < k) {
+        s_eb[j] = a.eb[i];
+        if (!kDense) s_rs[j] = a.rs[i];
+        if (MS == MsgSrc::kFrontier) {
+          s_msg[j] = reinterpret_cast<const Msg *>(a.msg)[i];
+        } else if (MS == MsgSrc::kSourceId) {
+          s_msg[j] = (Msg)(a.ids[i] + a.id_offset);
+        } else {
+          s_msg[j] = reinterpret_cast<const Msg *>(a.msg)[a.ids[i]];
+        }
+      } else {
+        s_eb[j] = (i < a.nsrc) ? a.eb[i] : (int32_t)a.E;  // sentinel
+      }
+    }
+    __syncwarp();
+#define PGX_EB(j) s_eb[j]
+#define PGX_RS(j) s_rs[j]
+#define PGX_MSG(j) s_msg[j]
+#else
+    // no staging: boundary candidates are 32 consecutive ints (one or two
+    // sectors per round) and per-source data are broadcast loads, both
+    // L1 hits after the first round -- all of shared memory stays L1
+    const int32_t *g_eb = a.eb + i0;
+    const int nrem = a.nsrc - i0;
+#define PGX_EB(j) ((j) < nrem ? __ldg(g_eb + (j)) : (int32_t)a.E)
+#define PGX_RS(j) __ldg(a.rs + i0 + (j))
+#define PGX_MSG(j)                                                              \
+  (MS == MsgSrc::kFrontier ? __ldg(reinterpret_cast<const Msg *>(a.msg) + i0 + (j)) \
+   : MS == MsgSrc::kSourceId ? (Msg)(__ldg(a.ids + i0 + (j)) + a.id_offset)       \
+   : __ldg(reinterpret_cast<const Msg *>(a.msg) + __ldg(a.ids + i0 + (j))))
+#endif
+
+    int cur = 0;  // eb[0] <= e0: tile_src names the source holding e0
+#pragma unroll 1
+    for (int pass = 0; pass < kItems / kPass; pass++) {
+      int w[kPass];
+      Msg mv[kPass];
+#pragma unroll
+      for (int r = 0; r < kPass; r++) {
+        const int64_t base = e0 + (pass * kPass + r) * 32;
+        const int64_t e = base + lane;
+        const int ci = cur + 1 + lane;
+        unsigned bit = 0;
+        if (ci <= k) {
+          const int64_t pp = (int64_t)PGX_EB(ci) - base;
+          if (pp >= 0 && pp < 32) bit = 1u << pp;
+        }
+        const unsigned bm = __reduce_or_sync(0xFFFFFFFFu, bit);
+        const int src = cur + __popc(bm & upto);
+        cur += __popc(bm);
+        w[r] = kInvalidEdge;
+        if (e < e1) {
+          const int64_t pos = kDense ? e : (int64_t)PGX_RS(src) + (e - PGX_EB(src));
+          w[r] = ld_stream(a.col + pos, pol);
+          mv[r] = PGX_MSG(src);
+        }
+      }
+      if (OP == PGX_OP_MIN_U32) {
+        // hybrid combiner, fire-and-forget: read-filter (the mailbox.py:159
+        // short-circuit), then one red.min.u32.  Publication (mailbox.py:
+        // 190-199) becomes an idempotent has-message bit set by every lane
+        // whose filter read saw NEUTRAL: the lane whose atomic lands first
+        // on an empty slot necessarily read NEUTRAL, so no recipient is
+        // lost, and nothing waits on an atomic's return value.
+        uint32_t *mb = reinterpret_cast<uint32_t *>(a.mailbox);
+        uint32_t old[kPass];
+#pragma unroll
+        for (int r = 0; r < kPass; r++) {
+          const int x = w[r];
+          old[r] = (x == kInvalidEdge) ? 0u
+                   : (x < 0) ? s_hub[x & 0x7FFFFFFF]  // hub: CTA-local filter
+                   : (read_filter ? mb[x] : kNeutralMin);
+        }
+#pragma unroll
+        for (int r = 0; r < kPass; r++) {
+          const int x = w[r];
+          const uint32_t msg = (uint32_t)mv[r];
+          if (x != kInvalidEdge && msg < old[r]) {
+            int v = x;
+            uint32_t prev = old[r];
+            if (x < 0) {  // hub: the CTA-local copy let it through; consult
+                          // the global slot (the shared filter) before the red
+              const int slot = x & 0x7FFFFFFF;
+              v = a.hub_ids[slot];
+              prev = mb[v];
+              s_hub[slot] = min(prev, msg);  // racy store: only weakens the filter
+              if (msg >= prev) v = -1;
+            }
+            if (v >= 0) {
+              red_min_u32(mb + v, msg);
+              if (a.has && prev == kNeutralMin) red_or_b32(a.has + (v >> 5), 1u << (v & 31));
+            }
+          }
+        }
+      } else {
+        double *mb = reinterpret_cast<double *>(a.mailbox);
+#pragma unroll
+        for (int r = 0; r < kPass; r++)
+          if (w[r] != kInvalidEdge) atomicAdd(mb + w[r], (double)mv[r]);
+      }
+    }
+#undef PGX_EB
+#undef PGX_RS
+#undef PGX_MSG
+  }
+}
+
+
+}  // namespace pgx

@@ -1,0 +1,246 @@
+// pgx_slice.cu -- the partitioned (multi-GPU) superstep, one phase per
+// launch: scatter into a full-width mailbox, apply on the owned slice.
+// The host (paper_2010_01542_b200/distributed.py) reduces the mailbox
+// slices onto their owners between the two (NCCL via torch.distributed).
+#include "pgx_apply.cuh"
+#include "pgx_common.cuh"
+#include "pgx_scatter.cuh"
+
+namespace pgx {
+namespace {
+
+// ------------------------------------------------------------------
+// phase kernels of the partitioned (multi-GPU) superstep, SURVEY 8(e).
+// Each rank owns the out-edges of a contiguous vertex range [lo, lo+len)
+// and a slice of the mailbox.  Per superstep: K1 scatters the rank's
+// senders into a FULL-WIDTH local mailbox (global destination ids); the
+// host reduces the mailbox slices onto their owners (NCCL min / sum);
+// K2 applies on the owned slice (has-message == mailbox != neutral after
+// the min reduction: messages are < n <= 2^31 and never the neutral).
+// Regular (non-cooperative) stream-ordered launches.
+// ------------------------------------------------------------------
+
+struct SliceCounters {       // device counters of one partitioned superstep
+  unsigned long long packed; // senders << 32 | edges of the next frontier
+  unsigned long long recip;  // recipients in the owned slice
+  unsigned long long bcast;  // vertices that computed a new value
+  double dangling;           // PageRank: rank mass of owned dangling vertices
+};
+
+#ifndef PGX_SCATTER_MIN_BLOCKS
+#define PGX_SCATTER_MIN_BLOCKS PGX_MIN_BLOCKS
+#endif
+
+template <int OP, MsgSrc MS>
+__global__ void __launch_bounds__(kBlock, PGX_SCATTER_MIN_BLOCKS) scatter_kernel(ScatterArgs a,
+                                                                          int read_filter) {
+  extern __shared__ __align__(16) char smem[];
+  scatter_phase<OP, MS>(a, smem, read_filter != 0);
+}
+
+template <int APP>
+__global__ void __launch_bounds__(kBlock) apply_slice_kernel(
+    int32_t len, const int32_t *__restrict__ row_ptr, uint32_t *val, uint32_t *mailbox,
+    int32_t *f_eb, int32_t *f_rs, uint32_t *f_msg, int32_t *tile_src, SliceCounters *ctr,
+    int32_t count_only, uint32_t neutral) {
+  __shared__ unsigned long long s_w[33];
+  __shared__ unsigned long long s_gbase;
+  __shared__ unsigned long long s_red[32];
+  constexpr int kI = 4;
+  const int base = blockIdx.x * kBlock * kI;
+  int deg[kI], rs[kI];
+  uint32_t m[kI];
+  unsigned long long mine = 0, recips = 0, bcast = 0;
+#pragma unroll
+  for (int j = 0; j < kI; j++) {
+    const int v = base + j * kBlock + threadIdx.x;
+    deg[j] = 0;
+    m[j] = (v < len) ? mailbox[v] : neutral;
+    if (m[j] != neutral) {
+      recips++;
+      if (!count_only) {
+        mailbox[v] = neutral;  // consume
+        if (m[j] < val[v]) {
+          val[v] = m[j];
+          bcast++;
+          rs[j] = row_ptr[v];
+          deg[j] = row_ptr[v + 1] - rs[j];
+          if (deg[j] > 0) mine += (1ull << 32) | (unsigned long long)deg[j];
+        }
+      }
+    }
+  }
+  unsigned long long total;
+  unsigned long long run = block_excl_scan_u64(mine, s_w, &total);
+  if (total) {
+    if (threadIdx.x == 0) s_gbase = atomicAdd(&ctr->packed, total);
+    __syncthreads();
+    run += s_gbase;
+#pragma unroll
+    for (int j = 0; j < kI; j++) {
+      if (deg[j] > 0) {
+        const unsigned pos = (unsigned)(run >> 32);
+        const int eb = (int)(run & 0xFFFFFFFFull);
+        f_eb[pos] = eb;
+        f_rs[pos] = rs[j];
+        f_msg[pos] = (APP == PGX_APP_SSSP) ? m[j] + 1u : m[j];
+        for (int64_t t = ((int64_t)eb + kTile - 1) / kTile; t * kTile < (int64_t)eb + deg[j]; t++)
+          tile_src[t] = (int)pos;
+        run += (1ull << 32) | (unsigned long long)deg[j];
+      }
+    }
+  }
+  recips = block_sum<unsigned long long>(recips, s_red);
+  if (threadIdx.x == 0 && recips) atomicAdd(&ctr->recip, recips);
+  bcast = block_sum<unsigned long long>(bcast, s_red);
+  if (threadIdx.x == 0 && bcast) atomicAdd(&ctr->bcast, bcast);
+}
+
+__global__ void __launch_bounds__(kBlock) pr_apply_slice_kernel(
+    int32_t len, const int32_t *__restrict__ row_ptr, double *rank, double *mailbox,
+    double *share, double base, double damping, double dn, int32_t last, double *partials) {
+  __shared__ double s_red[32];
+  const int v = blockIdx.x * kBlock + threadIdx.x;
+  double my_d = 0.0;
+  if (v < len) {
+    const double folded = mailbox[v];
+    mailbox[v] = 0.0;
+    const double r = __dadd_rn(base, __dmul_rn(damping, __dadd_rn(folded, dn)));
+    rank[v] = r;
+    const int deg = row_ptr[v + 1] - row_ptr[v];
+    if (deg == 0) my_d = r;
+    else if (!last) share[v] = __ddiv_rn(r, (double)deg);
+  }
+  const double b = block_sum<double>(my_d, s_red);
+  if (threadIdx.x == 0) partials[blockIdx.x] = b;
+}
+
+__global__ void slice_init_kernel(int app, int32_t len, int32_t lo, uint32_t *val,
+                                  const int32_t *row_ptr, double *rank, double *share,
+                                  double r0) {
+  for (int v = blockIdx.x * blockDim.x + threadIdx.x; v < len; v += gridDim.x * blockDim.x) {
+    if (app == PGX_APP_CC) val[v] = (uint32_t)(lo + v);
+    else if (app == PGX_APP_SSSP) val[v] = kNeutralMin;
+    else {
+      const int deg = row_ptr[v + 1] - row_ptr[v];
+      rank[v] = r0;
+      share[v] = deg ? __ddiv_rn(r0, (double)deg) : 0.0;
+    }
+  }
+}
+
+
+}  // namespace
+}  // namespace pgx
+
+using namespace pgx;
+
+extern "C" {
+
+int pgx_slice_init(int app, int32_t len, int32_t lo, void *val, const int32_t *row_ptr,
+                   double *share, double r0, uintptr_t stream) {
+  if (len < 0 || !val || (app == PGX_APP_PAGERANK && (!row_ptr || !share)))
+    return fail(PGX_EINVAL, "bad slice_init arguments");
+  if (!len) return PGX_OK;
+  const int grid = (int)std::min<int64_t>(ceil_div(len, 256), 148 * 16);
+  slice_init_kernel<<<grid, 256, 0, (cudaStream_t)stream>>>(
+      app, len, lo, (uint32_t *)val, row_ptr, (double *)val, share, r0);
+  PGX_CUDA(cudaGetLastError());
+  return PGX_OK;
+}
+
+int pgx_scatter(int op, int dense, const int32_t *col_idx, const int32_t *src_eb,
+                const int32_t *src_rs, const int32_t *src_ids, int32_t id_offset,
+                const void *src_msg, const int32_t *tile_src, int32_t nsrc, int64_t edges,
+                void *mailbox, uint32_t *has_bits, uintptr_t stream) {
+  if (op != PGX_OP_MIN_U32 && op != PGX_OP_SUM_F64) return fail(PGX_EINVAL, "unknown op");
+  if (edges < 0 || edges > INT32_MAX || nsrc < 0) return fail(PGX_EINVAL, "bad sizes");
+  if (edges == 0) return PGX_OK;
+  if (!col_idx || !src_eb || !tile_src || !mailbox || (!dense && (!src_rs || !src_msg)) ||
+      (dense && !src_ids) || (op == PGX_OP_SUM_F64 && !src_msg))
+    return fail(PGX_EINVAL, "null scatter pointer");
+  ScatterArgs a;
+  a.col = col_idx;
+  a.eb = src_eb;
+  a.rs = src_rs;
+  a.ids = src_ids;
+  a.msg = src_msg;
+  a.tile_src = tile_src;
+  a.nsrc = nsrc;
+  a.E = edges;
+  a.mailbox = mailbox;
+  a.has = has_bits;
+  a.id_offset = id_offset;
+  a.hub_ids = nullptr;
+  a.nhubs = 0;
+  const int64_t tiles = ceil_div(edges, kTile);
+  int sms = 148, dev = 0;
+  if (cudaGetDevice(&dev) == cudaSuccess)
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(ceil_div(tiles, kWarps),
+                                                               (int64_t)sms * PGX_SCATTER_MIN_BLOCKS));
+  cudaStream_t st = (cudaStream_t)stream;
+  const size_t smem = scatter_smem(op);
+  const int rf = g_opt[PGX_OPT_READ_FILTER];
+  if (op == PGX_OP_MIN_U32 && !dense) {
+    PGX_CUDA(cudaFuncSetAttribute(scatter_kernel<PGX_OP_MIN_U32, MsgSrc::kFrontier>,
+                                  cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    scatter_kernel<PGX_OP_MIN_U32, MsgSrc::kFrontier><<<grid, kBlock, smem, st>>>(a, rf);
+  } else if (op == PGX_OP_MIN_U32) {
+    PGX_CUDA(cudaFuncSetAttribute(scatter_kernel<PGX_OP_MIN_U32, MsgSrc::kSourceId>,
+                                  cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    scatter_kernel<PGX_OP_MIN_U32, MsgSrc::kSourceId><<<grid, kBlock, smem, st>>>(a, rf);
+  } else if (dense) {
+    PGX_CUDA(cudaFuncSetAttribute(scatter_kernel<PGX_OP_SUM_F64, MsgSrc::kShareById>,
+                                  cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    scatter_kernel<PGX_OP_SUM_F64, MsgSrc::kShareById><<<grid, kBlock, smem, st>>>(a, rf);
+  } else {
+    return fail(PGX_EINVAL, "sum scatter needs the dense sender list");
+  }
+  PGX_CUDA(cudaGetLastError());
+  return PGX_OK;
+}
+
+int pgx_slice_counters_bytes(size_t *bytes) {
+  if (!bytes) return fail(PGX_EINVAL, "null out pointer");
+  *bytes = sizeof(SliceCounters);
+  return PGX_OK;
+}
+
+int pgx_apply_slice(int app, int32_t len, const int32_t *row_ptr, uint32_t *val,
+                    uint32_t *mailbox_slice, int32_t *f_eb, int32_t *f_rs, uint32_t *f_msg,
+                    int32_t *tile_src, void *counters, int32_t count_only, uint32_t neutral,
+                    uintptr_t stream) {
+  if (app != PGX_APP_CC && app != PGX_APP_SSSP) return fail(PGX_EINVAL, "min apps only");
+  if (len < 0 || !counters) return fail(PGX_EINVAL, "bad apply_slice arguments");
+  if (!len) return PGX_OK;
+  const int grid = (int)ceil_div(len, kBlock * 4);
+  cudaStream_t st = (cudaStream_t)stream;
+  if (app == PGX_APP_CC)
+    apply_slice_kernel<PGX_APP_CC><<<grid, kBlock, 0, st>>>(len, row_ptr, val, mailbox_slice, f_eb,
+                                                           f_rs, f_msg, tile_src,
+                                                           (SliceCounters *)counters, count_only,
+                                                           neutral);
+  else
+    apply_slice_kernel<PGX_APP_SSSP><<<grid, kBlock, 0, st>>>(len, row_ptr, val, mailbox_slice,
+                                                             f_eb, f_rs, f_msg, tile_src,
+                                                             (SliceCounters *)counters,
+                                                             count_only, neutral);
+  PGX_CUDA(cudaGetLastError());
+  return PGX_OK;
+}
+
+int pgx_pr_apply_slice(int32_t len, const int32_t *row_ptr, double *rank, double *mailbox_slice,
+                       double *share, double base, double damping, double dangling_over_n,
+                       int32_t last, double *partials, uintptr_t stream) {
+  if (len < 0 || (len && (!row_ptr || !rank || !mailbox_slice || !share || !partials)))
+    return fail(PGX_EINVAL, "bad pr_apply_slice arguments");
+  if (!len) return PGX_OK;
+  const int grid = (int)ceil_div(len, kBlock);
+  pr_apply_slice_kernel<<<grid, kBlock, 0, (cudaStream_t)stream>>>(
+      len, row_ptr, rank, mailbox_slice, share, base, damping, dangling_over_n, last, partials);
+  PGX_CUDA(cudaGetLastError());
+  return PGX_OK;
+}
+
+}  // extern "C"
