@@ -76,7 +76,9 @@ const char *pgx_last_error(void);
 /* process-wide tuning knobs (A/B experiments; defaults are shipped) */
 #define PGX_OPT_READ_FILTER 0   /* 1: skip the atomic when min(old,msg)==old */
 #define PGX_OPT_CTAS_PER_SM 1   /* persistent CTAs per SM, 0 = occupancy max */
-#define PGX_OPT_COUNT 2
+#define PGX_OPT_CAS_LOOP 2      /* ablation: CAS retry loop per message (lock-style) */
+#define PGX_OPT_VERTEX_SCHED 3  /* ablation: one thread per sender (no edge balance) */
+#define PGX_OPT_COUNT 4
 int pgx_set_option(int key, int value);
 
 /* number of SMs of `device` (host out pointer; syncs) */

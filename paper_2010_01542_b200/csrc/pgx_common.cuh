@@ -273,6 +273,7 @@ struct ScatterArgs {
   int32_t id_offset;      // kSourceId: message = ids[i] + id_offset
   const int32_t *hub_ids; // hub slot -> vertex; col_idx entries of hubs are
   int32_t nhubs;          // (sign bit | slot).  nhubs == 0: no hub cache
+  int32_t cas_loop;       // ablation: CAS retry loop instead of red.min
 };
 
 // shared memory of the scatter: one source window per warp (+ the hub

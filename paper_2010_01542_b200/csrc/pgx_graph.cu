@@ -11,6 +11,8 @@ thread_local std::string g_last_error;
 int g_opt[PGX_OPT_COUNT] = {
     /* PGX_OPT_READ_FILTER */ 1,
     /* PGX_OPT_CTAS_PER_SM */ 0,   // 0 = occupancy maximum
+    /* PGX_OPT_CAS_LOOP */ 0,      // ablation: CAS retry per message
+    /* PGX_OPT_VERTEX_SCHED */ 0,  // ablation: one thread per sender
 };
 
 namespace {

@@ -49,6 +49,8 @@ struct MinRunParams {
   int32_t source;  // SSSP only
   int32_t max_steps;
   int32_t read_filter;
+  int32_t cas_loop;       // ablation arms (pgx_set_option)
+  int32_t vertex_sched;
   const int32_t *hub_ids;
   int32_t nhubs;
   int64_t *stats;
@@ -105,6 +107,7 @@ __global__ void __launch_bounds__(kBlock, PGX_MIN_BLOCKS) min_run_kernel(MinRunP
     a.id_offset = 0;
     a.hub_ids = p.hub_ids;
     a.nhubs = p.nhubs;
+    a.cas_loop = p.cas_loop;
     if (APP == PGX_APP_CC && s == 0) {
       a.eb = p.g.nz_eb;
       a.rs = nullptr;
@@ -113,7 +116,10 @@ __global__ void __launch_bounds__(kBlock, PGX_MIN_BLOCKS) min_run_kernel(MinRunP
       a.tile_src = p.g.tile_src;
       a.nsrc = p.g.hdr[0];
       a.E = p.m;
-      scatter_phase<PGX_OP_MIN_U32, MsgSrc::kSourceId>(a, smem, p.read_filter);
+      if (p.vertex_sched)
+        scatter_vertex_phase<MsgSrc::kSourceId>(a, p.read_filter);
+      else
+        scatter_phase<PGX_OP_MIN_U32, MsgSrc::kSourceId>(a, smem, p.read_filter);
     } else {
       const unsigned long long packed = p.ws.ctr[s].packed;
       a.eb = p.ws.f_eb;
@@ -123,7 +129,10 @@ __global__ void __launch_bounds__(kBlock, PGX_MIN_BLOCKS) min_run_kernel(MinRunP
       a.tile_src = p.ws.tile_src;
       a.nsrc = (int32_t)(packed >> 32);
       a.E = (int64_t)(packed & 0xFFFFFFFFull);
-      scatter_phase<PGX_OP_MIN_U32, MsgSrc::kFrontier>(a, smem, p.read_filter);
+      if (p.vertex_sched)
+        scatter_vertex_phase<MsgSrc::kFrontier>(a, p.read_filter);
+      else
+        scatter_phase<PGX_OP_MIN_U32, MsgSrc::kFrontier>(a, smem, p.read_filter);
     }
     if (blockIdx.x == 0 && threadIdx.x == 0) {
       StepCounters z = {};
@@ -233,6 +242,7 @@ __global__ void __launch_bounds__(kBlock, PGX_MIN_BLOCKS) pagerank_run_kernel(Pr
   a.id_offset = 0;
   a.hub_ids = nullptr;
   a.nhubs = 0;
+  a.cas_loop = 0;
   const unsigned long long ndangling = p.ws.misc[0];
   double dangling = __dmul_rn(p.r0, (double)ndangling);  // algorithms.py:55
   const int64_t nspread = (int64_t)p.n - (int64_t)ndangling;
@@ -448,6 +458,8 @@ static int min_run(int app, int32_t n, int64_t m, const int32_t *row_ptr, const 
   p.source = source;
   p.max_steps = max_supersteps;
   p.read_filter = g_opt[PGX_OPT_READ_FILTER];
+  p.cas_loop = g_opt[PGX_OPT_CAS_LOOP];
+  p.vertex_sched = g_opt[PGX_OPT_VERTEX_SCHED];
   p.hub_ids = hub_ids;
   p.nhubs = nhubs;
   p.stats = stats;

@@ -146,8 +146,18 @@ __device__ void scatter_phase(const ScatterArgs &a, char *smem, bool read_filter
               if (msg >= prev) v = -1;
             }
             if (v >= 0) {
-              red_min_u32(mb + v, msg);
-              if (a.has && prev == kNeutralMin) red_or_b32(a.has + (v >> 5), 1u << (v & 31));
+              if (a.cas_loop) {  // ablation: lock-style CAS retry per message
+                uint32_t cur = prev;
+                while (msg < cur) {
+                  const uint32_t got = atomicCAS(mb + v, cur, msg);
+                  if (got == cur) break;
+                  cur = got;
+                }
+                if (a.has && prev == kNeutralMin) atomicOr(a.has + (v >> 5), 1u << (v & 31));
+              } else {
+                red_min_u32(mb + v, msg);
+                if (a.has && prev == kNeutralMin) red_or_b32(a.has + (v >> 5), 1u << (v & 31));
+              }
             }
           }
         }
@@ -164,5 +174,40 @@ __device__ void scatter_phase(const ScatterArgs &a, char *smem, bool read_filter
   }
 }
 
+
+// Ablation arm of the scheduler (harness.py:273-292 grid): one thread per
+// sender walks its whole out-row (the reference's vertex-centric split,
+// scheduler.py:79-88).  No edge balance: a hub row serialises on one lane.
+template <MsgSrc MS>
+__device__ void scatter_vertex_phase(const ScatterArgs &a, bool read_filter) {
+  constexpr bool kDense = MS != MsgSrc::kFrontier;
+  uint32_t *mb = reinterpret_cast<uint32_t *>(a.mailbox);
+  const int nthreads = gridDim.x * blockDim.x;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < a.nsrc; i += nthreads) {
+    const int64_t eb = a.eb[i];
+    const int64_t ee = (i + 1 < a.nsrc) ? a.eb[i + 1] : a.E;
+    const int64_t rs = kDense ? eb : (int64_t)a.rs[i];
+    const uint32_t msg = (MS == MsgSrc::kFrontier)
+                             ? reinterpret_cast<const uint32_t *>(a.msg)[i]
+                             : (uint32_t)(a.ids[i] + a.id_offset);
+    for (int64_t e = eb; e < ee; e++) {
+      const int v = a.col[rs + (e - eb)];
+      const uint32_t prev = read_filter ? mb[v] : kNeutralMin;
+      if (msg < prev) {
+        if (a.cas_loop) {
+          uint32_t cur = prev;
+          while (msg < cur) {
+            const uint32_t got = atomicCAS(mb + v, cur, msg);
+            if (got == cur) break;
+            cur = got;
+          }
+        } else {
+          red_min_u32(mb + v, msg);
+        }
+        if (a.has && prev == kNeutralMin) red_or_b32(a.has + (v >> 5), 1u << (v & 31));
+      }
+    }
+  }
+}
 
 }  // namespace pgx

@@ -173,6 +173,7 @@ int pgx_scatter(int op, int dense, const int32_t *col_idx, const int32_t *src_eb
   a.id_offset = id_offset;
   a.hub_ids = nullptr;
   a.nhubs = 0;
+  a.cas_loop = 0;
   const int64_t tiles = ceil_div(edges, kTile);
   int sms = 148, dev = 0;
   if (cudaGetDevice(&dev) == cudaSuccess)
