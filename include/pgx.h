@@ -186,7 +186,22 @@ int pgx_scatter(int op, int dense, const int32_t *col_idx,
                 const int32_t *src_eb, const int32_t *src_rs,
                 const int32_t *src_ids, int32_t id_offset, const void *src_msg,
                 const int32_t *tile_src, int32_t nsrc, int64_t edges,
-                void *mailbox, uint32_t *has_bits, uintptr_t stream);
+                void *mailbox, uint32_t *has_bits, uint32_t neutral,
+                uintptr_t stream);
+
+/* Sparse exchange, min programs.  The touched slots of
+ * a full-width local mailbox are its set has-bits; pgx_touched counts those
+ * outside [lo, hi) into *count (device int64) and, when `pairs` is not
+ * NULL, compacts them in vertex order (hence grouped by owner) into
+ * (slot << 32 | value) pairs, resetting each compacted slot to `neutral`.
+ * scratch: pgx_touched_scratch_bytes(n).  pgx_scatter_pairs min-combines
+ * received pairs into a mailbox (global slot ids). */
+int pgx_touched_scratch_bytes(int32_t n, size_t *bytes);
+int pgx_touched(int32_t n, int32_t lo, int32_t hi, const uint32_t *has_bits,
+                uint32_t *mailbox, uint32_t neutral, uint64_t *pairs,
+                int64_t *count, void *scratch, uintptr_t stream);
+int pgx_scatter_pairs(const uint64_t *pairs, int64_t count, uint32_t *mailbox,
+                      uintptr_t stream);
 
 /* size of the device counter block used by pgx_apply_slice (host out) */
 int pgx_slice_counters_bytes(size_t *bytes);

@@ -35,7 +35,7 @@ EXPORTS = (
     "pgx_run_workspace_bytes", "pgx_hub_capacity", "pgx_sssp_run", "pgx_cc_run",
     "pgx_pagerank_run", "pgx_pagerank_pull_run", "pgx_rmat_keys", "pgx_microbench",
     "pgx_slice_init", "pgx_scatter", "pgx_slice_counters_bytes", "pgx_apply_slice",
-    "pgx_pr_apply_slice",
+    "pgx_pr_apply_slice", "pgx_touched_scratch_bytes", "pgx_touched", "pgx_scatter_pairs",
 )
 
 _lib = None
@@ -68,7 +68,10 @@ _SIGS = {
                                              _f64, _i32, _p, _p, _sz, _p, _up]),
     "pgx_slice_init": (ctypes.c_int, [ctypes.c_int, _i32, _i32, _p, _p, _p, _f64, _up]),
     "pgx_scatter": (ctypes.c_int, [ctypes.c_int, ctypes.c_int, _p, _p, _p, _p, _i32, _p, _p,
-                                   _i32, _i64, _p, _p, _up]),
+                                   _i32, _i64, _p, _p, ctypes.c_uint32, _up]),
+    "pgx_touched_scratch_bytes": (ctypes.c_int, [_i32, _p]),
+    "pgx_touched": (ctypes.c_int, [_i32, _i32, _i32, _p, _p, ctypes.c_uint32, _p, _p, _p, _up]),
+    "pgx_scatter_pairs": (ctypes.c_int, [_p, _i64, _p, _up]),
     "pgx_slice_counters_bytes": (ctypes.c_int, [_p]),
     "pgx_apply_slice": (ctypes.c_int, [ctypes.c_int, _i32, _p, _p, _p, _p, _p, _p, _p, _p,
                                        _i32, ctypes.c_uint32, _up]),

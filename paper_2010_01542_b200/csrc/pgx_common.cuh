@@ -274,6 +274,7 @@ struct ScatterArgs {
   const int32_t *hub_ids; // hub slot -> vertex; col_idx entries of hubs are
   int32_t nhubs;          // (sign bit | slot).  nhubs == 0: no hub cache
   int32_t cas_loop;       // ablation: CAS retry loop instead of red.min
+  uint32_t neutral;       // min neutral of the mailbox (has-bit publication)
 };
 
 // shared memory of the scatter: one source window per warp (+ the hub
@@ -287,6 +288,33 @@ __host__ __device__ constexpr size_t scatter_smem(int op, int nhubs = 0) {
   return scatter_windows_smem(op) + (op == PGX_OP_MIN_U32 ? sizeof(uint32_t) * nhubs : 0) + 16;
 }
 
+
+// block-wide exclusive scan of an int (any multiple-of-32 block size)
+__device__ __forceinline__ int block_excl_scan(int x, int *s_warp, int *total) {
+  int incl = x;
+  for (int o = 1; o < 32; o <<= 1) {
+    const int y = __shfl_up_sync(0xFFFFFFFFu, incl, o);
+    if ((int)lane_id() >= o) incl += y;
+  }
+  if (lane_id() == 31) s_warp[threadIdx.x >> 5] = incl;
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    const int nw = blockDim.x >> 5;
+    int w = (threadIdx.x < nw) ? s_warp[threadIdx.x] : 0;
+    int wi = w;
+    for (int o = 1; o < 32; o <<= 1) {
+      const int y = __shfl_up_sync(0xFFFFFFFFu, wi, o);
+      if ((int)threadIdx.x >= o) wi += y;
+    }
+    if (threadIdx.x < nw) s_warp[threadIdx.x] = wi - w;
+    if (threadIdx.x == 31) s_warp[32] = wi;
+  }
+  __syncthreads();
+  const int r = s_warp[threadIdx.x >> 5] + incl - x;
+  *total = s_warp[32];
+  __syncthreads();
+  return r;
+}
 
 // launch helper for the persistent (cooperative) kernels: CTAs per SM from
 // the occupancy calculator, capped by PGX_OPT_CTAS_PER_SM and kMaxCtas

@@ -28,32 +28,6 @@ __global__ void offsets_to_i32_kernel(const int64_t *in, int32_t *out, int64_t c
     out[i] = (int32_t)in[i];
 }
 
-__device__ __forceinline__ int block_excl_scan(int x, int *s_warp, int *total) {
-  int incl = x;
-  for (int o = 1; o < 32; o <<= 1) {
-    const int y = __shfl_up_sync(0xFFFFFFFFu, incl, o);
-    if ((int)lane_id() >= o) incl += y;
-  }
-  if (lane_id() == 31) s_warp[threadIdx.x >> 5] = incl;
-  __syncthreads();
-  if (threadIdx.x < 32) {
-    const int nw = blockDim.x >> 5;
-    int w = (threadIdx.x < nw) ? s_warp[threadIdx.x] : 0;
-    int wi = w;
-    for (int o = 1; o < 32; o <<= 1) {
-      const int y = __shfl_up_sync(0xFFFFFFFFu, wi, o);
-      if ((int)threadIdx.x >= o) wi += y;
-    }
-    if (threadIdx.x < nw) s_warp[threadIdx.x] = wi - w;
-    if (threadIdx.x == 31) s_warp[32] = wi;
-  }
-  __syncthreads();
-  const int r = s_warp[threadIdx.x >> 5] + incl - x;
-  *total = s_warp[32];
-  __syncthreads();
-  return r;
-}
-
 __global__ void nz_count_kernel(const int32_t *row_ptr, int32_t n, int32_t *blk) {
   __shared__ int s_warp[33];
   const int64_t v = blockIdx.x * (int64_t)kCompactBlock + threadIdx.x;

@@ -108,6 +108,7 @@ __global__ void __launch_bounds__(kBlock, PGX_MIN_BLOCKS) min_run_kernel(MinRunP
     a.hub_ids = p.hub_ids;
     a.nhubs = p.nhubs;
     a.cas_loop = p.cas_loop;
+    a.neutral = kNeutralMin;
     if (APP == PGX_APP_CC && s == 0) {
       a.eb = p.g.nz_eb;
       a.rs = nullptr;
@@ -243,6 +244,7 @@ __global__ void __launch_bounds__(kBlock, PGX_MIN_BLOCKS) pagerank_run_kernel(Pr
   a.hub_ids = nullptr;
   a.nhubs = 0;
   a.cas_loop = 0;
+  a.neutral = 0u;
   const unsigned long long ndangling = p.ws.misc[0];
   double dangling = __dmul_rn(p.r0, (double)ndangling);  // algorithms.py:55
   const int64_t nspread = (int64_t)p.n - (int64_t)ndangling;

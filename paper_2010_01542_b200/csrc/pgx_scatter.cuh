@@ -128,7 +128,7 @@ __device__ void scatter_phase(const ScatterArgs &a, char *smem, bool read_filter
           const int x = w[r];
           old[r] = (x == kInvalidEdge) ? 0u
                    : (x < 0) ? s_hub[x & 0x7FFFFFFF]  // hub: CTA-local filter
-                   : (read_filter ? mb[x] : kNeutralMin);
+                   : (read_filter ? mb[x] : a.neutral);
         }
 #pragma unroll
         for (int r = 0; r < kPass; r++) {
@@ -153,10 +153,10 @@ __device__ void scatter_phase(const ScatterArgs &a, char *smem, bool read_filter
                   if (got == cur) break;
                   cur = got;
                 }
-                if (a.has && prev == kNeutralMin) atomicOr(a.has + (v >> 5), 1u << (v & 31));
+                if (a.has && prev == a.neutral) atomicOr(a.has + (v >> 5), 1u << (v & 31));
               } else {
                 red_min_u32(mb + v, msg);
-                if (a.has && prev == kNeutralMin) red_or_b32(a.has + (v >> 5), 1u << (v & 31));
+                if (a.has && prev == a.neutral) red_or_b32(a.has + (v >> 5), 1u << (v & 31));
               }
             }
           }
@@ -192,7 +192,7 @@ __device__ void scatter_vertex_phase(const ScatterArgs &a, bool read_filter) {
                              : (uint32_t)(a.ids[i] + a.id_offset);
     for (int64_t e = eb; e < ee; e++) {
       const int v = a.col[rs + (e - eb)];
-      const uint32_t prev = read_filter ? mb[v] : kNeutralMin;
+      const uint32_t prev = read_filter ? mb[v] : a.neutral;
       if (msg < prev) {
         if (a.cas_loop) {
           uint32_t cur = prev;
@@ -204,7 +204,7 @@ __device__ void scatter_vertex_phase(const ScatterArgs &a, bool read_filter) {
         } else {
           red_min_u32(mb + v, msg);
         }
-        if (a.has && prev == kNeutralMin) red_or_b32(a.has + (v >> 5), 1u << (v & 31));
+        if (a.has && prev == a.neutral) red_or_b32(a.has + (v >> 5), 1u << (v & 31));
       }
     }
   }

@@ -130,6 +130,83 @@ __global__ void slice_init_kernel(int app, int32_t len, int32_t lo, uint32_t *va
 }
 
 
+// ---- sparse exchange -------------------------------
+// The touched slots of the full-width local mailbox are its set has-bits.
+// Those outside the rank's own range [lo, hi) are counted, or compacted in
+// vertex order into (slot << 32 | value) pairs -- which groups them by
+// owner -- and reset to the neutral; the owner min-combines the pairs it
+// receives into its slice.
+
+__device__ __forceinline__ uint32_t foreign_bits(const uint32_t *has, int wi, int32_t n, int32_t lo,
+                                                 int32_t hi) {
+  uint32_t w = has[wi];
+  const int v0 = wi << 5;
+  if (v0 + 32 > n) w &= (n - v0 >= 32) ? 0xFFFFFFFFu : ((1u << (n - v0)) - 1u);
+  // drop bits in [lo, hi)
+  const int a = max(lo - v0, 0), b = min(hi - v0, 32);
+  if (a < b) {
+    const uint32_t hi_mask = (b >= 32) ? 0xFFFFFFFFu : ((1u << b) - 1u);
+    const uint32_t lo_mask = (1u << a) - 1u;
+    w &= ~(hi_mask & ~lo_mask);
+  }
+  return w;
+}
+
+__global__ void __launch_bounds__(kCompactBlock) touched_count_kernel(
+    const uint32_t *has, int32_t n, int32_t lo, int32_t hi, int32_t *blk) {
+  __shared__ int s_warp[33];
+  const int words = (n + 31) >> 5;
+  const int wi = blockIdx.x * kCompactBlock + threadIdx.x;
+  const int c = (wi < words) ? __popc(foreign_bits(has, wi, n, lo, hi)) : 0;
+  int total;
+  block_excl_scan(c, s_warp, &total);
+  if (threadIdx.x == 0) blk[blockIdx.x] = total;
+}
+
+__global__ void __launch_bounds__(kCompactBlock) touched_scan_kernel(int32_t *blk, int32_t nb,
+                                                                    int64_t *count) {
+  __shared__ int s_warp[33];
+  int carry = 0;
+  for (int base = 0; base < nb; base += kCompactBlock) {
+    const int i = base + threadIdx.x;
+    const int x = (i < nb) ? blk[i] : 0;
+    int total;
+    const int ex = block_excl_scan(x, s_warp, &total);
+    if (i < nb) blk[i] = carry + ex;
+    carry += total;
+  }
+  if (threadIdx.x == 0) *count = carry;
+}
+
+__global__ void __launch_bounds__(kCompactBlock) touched_write_kernel(
+    const uint32_t *has, int32_t n, int32_t lo, int32_t hi, const int32_t *blk, uint32_t *mailbox,
+    uint32_t neutral, unsigned long long *pairs) {
+  __shared__ int s_warp[33];
+  const int words = (n + 31) >> 5;
+  const int wi = blockIdx.x * kCompactBlock + threadIdx.x;
+  const uint32_t w = (wi < words) ? foreign_bits(has, wi, n, lo, hi) : 0u;
+  int total;
+  int pos = blk[blockIdx.x] + block_excl_scan(__popc(w), s_warp, &total);
+  uint32_t rem = w;
+  while (rem) {
+    const int b = __ffs(rem) - 1;
+    rem &= rem - 1;
+    const int v = (wi << 5) + b;
+    const uint32_t m = mailbox[v];
+    mailbox[v] = neutral;
+    pairs[pos++] = ((unsigned long long)(uint32_t)v << 32) | m;
+  }
+}
+
+__global__ void scatter_pairs_min_kernel(const unsigned long long *pairs, int64_t count,
+                                         uint32_t *mailbox) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < count;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const unsigned long long p = pairs[i];
+    red_min_u32(mailbox + (uint32_t)(p >> 32), (uint32_t)(p & 0xFFFFFFFFull));
+  }
+}
+
 }  // namespace
 }  // namespace pgx
 
@@ -152,7 +229,7 @@ int pgx_slice_init(int app, int32_t len, int32_t lo, void *val, const int32_t *r
 int pgx_scatter(int op, int dense, const int32_t *col_idx, const int32_t *src_eb,
                 const int32_t *src_rs, const int32_t *src_ids, int32_t id_offset,
                 const void *src_msg, const int32_t *tile_src, int32_t nsrc, int64_t edges,
-                void *mailbox, uint32_t *has_bits, uintptr_t stream) {
+                void *mailbox, uint32_t *has_bits, uint32_t neutral, uintptr_t stream) {
   if (op != PGX_OP_MIN_U32 && op != PGX_OP_SUM_F64) return fail(PGX_EINVAL, "unknown op");
   if (edges < 0 || edges > INT32_MAX || nsrc < 0) return fail(PGX_EINVAL, "bad sizes");
   if (edges == 0) return PGX_OK;
@@ -174,6 +251,7 @@ int pgx_scatter(int op, int dense, const int32_t *col_idx, const int32_t *src_eb
   a.hub_ids = nullptr;
   a.nhubs = 0;
   a.cas_loop = 0;
+  a.neutral = neutral;
   const int64_t tiles = ceil_div(edges, kTile);
   int sms = 148, dev = 0;
   if (cudaGetDevice(&dev) == cudaSuccess)
@@ -198,6 +276,41 @@ int pgx_scatter(int op, int dense, const int32_t *col_idx, const int32_t *src_eb
   } else {
     return fail(PGX_EINVAL, "sum scatter needs the dense sender list");
   }
+  PGX_CUDA(cudaGetLastError());
+  return PGX_OK;
+}
+
+int pgx_touched_scratch_bytes(int32_t n, size_t *bytes) {
+  if (!bytes || n < 0) return fail(PGX_EINVAL, "bad arguments");
+  *bytes = sizeof(int32_t) * (size_t)(ceil_div(ceil_div(n, 32), kCompactBlock) + 2);
+  return PGX_OK;
+}
+
+int pgx_touched(int32_t n, int32_t lo, int32_t hi, const uint32_t *has_bits, uint32_t *mailbox,
+                uint32_t neutral, uint64_t *pairs, int64_t *count, void *scratch,
+                uintptr_t stream) {
+  if (n < 1 || lo < 0 || hi < lo || hi > n || !has_bits || !count || !scratch ||
+      (pairs && !mailbox))
+    return fail(PGX_EINVAL, "bad pgx_touched arguments");
+  const int words = (int)ceil_div(n, 32);
+  const int nb = (int)ceil_div(words, kCompactBlock);
+  cudaStream_t st = (cudaStream_t)stream;
+  int32_t *blk = (int32_t *)scratch;
+  touched_count_kernel<<<nb, kCompactBlock, 0, st>>>(has_bits, n, lo, hi, blk);
+  touched_scan_kernel<<<1, kCompactBlock, 0, st>>>(blk, nb, count);
+  if (pairs)
+    touched_write_kernel<<<nb, kCompactBlock, 0, st>>>(has_bits, n, lo, hi, blk, mailbox, neutral,
+                                                       (unsigned long long *)pairs);
+  PGX_CUDA(cudaGetLastError());
+  return PGX_OK;
+}
+
+int pgx_scatter_pairs(const uint64_t *pairs, int64_t count, uint32_t *mailbox, uintptr_t stream) {
+  if (count < 0 || (count && (!pairs || !mailbox))) return fail(PGX_EINVAL, "bad pairs");
+  if (!count) return PGX_OK;
+  const int grid = (int)std::min<int64_t>(ceil_div(count, 256), 148 * 16);
+  scatter_pairs_min_kernel<<<grid, 256, 0, (cudaStream_t)stream>>>(
+      (const unsigned long long *)pairs, count, mailbox);
   PGX_CUDA(cudaGetLastError());
   return PGX_OK;
 }

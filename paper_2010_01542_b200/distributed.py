@@ -20,6 +20,14 @@ one GPU (CC labels / SSSP distances bit-exact, PageRank within 1e-9):
 * has-message after the reduction is ``mailbox != neutral``: CC / SSSP
   messages are < n <= 2^31 and never equal UINT32_MAX, and PageRank needs
   no flag (the paper's neutral-value caveat).
+* **sparse exchange** (SURVEY 8(f) row 3): late supersteps touch few
+  mailbox slots, yet the dense reduction always moves n slots.  Every rank
+  counts the slots it touched outside its own range (has-bits of the
+  scatter); when the largest count makes 8-byte (slot, value) pairs cheaper
+  than half the dense volume, the ranks compact their touched slots in
+  vertex order (grouped by owner) and exchange them with one variable-size
+  ``all_to_all_single``; owners min-combine what they receive.  The choice
+  is collective (an all-reduce of the counts) and recorded per superstep.
 
 The orchestration below is backend-agnostic: ``CudaBackend`` drives
 libpgx.so on the rank's GPU (NCCL process group); tests/ drive the same
@@ -82,6 +90,7 @@ class PartitionedRun:
         self.n, self.m = n, m
         self.lo = int(self.bounds[self.rank])
         self.hi = int(self.bounds[self.rank + 1])
+        self.sparse_ok = True  # allow the sparse exchange (A/B switch)
 
     # ---- collectives --------------------------------------------------
 
@@ -91,6 +100,25 @@ class PartitionedRun:
             lo, hi = int(self.bounds[r]), int(self.bounds[r + 1])
             if hi > lo:
                 self.dist.reduce(full[lo:hi], dst=r, op=op)
+
+    def _exchange_min(self, op) -> str:
+        """Dense per-owner reduction or sparse pair exchange (collective choice)."""
+        touched = self.b.touched_count()
+        t = torch.tensor([touched], dtype=torch.int64, device=self.b.device)
+        self.dist.all_reduce(t, op=self.dist.ReduceOp.MAX)
+        if self.sparse_ok and 8 * int(t.item()) * 2 < 4 * self.n:
+            pairs, splits = self.b.compact_touched(self.bounds)
+            sc = torch.tensor(splits, dtype=torch.int64, device=self.b.device)
+            rc = torch.empty_like(sc)
+            self.dist.all_to_all_single(rc, sc)
+            recv_splits = rc.tolist()
+            recv = torch.empty(sum(recv_splits), dtype=torch.int64, device=self.b.device)
+            self.dist.all_to_all_single(recv, pairs, recv_splits, list(splits))
+            self.b.scatter_pairs(recv)
+            return "sparse"
+        self._reduce_slices(op)
+        self.b.dense_exchanged()
+        return "dense"
 
     def _allreduce_counts(self, c: StepCounts) -> StepCounts:
         t = torch.tensor([c.recipients, c.broadcasts, c.senders, c.edges],
@@ -135,7 +163,7 @@ class PartitionedRun:
             self.b.reset_mailbox()
             self.b.scatter_min(dense=(app == "components" and s == 0),
                                id_offset=self.lo)
-            self._reduce_slices(op)
+            exchange = self._exchange_min(op)
             at_cap = s + 1 == max_steps
             local = self.b.apply_min(app, count_only=at_cap)
             nxt = self._allreduce_counts(local)
@@ -144,7 +172,7 @@ class PartitionedRun:
                               messages_sent=sent, edges=cur.edges,
                               senders=cur.senders, recipients=nxt.recipients,
                               broadcasters=cur.broadcasts,
-                              seconds=time.perf_counter() - ts))
+                              seconds=time.perf_counter() - ts, exchange=exchange))
             active = nxt.recipients
             if nxt.recipients == 0:
                 break
@@ -241,6 +269,12 @@ class CudaBackend:
         self.f_msg = torch.empty(self.len + 1, dtype=torch.int32, device=dev)
         self.f_tile = torch.empty(ntile, dtype=torch.int32, device=dev)
         self.nsrc, self.E = 0, 0
+        self.lo_own, self.hi_own = lo, hi
+        self.has = torch.zeros(self.n // 32 + 2, dtype=torch.int32, device=dev)
+        sb = _lib.out_size(self.lib.pgx_touched_scratch_bytes, self.n)
+        self.tscratch = torch.empty(sb, dtype=torch.uint8, device=dev)
+        self.tcount = torch.zeros(1, dtype=torch.int64, device=dev)
+        self._full_reset = True
 
     # ---- helpers ----
     def global_out_degree(self, v: int) -> int:
@@ -281,8 +315,43 @@ class CudaBackend:
     def reset_mailbox(self):
         if self.app == "pagerank":
             self.mailbox.zero_()
-        else:
+            return
+        # after a sparse exchange the foreign touched slots were reset by the
+        # compaction and the own slice by the apply; after a dense one every
+        # non-owned slot holds stale partial values
+        if self._full_reset:
             self.mailbox.fill_(EXCHANGE_NEUTRAL)
+        self.has.zero_()
+        self._full_reset = False
+
+    def dense_exchanged(self):
+        self._full_reset = True
+
+    def touched_count(self) -> int:
+        self._lib.check(self.lib.pgx_touched(
+            self.n, self.lo_own, self.hi_own, self.has.data_ptr(), None, EXCHANGE_NEUTRAL,
+            None, self.tcount.data_ptr(), self.tscratch.data_ptr(), self.stream.cuda_stream),
+            "pgx_touched")
+        return int(self.tcount.item())
+
+    def compact_touched(self, bounds):
+        cnt = int(self.tcount.item())
+        pairs = torch.empty(max(cnt, 1), dtype=torch.int64, device=self.device)
+        self._lib.check(self.lib.pgx_touched(
+            self.n, self.lo_own, self.hi_own, self.has.data_ptr(), self.mailbox.data_ptr(),
+            EXCHANGE_NEUTRAL, pairs.data_ptr(), self.tcount.data_ptr(),
+            self.tscratch.data_ptr(), self.stream.cuda_stream), "pgx_touched")
+        pairs = pairs[:cnt]
+        slots = pairs >> 32
+        b = torch.as_tensor(bounds[1:-1], dtype=torch.int64, device=self.device)
+        owner = torch.searchsorted(b, slots, right=True)
+        splits = torch.bincount(owner, minlength=len(bounds) - 1).tolist()
+        return pairs, splits
+
+    def scatter_pairs(self, pairs):
+        self._lib.check(self.lib.pgx_scatter_pairs(pairs.data_ptr(), pairs.numel(),
+                                                   self.mailbox.data_ptr(),
+                                                   self.stream.cuda_stream), "pgx_scatter_pairs")
 
     def scatter_min(self, dense: bool, id_offset: int):
         L, st = self.lib, self.stream.cuda_stream
@@ -292,12 +361,14 @@ class CudaBackend:
             rc = L.pgx_scatter(op, 1, self.col.data_ptr(), self._g_nz_eb.data_ptr(), None,
                                self._g_nz_id.data_ptr(), id_offset, None,
                                self._g_tile.data_ptr(), nnz, self.m_local,
-                               self.mailbox.data_ptr(), None, st)
+                               self.mailbox.data_ptr(), self.has.data_ptr(),
+                               EXCHANGE_NEUTRAL, st)
         else:
             rc = L.pgx_scatter(op, 0, self.col.data_ptr(), self.f_eb.data_ptr(),
                                self.f_rs.data_ptr(), None, 0, self.f_msg.data_ptr(),
                                self.f_tile.data_ptr(), self.nsrc, self.E,
-                               self.mailbox.data_ptr(), None, st)
+                               self.mailbox.data_ptr(), self.has.data_ptr(),
+                               EXCHANGE_NEUTRAL, st)
         self._lib.check(rc, "pgx_scatter")
 
     def apply_min(self, app, count_only: bool) -> StepCounts:
@@ -335,7 +406,7 @@ class CudaBackend:
         self._lib.check(self.lib.pgx_scatter(
             self._lib.PGX_OP_SUM_F64, 1, self.col.data_ptr(), self._g_nz_eb.data_ptr(), None,
             self._g_nz_id.data_ptr(), 0, self.share.data_ptr(), self._g_tile.data_ptr(), nnz,
-            self.m_local, self.mailbox.data_ptr(), None, self.stream.cuda_stream),
+            self.m_local, self.mailbox.data_ptr(), None, 0, self.stream.cuda_stream),
             "pgx_scatter")
 
     def apply_pagerank(self, base, damping, dn, last: bool) -> float:
@@ -377,7 +448,7 @@ def run_partitioned(graph, program, low, config, dist):
                                                 config.max_supersteps)
         v = vals.cpu().numpy().view(np.uint32)
         values = v.astype(np.int64) if app == "components" else v
-    steps = [SuperstepStats(**s) for s in stats]
+    steps = [SuperstepStats(**{k: v for k, v in s.items() if k != "exchange"}) for s in stats]
     if program.extract is not None:
         from types import SimpleNamespace
         values = program.extract(SimpleNamespace(state=values,

@@ -27,6 +27,8 @@ class CpuBackend:
         self.col = np.asarray(tgt[base:off[hi]], np.int64)
         self.deg = np.diff(self.row_ptr)
         self.front = (np.empty(0, np.int64), np.empty(0, np.int64))  # (local ids, msgs)
+        self.has = np.zeros(self.n, bool)
+        self._full_reset = True
 
     def global_out_degree(self, v):
         return int(self.glob_deg[v])
@@ -60,8 +62,35 @@ class CpuBackend:
     def reset_mailbox(self):
         if self.app == "pagerank":
             self.mailbox.zero_()
-        else:
+            return
+        if self._full_reset:
             self.mailbox.fill_(EXCHANGE_NEUTRAL)
+        self.has[:] = False
+        self._full_reset = False
+
+    def dense_exchanged(self):
+        self._full_reset = True
+
+    def _foreign(self):
+        idx = np.flatnonzero(self.has)
+        return idx[(idx < self.lo) | (idx >= self.hi)]
+
+    def touched_count(self):
+        return int(self._foreign().size)
+
+    def compact_touched(self, bounds):
+        idx = self._foreign()
+        mb = self.mailbox.numpy()
+        vals = mb[idx].astype(np.int64)
+        mb[idx] = EXCHANGE_NEUTRAL
+        pairs = torch.from_numpy((idx.astype(np.int64) << 32) | vals)
+        owner = np.searchsorted(np.asarray(bounds[1:-1]), idx, side="right")
+        return pairs, np.bincount(owner, minlength=len(bounds) - 1).tolist()
+
+    def scatter_pairs(self, pairs):
+        p = pairs.numpy()
+        np.minimum.at(self.mailbox.numpy(), (p >> 32).astype(np.int64),
+                      (p & 0xFFFFFFFF).astype(np.int32))
 
     def scatter_min(self, dense, id_offset):
         if dense:
@@ -72,6 +101,7 @@ class CpuBackend:
         dst, m = self._edges_of(lv, msg)
         mb = self.mailbox.numpy()
         np.minimum.at(mb, dst, m.astype(np.int32))
+        self.has[dst] = True
 
     def apply_min(self, app, count_only):
         sl = self.mailbox.numpy()[self.lo:self.hi].astype(np.int64)

@@ -31,7 +31,7 @@ def _free_port():
         return s.getsockname()[1]
 
 
-def _worker(rank, world, port, jobs, out_dir):
+def _worker(rank, world, port, jobs, out_dir, sparse_ok=True):
     import sys
     here = os.path.dirname(os.path.abspath(__file__))
     sys.path.insert(0, here)
@@ -45,6 +45,7 @@ def _worker(rank, world, port, jobs, out_dir):
         bounds = partition_bounds(np.diff(off), world)
         be = CpuBackend(off, tgt, int(bounds[rank]), int(bounds[rank + 1]))
         run = PartitionedRun(be, dist, bounds, n, int(tgt.size))
+        run.sparse_ok = sparse_ok
         cap = kw.get("max_supersteps", 10_000)
         if app == "pagerank":
             vals, stats, hit, _ = run.run_pagerank(kw.get("iterations", 10),
@@ -52,7 +53,8 @@ def _worker(rank, world, port, jobs, out_dir):
         else:
             vals, stats, hit, _ = run.run_min(app, kw.get("source", 0), cap)
         results.append((vals.numpy(), [(s["active_count"], s["messages_sent"])
-                                        for s in stats], hit))
+                                        for s in stats], hit,
+                        [s.get("exchange") for s in stats]))
     if rank == 0:
         torch.save(results, os.path.join(out_dir, "results.pt"))
     dist.barrier()
@@ -86,13 +88,15 @@ def _expected(off, tgt, app, kw):
                           max_steps=cap)
 
 
-@pytest.mark.parametrize("world", [2, 3])
-def test_partitioned_run_matches_oracle(world, tmp_path):
+@pytest.mark.parametrize("world,sparse_ok", [(2, True), (3, True), (2, False)])
+def test_partitioned_run_matches_oracle(world, sparse_ok, tmp_path):
     jobs = _jobs()
-    mp.start_processes(_worker, args=(world, _free_port(), jobs, str(tmp_path)),
+    mp.start_processes(_worker, args=(world, _free_port(), jobs, str(tmp_path), sparse_ok),
                        nprocs=world, start_method="spawn")
     results = torch.load(os.path.join(tmp_path, "results.pt"), weights_only=False)
-    for (off, tgt, app, kw), (vals, stats, hit) in zip(jobs, results):
+    modes = set()
+    for (off, tgt, app, kw), (vals, stats, hit, ex) in zip(jobs, results):
+        modes.update(m for m in ex if m)
         want = _expected(off, tgt, app, kw)
         if app == "pagerank":
             assert np.max(np.abs(vals - want.values) / np.abs(want.values)) <= 1e-9
@@ -101,6 +105,8 @@ def test_partitioned_run_matches_oracle(world, tmp_path):
         assert [a for a, _ in stats] == want.active_counts, (app, kw)
         assert [m for _, m in stats] == want.messages_sent, (app, kw)
         assert hit == want.hit_superstep_cap
+    # both exchanges ran (sparse on the late supersteps) unless disabled
+    assert modes == ({"dense", "sparse"} if sparse_ok else {"dense"})
 
 
 def test_partition_bounds_edge_balanced():

@@ -22,7 +22,7 @@ SPECS = [O.RmatSpec(14, 8, .57, .19, .19, 31, True),
          O.RmatSpec(13, 16, .45, .22, .22, 32, False)]
 
 
-def _run(off, tgt, app, kw, world):
+def _run(off, tgt, app, kw, world, sparse_ok=True):
     n = off.size - 1
     g = pgx.from_csr(torch.from_numpy(off).cuda(), torch.from_numpy(tgt).cuda())
     bounds = partition_bounds(np.diff(off), world)
@@ -30,6 +30,7 @@ def _run(off, tgt, app, kw, world):
     def rank_fn(r, d):
         be = CudaBackend(g, int(bounds[r]), int(bounds[r + 1]), "cuda:0")
         run = PartitionedRun(be, d, bounds, n, int(tgt.size))
+        run.sparse_ok = sparse_ok
         cap = kw.get("max_supersteps", 10_000)
         if app == "pagerank":
             return run.run_pagerank(10, 0.85, cap)
@@ -39,7 +40,8 @@ def _run(off, tgt, app, kw, world):
 
 @pytest.mark.parametrize("world", [1, 2, 4])
 @pytest.mark.parametrize("spec", SPECS, ids=["sym", "dir"])
-def test_partitioned_cuda_matches_oracle(spec, world):
+@pytest.mark.parametrize("sparse_ok", [True, False], ids=["hybrid-exchange", "dense-exchange"])
+def test_partitioned_cuda_matches_oracle(spec, world, sparse_ok):
     n, off, tgt = O.rmat_csr(spec)
     src = int(np.argmax(np.diff(off)))
     for app, kw, want in (
@@ -47,7 +49,7 @@ def test_partitioned_cuda_matches_oracle(spec, world):
             ("sssp", {"source": src}, O.run_sssp(n, off, tgt, src)),
             ("components", {"max_supersteps": 2}, O.run_cc(n, off, tgt, max_steps=2)),
             ("pagerank", {}, O.run_pagerank(n, off, tgt))):
-        vals, stats, hit, _ = _run(off, tgt, app, kw, world)
+        vals, stats, hit, _ = _run(off, tgt, app, kw, world, sparse_ok)
         v = vals.cpu().numpy()
         if app == "pagerank":
             assert np.max(np.abs(v - want.values) / np.abs(want.values)) <= 1e-9

@@ -69,6 +69,24 @@ class ThreadDist:
         torch.cuda.synchronize() if tensor.is_cuda else None
         self._bar.wait()
 
+    def all_to_all_single(self, out, inp, out_splits=None, in_splits=None):
+        r = self.get_rank()
+        torch.cuda.synchronize() if inp.is_cuda else None
+        w = self.world
+        ins = in_splits if in_splits is not None else [inp.numel() // w] * w
+        self._slots[r] = (inp, list(ins))
+        self._bar.wait()
+        chunks = []
+        for src in range(w):
+            t, sp = self._slots[src]
+            off = sum(sp[:r])
+            chunks.append(t[off:off + sp[r]])
+        self._bar.wait()
+        if chunks:
+            out.copy_(torch.cat(chunks))
+        torch.cuda.synchronize() if out.is_cuda else None
+        self._bar.wait()
+
     def all_gather(self, parts, tensor):
         r = self.get_rank()
         torch.cuda.synchronize() if tensor.is_cuda else None
