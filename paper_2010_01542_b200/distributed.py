@@ -91,15 +91,26 @@ class PartitionedRun:
         self.lo = int(self.bounds[self.rank])
         self.hi = int(self.bounds[self.rank + 1])
         self.sparse_ok = True  # allow the sparse exchange (A/B switch)
+        self._coalesced = None  # NCCL uneven reduce_scatter available?
 
     # ---- collectives --------------------------------------------------
 
     def _reduce_slices(self, op):
+        """Deliver every owner the reduction of its mailbox slice."""
         full = self.b.mailbox
-        for r in range(self.world):
-            lo, hi = int(self.bounds[r]), int(self.bounds[r + 1])
-            if hi > lo:
-                self.dist.reduce(full[lo:hi], dst=r, op=op)
+        parts = [full[int(self.bounds[r]):int(self.bounds[r + 1])] for r in range(self.world)]
+        backend = getattr(self.dist, "get_backend", lambda: None)()
+        if self._coalesced is not False and str(backend) == "nccl":
+            # one uneven reduce_scatter: NCCL coalesces the per-owner reduces
+            try:
+                self.dist.reduce_scatter(parts[self.rank], parts, op=op)
+                self._coalesced = True
+                return
+            except Exception:  # pragma: no cover - torch without uneven support
+                self._coalesced = False
+        for r, part in enumerate(parts):
+            if part.numel():
+                self.dist.reduce(part, dst=r, op=op)
 
     def _exchange_min(self, op) -> str:
         """Dense per-owner reduction or sparse pair exchange (collective choice)."""
