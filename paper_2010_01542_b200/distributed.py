@@ -42,7 +42,6 @@ from dataclasses import dataclass
 import numpy as np
 import torch
 
-from .errors import ConfigError
 from .scheduler import edge_balanced_partition
 
 #: min neutral of the exchanged mailbox: INT32_MAX, so that the signed

@@ -18,7 +18,6 @@ honoured (applied to the final state on the host, engine.py:310-311).
 
 from __future__ import annotations
 
-import ctypes
 import time
 from dataclasses import dataclass, field
 from enum import Enum

@@ -7,7 +7,6 @@ import os
 import re
 import subprocess
 
-import numpy as np
 import pytest
 
 import paper_2010_01542_b200 as pgx
