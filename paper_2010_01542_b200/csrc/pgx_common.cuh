@@ -19,9 +19,6 @@
 #ifndef PGX_MIN_BLOCKS
 #define PGX_MIN_BLOCKS 2     // persistent CTAs of 512 threads per SM (64 regs)
 #endif
-#ifndef PGX_SCATTER_SMEM
-#define PGX_SCATTER_SMEM 1   // stage each warp tile's sources in shared memory
-#endif
 #ifndef PGX_PASS
 #define PGX_PASS 4           // 32-edge rounds in flight per scatter pass
 #endif
@@ -280,9 +277,11 @@ struct ScatterArgs {
 // shared memory of the scatter: one source window per warp (+ the hub
 // cache of the min combiner, right after the windows)
 __host__ __device__ constexpr size_t scatter_windows_smem(int op) {
-  return PGX_SCATTER_SMEM
-             ? (size_t)kWarps * kSlots * (sizeof(int32_t) * 2 + (op == PGX_OP_SUM_F64 ? 8 : 4))
-             : (size_t)kApplyListBytes;  // the apply's recipient list still needs smem
+  // s_eb (4 B) + {message | row offset, message} (8 B) per slot; the apply
+  // reuses the same region for its recipient list
+  return (size_t)kWarps * kSlots * (sizeof(int32_t) + 8) > (size_t)kApplyListBytes
+             ? (size_t)kWarps * kSlots * (sizeof(int32_t) + 8)
+             : (size_t)kApplyListBytes;
 }
 __host__ __device__ constexpr size_t scatter_smem(int op, int nhubs = 0) {
   return scatter_windows_smem(op) + (op == PGX_OP_MIN_U32 ? sizeof(uint32_t) * nhubs : 0) + 16;

@@ -32,10 +32,13 @@ __device__ void scatter_phase(const ScatterArgs &a, char *smem, bool read_filter
   constexpr bool kDense = MS != MsgSrc::kFrontier;
   const int lane = (int)lane_id();
   const int warp = threadIdx.x >> 5;
+  // per-warp source window: row starts (boundary candidates) and, per
+  // source, either the message (dense senders: pos = e) or the packed pair
+  // {row offset - edge base, message} (sparse frontier: pos = e + off)
   int32_t *s_eb = reinterpret_cast<int32_t *>(smem) + warp * kSlots;
-  int32_t *s_rs = reinterpret_cast<int32_t *>(smem) + kWarps * kSlots + warp * kSlots;
-  Msg *s_msg = reinterpret_cast<Msg *>(reinterpret_cast<int32_t *>(smem) + 2 * kWarps * kSlots) +
-               warp * kSlots;
+  char *s_second = smem + sizeof(int32_t) * kWarps * kSlots;
+  Msg *s_msg = reinterpret_cast<Msg *>(s_second) + warp * kSlots;
+  uint2 *s_om = reinterpret_cast<uint2 *>(s_second) + warp * kSlots;
   const uint64_t pol = evict_first_policy();
   const int64_t ntiles = (a.E + kTile - 1) / kTile;
   const unsigned upto = (lane == 31) ? 0xFFFFFFFFu : ((2u << lane) - 1u);
@@ -53,15 +56,15 @@ __device__ void scatter_phase(const ScatterArgs &a, char *smem, bool read_filter
     const int i0 = a.tile_src[t];
     const int i1 = (t + 1 < ntiles) ? a.tile_src[t + 1] : a.nsrc - 1;
     const int k = i1 - i0 + 1;  // <= kTile + 1
-#if PGX_SCATTER_SMEM
     __syncwarp();
     for (int j = lane; j <= k; j += 32) {
       const int i = i0 + j;
       if (j < k) {
-        s_eb[j] = a.eb[i];
-        if (!kDense) s_rs[j] = a.rs[i];
+        const int32_t eb = a.eb[i];
+        s_eb[j] = eb;
         if (MS == MsgSrc::kFrontier) {
-          s_msg[j] = reinterpret_cast<const Msg *>(a.msg)[i];
+          s_om[j] = make_uint2((uint32_t)(a.rs[i] - eb),
+                               (uint32_t)reinterpret_cast<const uint32_t *>(a.msg)[i]);
         } else if (MS == MsgSrc::kSourceId) {
           s_msg[j] = (Msg)(a.ids[i] + a.id_offset);
         } else {
@@ -72,24 +75,8 @@ __device__ void scatter_phase(const ScatterArgs &a, char *smem, bool read_filter
       }
     }
     __syncwarp();
-#define PGX_EB(j) s_eb[j]
-#define PGX_RS(j) s_rs[j]
-#define PGX_MSG(j) s_msg[j]
-#else
-    // no staging: boundary candidates are 32 consecutive ints (one or two
-    // sectors per round) and per-source data are broadcast loads, both
-    // L1 hits after the first round -- all of shared memory stays L1
-    const int32_t *g_eb = a.eb + i0;
-    const int nrem = a.nsrc - i0;
-#define PGX_EB(j) ((j) < nrem ? __ldg(g_eb + (j)) : (int32_t)a.E)
-#define PGX_RS(j) __ldg(a.rs + i0 + (j))
-#define PGX_MSG(j)                                                              \
-  (MS == MsgSrc::kFrontier ? __ldg(reinterpret_cast<const Msg *>(a.msg) + i0 + (j)) \
-   : MS == MsgSrc::kSourceId ? (Msg)(__ldg(a.ids + i0 + (j)) + a.id_offset)       \
-   : __ldg(reinterpret_cast<const Msg *>(a.msg) + __ldg(a.ids + i0 + (j))))
-#endif
 
-    int cur = 0;  // eb[0] <= e0: tile_src names the source holding e0
+    int cur = 0;  // s_eb[0] <= e0: tile_src names the source holding e0
 #pragma unroll 1
     for (int pass = 0; pass < kItems / kPass; pass++) {
       int w[kPass];
@@ -101,7 +88,7 @@ __device__ void scatter_phase(const ScatterArgs &a, char *smem, bool read_filter
         const int ci = cur + 1 + lane;
         unsigned bit = 0;
         if (ci <= k) {
-          const int64_t pp = (int64_t)PGX_EB(ci) - base;
+          const int64_t pp = (int64_t)s_eb[ci] - base;
           if (pp >= 0 && pp < 32) bit = 1u << pp;
         }
         const unsigned bm = __reduce_or_sync(0xFFFFFFFFu, bit);
@@ -109,9 +96,15 @@ __device__ void scatter_phase(const ScatterArgs &a, char *smem, bool read_filter
         cur += __popc(bm);
         w[r] = kInvalidEdge;
         if (e < e1) {
-          const int64_t pos = kDense ? e : (int64_t)PGX_RS(src) + (e - PGX_EB(src));
+          int64_t pos = e;
+          if (kDense) {
+            mv[r] = s_msg[src];
+          } else {
+            const uint2 om = s_om[src];
+            pos = e + (int32_t)om.x;
+            mv[r] = (Msg)om.y;
+          }
           w[r] = ld_stream(a.col + pos, pol);
-          mv[r] = PGX_MSG(src);
         }
       }
       if (OP == PGX_OP_MIN_U32) {
@@ -168,9 +161,6 @@ __device__ void scatter_phase(const ScatterArgs &a, char *smem, bool read_filter
           if (w[r] != kInvalidEdge) atomicAdd(mb + w[r], (double)mv[r]);
       }
     }
-#undef PGX_EB
-#undef PGX_RS
-#undef PGX_MSG
   }
 }
 
