@@ -24,7 +24,8 @@ for it in range(6):
     a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     a.record()
     _lib.check(lib.pgx_scatter(0, 1, c.col_idx.data_ptr(), nz_eb.data_ptr(), None, nz_id.data_ptr(),
-                               0, None, tile.data_ptr(), nnz, m, mb.data_ptr(), has.data_ptr(), st),
+                               0, None, tile.data_ptr(), nnz, m, mb.data_ptr(), has.data_ptr(),
+                               0xFFFFFFFF, st),
                "pgx_scatter")
     b.record(); torch.cuda.synchronize()
     ts.append(a.elapsed_time(b))
