@@ -44,15 +44,18 @@ __device__ __forceinline__ unsigned long long block_excl_scan_u64(unsigned long 
   return r;
 }
 
-// Apply chunk: kApplyWords bitmask words per block iteration.  The set
-// bits are first compacted into a shared-memory vertex list (block scan
-// of popcounts), then every thread consumes up to kApplyItems recipients
-// with independent loads -- no per-word serial chains.
-#ifndef PGX_APPLY_WORDS
-#define PGX_APPLY_WORDS 64
+// Apply chunk: every CTA takes kBlock bitmask words (one per thread, in
+// 32-word groups interleaved across the grid; a quiet chunk costs one load
+// and one barrier).  The set bits are compacted
+// into a shared-memory vertex list (block scan of popcounts, segments of
+// kListCap ids), which is consumed in batches of kApplyItems independent
+// recipients per thread -- a handful of dependent round trips per chunk
+// instead of one serial chain per 64 words.
+#ifndef PGX_APPLY_ITEMS
+#define PGX_APPLY_ITEMS 4
 #endif
-constexpr int kApplyWords = PGX_APPLY_WORDS;
-constexpr int kApplyItems = kApplyWords * 32 / kBlock;  // 4
+constexpr int kApplyItems = PGX_APPLY_ITEMS;
+constexpr int kListCap = kApplyListBytes / (int)sizeof(int32_t);
 
 // Returns (recipients counted) << 32 | (broadcasts) for this thread.  With
 // `count_only` the bitmask is only counted (superstep cap reached: the
@@ -63,7 +66,7 @@ __device__ unsigned long long apply_min_phase(const int32_t *__restrict__ row_pt
                                               StepCounters *ctr, char *smem, bool count_only) {
   __shared__ unsigned long long s_w[33];
   __shared__ unsigned long long s_gbase;
-  int32_t *s_list = reinterpret_cast<int32_t *>(smem);  // kApplyWords * 32 ids
+  int32_t *s_list = reinterpret_cast<int32_t *>(smem);  // kListCap vertex ids
   uint32_t *f_msg = reinterpret_cast<uint32_t *>(ws.f_msg);
   const int words = (n + 31) >> 5;
   unsigned bcast = 0, recips = 0;
@@ -72,88 +75,100 @@ __device__ unsigned long long apply_min_phase(const int32_t *__restrict__ row_pt
       recips += __popc(ws.has[wi]);
     return ((unsigned long long)recips << 32);
   }
-  for (int base = blockIdx.x * kApplyWords; base < words; base += gridDim.x * kApplyWords) {
-    // ---- expand the chunk's set bits into s_list (vertex order) ----
+  // warp w of CTA b takes 32-word group gb + w * grid + b: consecutive
+  // groups go to consecutive CTAs, which spreads the dense
+  // (low-id) region of a power-law graph over the whole grid
+  const int groups = (words + 31) >> 5;
+  for (int gb = 0; gb < groups; gb += gridDim.x * kWarps) {  // block-uniform
+    const int g = gb + (int)(threadIdx.x >> 5) * gridDim.x + blockIdx.x;
+    const int wi = g * 32 + (int)lane_id();
     uint32_t word = 0;
-    const int wi = base + threadIdx.x;
-    if (threadIdx.x < kApplyWords && wi < words) {
+    if (g < groups && wi < words) {
       word = ws.has[wi];
       if (word) ws.has[wi] = 0u;
     }
-    if (!__syncthreads_or(word != 0)) continue;  // empty chunk: one barrier
-    recips += __popc(word);
+    if (!__syncthreads_or(word != 0)) continue;  // quiet chunk: one barrier
+    const int c = __popc(word);
+    recips += c;
     unsigned long long tot64;
-    const int off = (int)block_excl_scan_u64((unsigned long long)__popc(word), s_w, &tot64);
+    const int off = (int)block_excl_scan_u64((unsigned long long)c, s_w, &tot64);
     const int T = (int)tot64;
-    if (T == 0) continue;  // block-uniform
-    {
-      int o = off;
-      uint32_t rem = word;
-      while (rem) {
-        const int b = __ffs(rem) - 1;
-        rem &= rem - 1;
-        s_list[o++] = (wi << 5) + b;
-      }
-    }
-    __syncthreads();
-    // ---- consume + compute, kApplyItems independent recipients / thread ----
-    int v[kApplyItems];
-    uint32_t m[kApplyItems], cv[kApplyItems];
-    int deg[kApplyItems], rs[kApplyItems];
-#pragma unroll
-    for (int j = 0; j < kApplyItems; j++) {
-      const int idx = j * kBlock + threadIdx.x;
-      v[j] = (idx < T) ? s_list[idx] : -1;
-    }
-#pragma unroll
-    for (int j = 0; j < kApplyItems; j++) {
-      if (v[j] >= 0) {
-        m[j] = mailbox[v[j]];
-        cv[j] = val[v[j]];
-      }
-    }
-    unsigned long long mine = 0;
-#pragma unroll
-    for (int j = 0; j < kApplyItems; j++) {
-      deg[j] = 0;
-      if (v[j] >= 0) {
-        mailbox[v[j]] = kNeutralMin;  // consume (mailbox.py:112-117)
-        if (m[j] < cv[j]) {
-          val[v[j]] = m[j];
-          bcast++;
-          rs[j] = row_ptr[v[j]];
-          deg[j] = -1;  // improved; degree resolved below
+    for (int seg = 0; seg < T; seg += kListCap) {  // block-uniform
+      // ---- expand this segment of the set bits into s_list (vertex order) ----
+      if (off < seg + kListCap && off + c > seg) {
+        int o = off;
+        uint32_t rem = word;
+        while (rem) {
+          const int b = __ffs(rem) - 1;
+          rem &= rem - 1;
+          if (o >= seg && o < seg + kListCap) s_list[o - seg] = (wi << 5) + b;
+          o++;
         }
       }
-    }
-#pragma unroll
-    for (int j = 0; j < kApplyItems; j++) {
-      if (deg[j] == -1) {
-        deg[j] = row_ptr[v[j] + 1] - rs[j];
-        if (deg[j] > 0) mine += (1ull << 32) | (unsigned long long)deg[j];
-      }
-    }
-    unsigned long long total;
-    unsigned long long run = block_excl_scan_u64(mine, s_w, &total);
-    if (total != 0) {  // block-uniform
-      if (threadIdx.x == 0) s_gbase = atomicAdd(&ctr->packed, total);
       __syncthreads();
-      run += s_gbase;
+      const int cnt = min(kListCap, T - seg);
+      for (int b0 = 0; b0 < cnt; b0 += kBlock * kApplyItems) {  // block-uniform
+        // ---- consume + compute, kApplyItems independent recipients / thread ----
+        int v[kApplyItems];
+        uint32_t m[kApplyItems], cv[kApplyItems];
+        int deg[kApplyItems], rs[kApplyItems];
 #pragma unroll
-      for (int j = 0; j < kApplyItems; j++) {
-        if (deg[j] > 0) {
-          const unsigned pos = (unsigned)(run >> 32);
-          const int eb = (int)(run & 0xFFFFFFFFull);
-          ws.f_eb[pos] = eb;
-          ws.f_rs[pos] = rs[j];
-          f_msg[pos] = (APP == PGX_APP_SSSP) ? m[j] + 1u : m[j];
-          for (int64_t t = ((int64_t)eb + kTile - 1) / kTile; t * kTile < (int64_t)eb + deg[j]; t++)
-            ws.tile_src[t] = (int)pos;
-          run += (1ull << 32) | (unsigned long long)deg[j];
+        for (int j = 0; j < kApplyItems; j++) {
+          const int idx = b0 + j * kBlock + threadIdx.x;
+          v[j] = (idx < cnt) ? s_list[idx] : -1;
+        }
+#pragma unroll
+        for (int j = 0; j < kApplyItems; j++) {
+          if (v[j] >= 0) {
+            m[j] = mailbox[v[j]];
+            cv[j] = val[v[j]];
+          }
+        }
+        unsigned long long mine = 0;
+#pragma unroll
+        for (int j = 0; j < kApplyItems; j++) {
+          deg[j] = 0;
+          if (v[j] >= 0) {
+            mailbox[v[j]] = kNeutralMin;  // consume (mailbox.py:112-117)
+            if (m[j] < cv[j]) {
+              val[v[j]] = m[j];
+              bcast++;
+              rs[j] = row_ptr[v[j]];
+              deg[j] = -1;  // improved; degree resolved below
+            }
+          }
+        }
+#pragma unroll
+        for (int j = 0; j < kApplyItems; j++) {
+          if (deg[j] == -1) {
+            deg[j] = row_ptr[v[j] + 1] - rs[j];
+            if (deg[j] > 0) mine += (1ull << 32) | (unsigned long long)deg[j];
+          }
+        }
+        unsigned long long total;
+        unsigned long long run = block_excl_scan_u64(mine, s_w, &total);
+        if (total != 0) {  // block-uniform
+          if (threadIdx.x == 0) s_gbase = atomicAdd(&ctr->packed, total);
+          __syncthreads();
+          run += s_gbase;
+#pragma unroll
+          for (int j = 0; j < kApplyItems; j++) {
+            if (deg[j] > 0) {
+              const unsigned pos = (unsigned)(run >> 32);
+              const int eb = (int)(run & 0xFFFFFFFFull);
+              ws.f_eb[pos] = eb;
+              ws.f_rs[pos] = rs[j];
+              f_msg[pos] = (APP == PGX_APP_SSSP) ? m[j] + 1u : m[j];
+              for (int64_t t = ((int64_t)eb + kTile - 1) / kTile; t * kTile < (int64_t)eb + deg[j];
+                   t++)
+                ws.tile_src[t] = (int)pos;
+              run += (1ull << 32) | (unsigned long long)deg[j];
+            }
+          }
         }
       }
+      __syncthreads();  // s_list reuse
     }
-    __syncthreads();  // s_list / s_gbase reuse
   }
   return ((unsigned long long)recips << 32) | bcast;
 }

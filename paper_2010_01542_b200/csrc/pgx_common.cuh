@@ -34,7 +34,7 @@ constexpr int kSlots = kTile + 2;    // sources per warp tile (+ sentinel)
 constexpr uint32_t kNeutralMin = 0xFFFFFFFFu;
 constexpr int kHubs = 12288;         // hub recipients cached per CTA (48 KB smem)
 constexpr int kInvalidEdge = 0x7FFFFFFF;  // never a vertex id (n < 2^31 - 1)
-constexpr int kApplyListBytes = 128 * 32 * 4;  // apply: up to 128 words * 32 vertex ids
+constexpr int kApplyListBytes = 12288 * 4;  // apply: vertex-id list segment (fits the scatter windows)
 constexpr int kMaxCtas = 4096;
 constexpr int kCompactBlock = 1024;
 
