@@ -282,7 +282,9 @@ def bench_gpu(args):
         else SCATTER_CEILING["load"]
     per_config = {}
     if world == 1 and not args.no_per_config:
-        for c2 in ("C1", "C3", "C4"):
+        # C5 on one GPU is the same-workload N=1 point of the 2/4/8-GPU
+        # scaling runs (which measure C5); the headline N=1 line is C2
+        for c2 in ("C1", "C3", "C4", "C5"):
             if c2 == cfg:
                 continue
             del plan

@@ -78,7 +78,16 @@ const char *pgx_last_error(void);
 #define PGX_OPT_CTAS_PER_SM 1   /* persistent CTAs per SM, 0 = occupancy max */
 #define PGX_OPT_CAS_LOOP 2      /* ablation: CAS retry loop per message (lock-style) */
 #define PGX_OPT_VERTEX_SCHED 3  /* ablation: one thread per sender (no edge balance) */
-#define PGX_OPT_COUNT 4
+#define PGX_OPT_LAYOUT 4        /* ablation: PGX_LAYOUT_* of the CC/SSSP vertex state */
+#define PGX_OPT_COUNT 5
+
+/* PGX_OPT_LAYOUT values (LayoutMode, layout.py:31-33).  EXTERNALISED is the
+ * default SoA (value[], mailbox[] apart).  INTERLEAVED keeps one {mailbox,
+ * value} record per vertex (the reference's AoS record, layout.py:85-129)
+ * inside the run workspace; pgx_run_workspace_bytes sizes it, so set the
+ * option before querying the size. */
+#define PGX_LAYOUT_EXTERNALISED 0
+#define PGX_LAYOUT_INTERLEAVED 1
 int pgx_set_option(int key, int value);
 
 /* number of SMs of `device` (host out pointer; syncs) */

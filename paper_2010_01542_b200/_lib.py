@@ -22,6 +22,8 @@ PGX_APP_PAGERANK, PGX_APP_CC, PGX_APP_SSSP, PGX_APP_PAGERANK_PULL = 0, 1, 2, 3
 PGX_OP_MIN_U32, PGX_OP_SUM_F64 = 0, 1
 PGX_STAT_HDR, PGX_STAT_FIELDS = 4, 8
 PGX_OPT_READ_FILTER, PGX_OPT_CTAS_PER_SM, PGX_OPT_CAS_LOOP, PGX_OPT_VERTEX_SCHED = 0, 1, 2, 3
+PGX_OPT_LAYOUT = 4
+PGX_LAYOUT_EXTERNALISED, PGX_LAYOUT_INTERLEAVED = 0, 1
 
 
 def set_option(key: int, value: int) -> None:

@@ -60,7 +60,7 @@ constexpr int kListCap = kApplyListBytes / (int)sizeof(int32_t);
 // Returns (recipients counted) << 32 | (broadcasts) for this thread.  With
 // `count_only` the bitmask is only counted (superstep cap reached: the
 // pending messages must stay unconsumed, engine.py:299-300).
-template <int APP>
+template <int APP, int S = 0>
 __device__ unsigned long long apply_min_phase(const int32_t *__restrict__ row_ptr, uint32_t *val,
                                               uint32_t *mailbox, int32_t n, const RunWs &ws,
                                               StepCounters *ctr, char *smem, bool count_only) {
@@ -120,8 +120,8 @@ __device__ unsigned long long apply_min_phase(const int32_t *__restrict__ row_pt
 #pragma unroll
         for (int j = 0; j < kApplyItems; j++) {
           if (v[j] >= 0) {
-            m[j] = mailbox[v[j]];
-            cv[j] = val[v[j]];
+            m[j] = *slot<S>(mailbox, v[j]);
+            cv[j] = *slot<S>(val, v[j]);
           }
         }
         unsigned long long mine = 0;
@@ -129,9 +129,9 @@ __device__ unsigned long long apply_min_phase(const int32_t *__restrict__ row_pt
         for (int j = 0; j < kApplyItems; j++) {
           deg[j] = 0;
           if (v[j] >= 0) {
-            mailbox[v[j]] = kNeutralMin;  // consume (mailbox.py:112-117)
+            *slot<S>(mailbox, v[j]) = kNeutralMin;  // consume (mailbox.py:112-117)
             if (m[j] < cv[j]) {
-              val[v[j]] = m[j];
+              *slot<S>(val, v[j]) = m[j];
               bcast++;
               rs[j] = row_ptr[v[j]];
               deg[j] = -1;  // improved; degree resolved below

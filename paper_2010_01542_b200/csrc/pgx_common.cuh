@@ -105,6 +105,13 @@ __device__ __forceinline__ uint64_t evict_first_policy() {
 
 __device__ __forceinline__ unsigned lane_id() { return threadIdx.x & 31u; }
 
+// Vertex slot v of a state array: S = 0 externalised SoA, S = 1 the
+// interleaved {mailbox, value} record array (PGX_LAYOUT_INTERLEAVED).
+template <int S, typename T>
+__device__ __forceinline__ T *slot(T *base, int64_t v) {
+  return base + (v << S);
+}
+
 __device__ __forceinline__ void red_min_u32(uint32_t *p, uint32_t v) {
   asm volatile("red.relaxed.gpu.global.min.u32 [%0], %1;" :: "l"(p), "r"(v) : "memory");
 }
@@ -214,7 +221,7 @@ struct RunWs {
 };
 
 inline size_t run_ws_layout(int app, int64_t n, int64_t m, int32_t max_steps, RunWs *ws,
-                     char *base) {
+                     char *base, bool interleaved = false) {
   size_t off = 0;
   auto take = [&](size_t bytes) {
     char *p = base ? base + off : nullptr;
@@ -229,7 +236,8 @@ inline size_t run_ws_layout(int app, int64_t n, int64_t m, int32_t max_steps, Ru
   w.partials = (double *)take(sizeof(double) * kMaxCtas);
   w.misc = (unsigned long long *)take(64);
   w.f_msg = take(W * (size_t)(n + 1));
-  w.mailbox = take(W * (size_t)(n + 1));
+  // interleaved layout (min programs): {mailbox, value} records
+  w.mailbox = take(W * (size_t)(n + 1) * (interleaved && !pr ? 2 : 1));
   w.share2 = w.head = w.tail = nullptr;
   if (app == PGX_APP_PAGERANK_PULL) {
     w.share2 = (double *)take(sizeof(double) * (size_t)(n + 1));

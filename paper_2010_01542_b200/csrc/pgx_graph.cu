@@ -13,6 +13,7 @@ int g_opt[PGX_OPT_COUNT] = {
     /* PGX_OPT_CTAS_PER_SM */ 0,   // 0 = occupancy maximum
     /* PGX_OPT_CAS_LOOP */ 0,      // ablation: CAS retry per message
     /* PGX_OPT_VERTEX_SCHED */ 0,  // ablation: one thread per sender
+    /* PGX_OPT_LAYOUT */ PGX_LAYOUT_EXTERNALISED,
 };
 
 namespace {

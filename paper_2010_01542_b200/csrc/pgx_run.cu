@@ -51,25 +51,30 @@ struct MinRunParams {
   int32_t read_filter;
   int32_t cas_loop;       // ablation arms (pgx_set_option)
   int32_t vertex_sched;
+  int32_t interleaved;    // PGX_LAYOUT_INTERLEAVED: {mailbox, value} records in ws.mailbox
   const int32_t *hub_ids;
   int32_t nhubs;
   int64_t *stats;
 };
 
-template <int APP>
+// S = 0: externalised SoA (value = the caller's output array); S = 1:
+// interleaved {mailbox, value} records (layout.py's INTERLEAVED), values
+// copied out to the caller's array at the end of the run.
+template <int APP, int S>
 __global__ void __launch_bounds__(kBlock, PGX_MIN_BLOCKS) min_run_kernel(MinRunParams p) {
   extern __shared__ __align__(16) char smem[];
   __shared__ unsigned s_red[32];
   unsigned gen = 0;
   if (threadIdx.x == 0) gen = ld_acquire(&p.ws.bar->gen);
   uint32_t *mailbox = reinterpret_cast<uint32_t *>(p.ws.mailbox);
+  uint32_t *val = S ? mailbox + 1 : p.val;
   const unsigned nthreads = gridDim.x * blockDim.x;
   const unsigned gtid = blockIdx.x * blockDim.x + threadIdx.x;
 
   // ---- setup (algorithms.py:96-97 / 129-134) + superstep-0 senders ----
   for (unsigned v = gtid; v < (unsigned)p.n; v += nthreads) {
-    p.val[v] = (APP == PGX_APP_CC) ? v : kNeutralMin;
-    mailbox[v] = kNeutralMin;
+    *slot<S>(val, v) = (APP == PGX_APP_CC) ? v : kNeutralMin;
+    *slot<S>(mailbox, v) = kNeutralMin;
   }
   for (unsigned wi = gtid; wi < (unsigned)(p.n / 32 + 2); wi += nthreads) p.ws.has[wi] = 0u;
   if (blockIdx.x == 0 && threadIdx.x == 0) {
@@ -95,7 +100,7 @@ __global__ void __launch_bounds__(kBlock, PGX_MIN_BLOCKS) min_run_kernel(MinRunP
     }
   }
   grid_sync(p.ws.bar, gen);
-  if (APP == PGX_APP_SSSP && gtid == 0) p.val[p.source] = 0u;
+  if (APP == PGX_APP_SSSP && gtid == 0) *slot<S>(val, p.source) = 0u;
   if (gtid == 0) p.stats[PGX_STAT_HDR + 7] = (int64_t)globaltimer();
 
   for (int s = 0;; s++) {
@@ -118,9 +123,9 @@ __global__ void __launch_bounds__(kBlock, PGX_MIN_BLOCKS) min_run_kernel(MinRunP
       a.nsrc = p.g.hdr[0];
       a.E = p.m;
       if (p.vertex_sched)
-        scatter_vertex_phase<MsgSrc::kSourceId>(a, p.read_filter);
+        scatter_vertex_phase<MsgSrc::kSourceId, S>(a, p.read_filter);
       else
-        scatter_phase<PGX_OP_MIN_U32, MsgSrc::kSourceId>(a, smem, p.read_filter);
+        scatter_phase<PGX_OP_MIN_U32, MsgSrc::kSourceId, S>(a, smem, p.read_filter);
     } else {
       const unsigned long long packed = p.ws.ctr[s].packed;
       a.eb = p.ws.f_eb;
@@ -131,9 +136,9 @@ __global__ void __launch_bounds__(kBlock, PGX_MIN_BLOCKS) min_run_kernel(MinRunP
       a.nsrc = (int32_t)(packed >> 32);
       a.E = (int64_t)(packed & 0xFFFFFFFFull);
       if (p.vertex_sched)
-        scatter_vertex_phase<MsgSrc::kFrontier>(a, p.read_filter);
+        scatter_vertex_phase<MsgSrc::kFrontier, S>(a, p.read_filter);
       else
-        scatter_phase<PGX_OP_MIN_U32, MsgSrc::kFrontier>(a, smem, p.read_filter);
+        scatter_phase<PGX_OP_MIN_U32, MsgSrc::kFrontier, S>(a, smem, p.read_filter);
     }
     if (blockIdx.x == 0 && threadIdx.x == 0) {
       StepCounters z = {};
@@ -146,7 +151,7 @@ __global__ void __launch_bounds__(kBlock, PGX_MIN_BLOCKS) min_run_kernel(MinRunP
     //      pending messages are only counted (engine.py:299-300) ----
     const bool at_cap = (s + 1 == p.max_steps);
     const unsigned long long rb =
-        apply_min_phase<APP>(p.row_ptr, p.val, mailbox, p.n, p.ws, &p.ws.ctr[s + 1], smem, at_cap);
+        apply_min_phase<APP, S>(p.row_ptr, val, mailbox, p.n, p.ws, &p.ws.ctr[s + 1], smem, at_cap);
     const unsigned bc = block_sum<unsigned>((unsigned)(rb & 0xFFFFFFFFull), s_red);
     const unsigned rc = block_sum<unsigned>((unsigned)(rb >> 32), s_red);
     if (threadIdx.x == 0) {
@@ -178,6 +183,9 @@ __global__ void __launch_bounds__(kBlock, PGX_MIN_BLOCKS) min_run_kernel(MinRunP
       }
     }
     if (nrecip == 0 || at_cap) break;
+  }
+  if (S) {  // RunReport.values from the records (engine.py:310-311)
+    for (unsigned v = gtid; v < (unsigned)p.n; v += nthreads) p.val[v] = *slot<S>(val, v);
   }
 }
 
@@ -432,7 +440,8 @@ int pgx_run_workspace_bytes(int app, int64_t n, int64_t m, int32_t max_superstep
                             size_t *bytes) {
   if (!bytes || n < 0 || m < 0 || max_supersteps < 1 || app < 0 || app > 3)
     return fail(PGX_EINVAL, "bad run workspace arguments");
-  *bytes = run_ws_layout(app, n, m, max_supersteps, nullptr, nullptr);
+  *bytes = run_ws_layout(app, n, m, max_supersteps, nullptr, nullptr,
+                         g_opt[PGX_OPT_LAYOUT] == PGX_LAYOUT_INTERLEAVED);
   return PGX_OK;
 }
 
@@ -454,7 +463,9 @@ static int min_run(int app, int32_t n, int64_t m, const int32_t *row_ptr, const 
   p.row_ptr = row_ptr;
   p.col = col_idx;
   graph_ws_layout(n, m, &p.g, (char *)graph_ws);
-  if (run_ws_layout(app, n, m, max_supersteps, &p.ws, (char *)run_ws) > run_ws_bytes)
+  p.interleaved = g_opt[PGX_OPT_LAYOUT] == PGX_LAYOUT_INTERLEAVED;
+  if (run_ws_layout(app, n, m, max_supersteps, &p.ws, (char *)run_ws, p.interleaved) >
+      run_ws_bytes)
     return fail(PGX_ENOMEM, "run workspace too small");
   p.val = val;
   p.source = source;
@@ -470,17 +481,14 @@ static int min_run(int app, int32_t n, int64_t m, const int32_t *row_ptr, const 
   const size_t smem = scatter_smem(PGX_OP_MIN_U32, nhubs);
   int grid = 0;
   void *args[] = {&p};
-  if (app == PGX_APP_SSSP) {
-    rc = coop_grid(min_run_kernel<PGX_APP_SSSP>, smem, &grid);
-    if (rc) return rc;
-    PGX_CUDA(cudaLaunchCooperativeKernel((void *)min_run_kernel<PGX_APP_SSSP>, grid, kBlock,
-                                         args, smem, st));
-  } else {
-    rc = coop_grid(min_run_kernel<PGX_APP_CC>, smem, &grid);
-    if (rc) return rc;
-    PGX_CUDA(cudaLaunchCooperativeKernel((void *)min_run_kernel<PGX_APP_CC>, grid, kBlock,
-                                         args, smem, st));
-  }
+  void (*kern)(MinRunParams) =
+      app == PGX_APP_SSSP ? (p.interleaved ? min_run_kernel<PGX_APP_SSSP, 1>
+                                           : min_run_kernel<PGX_APP_SSSP, 0>)
+                          : (p.interleaved ? min_run_kernel<PGX_APP_CC, 1>
+                                           : min_run_kernel<PGX_APP_CC, 0>);
+  rc = coop_grid(kern, smem, &grid);
+  if (rc) return rc;
+  PGX_CUDA(cudaLaunchCooperativeKernel((void *)kern, grid, kBlock, args, smem, st));
   return PGX_OK;
 }
 

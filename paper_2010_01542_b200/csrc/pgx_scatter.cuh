@@ -26,7 +26,7 @@ namespace pgx {
 // and filtered against a per-CTA shared-memory copy of their mailbox;
 // only a CTA-local improvement goes to the global red.min.
 
-template <int OP, MsgSrc MS>
+template <int OP, MsgSrc MS, int S = 0>
 __device__ void scatter_phase(const ScatterArgs &a, char *smem, bool read_filter = true) {
   using Msg = typename std::conditional<OP == PGX_OP_SUM_F64, double, uint32_t>::type;
   constexpr bool kDense = MS != MsgSrc::kFrontier;
@@ -121,7 +121,7 @@ __device__ void scatter_phase(const ScatterArgs &a, char *smem, bool read_filter
           const int x = w[r];
           old[r] = (x == kInvalidEdge) ? 0u
                    : (x < 0) ? s_hub[x & 0x7FFFFFFF]  // hub: CTA-local filter
-                   : (read_filter ? mb[x] : a.neutral);
+                   : (read_filter ? *slot<S>(mb, x) : a.neutral);
         }
 #pragma unroll
         for (int r = 0; r < kPass; r++) {
@@ -132,23 +132,23 @@ __device__ void scatter_phase(const ScatterArgs &a, char *smem, bool read_filter
             uint32_t prev = old[r];
             if (x < 0) {  // hub: the CTA-local copy let it through; consult
                           // the global slot (the shared filter) before the red
-              const int slot = x & 0x7FFFFFFF;
-              v = a.hub_ids[slot];
-              prev = mb[v];
-              s_hub[slot] = min(prev, msg);  // racy store: only weakens the filter
+              const int hs = x & 0x7FFFFFFF;
+              v = a.hub_ids[hs];
+              prev = *slot<S>(mb, v);
+              s_hub[hs] = min(prev, msg);  // racy store: only weakens the filter
               if (msg >= prev) v = -1;
             }
             if (v >= 0) {
               if (a.cas_loop) {  // ablation: lock-style CAS retry per message
                 uint32_t cur = prev;
                 while (msg < cur) {
-                  const uint32_t got = atomicCAS(mb + v, cur, msg);
+                  const uint32_t got = atomicCAS(slot<S>(mb, v), cur, msg);
                   if (got == cur) break;
                   cur = got;
                 }
                 if (a.has && prev == a.neutral) atomicOr(a.has + (v >> 5), 1u << (v & 31));
               } else {
-                red_min_u32(mb + v, msg);
+                red_min_u32(slot<S>(mb, v), msg);
                 if (a.has && prev == a.neutral) red_or_b32(a.has + (v >> 5), 1u << (v & 31));
               }
             }
@@ -168,7 +168,7 @@ __device__ void scatter_phase(const ScatterArgs &a, char *smem, bool read_filter
 // Ablation arm of the scheduler (harness.py:273-292 grid): one thread per
 // sender walks its whole out-row (the reference's vertex-centric split,
 // scheduler.py:79-88).  No edge balance: a hub row serialises on one lane.
-template <MsgSrc MS>
+template <MsgSrc MS, int S = 0>
 __device__ void scatter_vertex_phase(const ScatterArgs &a, bool read_filter) {
   constexpr bool kDense = MS != MsgSrc::kFrontier;
   uint32_t *mb = reinterpret_cast<uint32_t *>(a.mailbox);
@@ -182,17 +182,17 @@ __device__ void scatter_vertex_phase(const ScatterArgs &a, bool read_filter) {
                              : (uint32_t)(a.ids[i] + a.id_offset);
     for (int64_t e = eb; e < ee; e++) {
       const int v = a.col[rs + (e - eb)];
-      const uint32_t prev = read_filter ? mb[v] : a.neutral;
+      const uint32_t prev = read_filter ? *slot<S>(mb, v) : a.neutral;
       if (msg < prev) {
         if (a.cas_loop) {
           uint32_t cur = prev;
           while (msg < cur) {
-            const uint32_t got = atomicCAS(mb + v, cur, msg);
+            const uint32_t got = atomicCAS(slot<S>(mb, v), cur, msg);
             if (got == cur) break;
             cur = got;
           }
         } else {
-          red_min_u32(mb + v, msg);
+          red_min_u32(slot<S>(mb, v), msg);
         }
         if (a.has && prev == a.neutral) red_or_b32(a.has + (v >> 5), 1u << (v & 31));
       }

@@ -64,3 +64,23 @@ def test_no_cpu_fallback():
     for prog in (pgx.pagerank(), pgx.connected_components(), pgx.sssp(0)):
         with pytest.raises(pgx.ExecutionError):
             pgx.run(g, prog)
+
+
+def test_header_constants_match_the_binding():
+    defines = dict(re.findall(r"#define (PGX_[A-Z0-9_]+) (-?\d+)", open(HEADER).read()))
+    bound = {k: getattr(_lib, k) for k in defines if hasattr(_lib, k)}
+    assert {"PGX_OPT_LAYOUT", "PGX_LAYOUT_INTERLEAVED", "PGX_OPT_READ_FILTER"} <= set(bound)
+    for k, v in bound.items():
+        assert int(defines[k]) == v, k
+
+
+def test_interleaved_layout_sizes_the_record_array():
+    lib = _lib.load()
+    soa, aos = ctypes.c_size_t(0), ctypes.c_size_t(0)
+    assert lib.pgx_run_workspace_bytes(1, 1 << 20, 1 << 24, 16, ctypes.byref(soa)) == 0
+    _lib.set_option(_lib.PGX_OPT_LAYOUT, _lib.PGX_LAYOUT_INTERLEAVED)
+    try:
+        assert lib.pgx_run_workspace_bytes(1, 1 << 20, 1 << 24, 16, ctypes.byref(aos)) == 0
+    finally:
+        _lib.set_option(_lib.PGX_OPT_LAYOUT, _lib.PGX_LAYOUT_EXTERNALISED)
+    assert aos.value - soa.value >= 4 * (1 << 20)

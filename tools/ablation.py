@@ -1,9 +1,9 @@
 """B200 ablation grid mirroring the reference harness's grid_variants
 (harness.py:273-292: baseline, then each optimisation alone, then all):
 
-  combiner   lock-style CAS retry per message  ->  hybrid (read-filter + red.min)
-  scheduler  one thread per sender             ->  edge-balanced 256-edge warp tiles
-  layout     (always SoA on the device)
+  layout     interleaved {mailbox, value} records  ->  externalised SoA
+  combiner   lock-style CAS retry per message       ->  hybrid (read-filter + red.min)
+  scheduler  one thread per sender                  ->  edge-balanced 256-edge warp tiles
 
 Every arm must reproduce the shipped arm's values and per-superstep counts.
 Writes profiles/ablation_<tag>.json and prints a markdown table.
@@ -15,19 +15,24 @@ import paper_2010_01542_b200 as pgx
 from paper_2010_01542_b200 import _lib
 from paper_2010_01542_b200.rmat import rmat_graph
 
-ARMS = [  # name, read_filter, cas_loop, vertex_sched
-    ("baseline (vertex-per-thread, CAS loop)", 0, 1, 1),
-    ("+ edge-balanced tiles only", 0, 1, 0),
-    ("+ hybrid combiner only", 1, 0, 1),
-    ("final (edge tiles + hybrid)", 1, 0, 0),
-    ("final, red.min without read-filter", 0, 0, 0),
+IL, EX = _lib.PGX_LAYOUT_INTERLEAVED, _lib.PGX_LAYOUT_EXTERNALISED
+ARMS = [  # name, read_filter, cas_loop, vertex_sched, layout
+    ("baseline (interleaved, vertex-per-thread, CAS loop)", 0, 1, 1, IL),
+    ("+ hybrid combiner only", 1, 0, 1, IL),
+    ("+ externalised layout only", 0, 1, 1, EX),
+    ("+ edge-balanced tiles only", 0, 1, 0, IL),
+    ("final (externalised + edge tiles + hybrid)", 1, 0, 0, EX),
+    ("final with the interleaved layout", 1, 0, 0, IL),
+    ("final, red.min without read-filter", 0, 0, 0, EX),
 ]
+FINAL = 4
 
 
-def set_arm(rf, cas, vs):
+def set_arm(rf, cas, vs, layout):
     _lib.set_option(_lib.PGX_OPT_READ_FILTER, rf)
     _lib.set_option(_lib.PGX_OPT_CAS_LOOP, cas)
     _lib.set_option(_lib.PGX_OPT_VERTEX_SCHED, vs)
+    _lib.set_option(_lib.PGX_OPT_LAYOUT, layout)
 
 
 def time_plan(plan, prog, reps):
@@ -50,8 +55,9 @@ def main():
         prog = pgx.connected_components() if cfg == "C2" else pgx.sssp(int(torch.argmax(g.out_degrees)))
         ref = None
         res = {}
-        for name, rf, cas, vs in reversed(ARMS):   # final first: the reference arm
-            set_arm(rf, cas, vs)
+        order = [ARMS[FINAL]] + [a for i, a in enumerate(ARMS) if i != FINAL]
+        for name, *opts in order:   # final first: the reference arm
+            set_arm(*opts)
             plan = pgx.plan_run(g, prog)
             ms, rep = time_plan(plan, prog, reps)
             if ref is None:
@@ -61,7 +67,7 @@ def main():
             E = sum(s.edges for s in rep.supersteps)
             res[name] = {"ms": round(ms, 3), "GTEPS": round(E / ms / 1e6, 2), "identical": bool(same)}
             print(cfg, name, res[name], flush=True)
-        set_arm(1, 0, 0)
+        set_arm(*ARMS[FINAL][1:])
         base = res[ARMS[0][0]]["ms"]
         for name, *_ in ARMS:
             res[name]["speedup_vs_baseline"] = round(base / res[name]["ms"], 2)
