@@ -355,8 +355,10 @@ def bench_gpu(args):
 
 def bench_multi(args):
     """N > 1 under torchrun: the partitioned superstep of the
-    same workload on every rank's GPU, NCCL reductions over NVLink; strong
-    scaling (the graph is fixed).  Timed with CUDA events around each run,
+    same workload on every rank's GPU; min programs combine foreign messages
+    straight into the owners' mailboxes over NVLink peer memory (the fused
+    exchange, --exchange auto/peer) or through NCCL collectives (--exchange
+    hybrid/dense); strong scaling (the graph is fixed).  Timed with CUDA events around each run,
     max over ranks."""
     import torch
     import torch.distributed as dist
@@ -365,16 +367,23 @@ def bench_multi(args):
 
     world = int(os.environ["WORLD_SIZE"])
     rank = int(os.environ.get("RANK", "0"))
-    local = int(os.environ.get("LOCAL_RANK", "0"))
+    # LOCAL_RANK modulo the visible devices: identity on a node with a GPU
+    # per rank; lets a functional run put several ranks on one GPU
+    local = int(os.environ.get("LOCAL_RANK", "0")) % torch.cuda.device_count()
     torch.cuda.set_device(local)
     os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
-    dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    backend = os.environ.get("PGX_DIST_BACKEND", "nccl")  # gloo: functional runs only
+    if backend == "nccl":
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    else:
+        dist.init_process_group(backend)
     cfg = args.config
     app = APP_OF[cfg]
     g = rmat_graph(cfg)
     n, m = g.vertex_count, g.edge_count
     prog = program_for(pgx, app, g)
     flush = torch.empty(512 << 20, dtype=torch.uint8, device="cuda")
+    os.environ["PGX_EXCHANGE"] = args.exchange
     for _ in range(args.warmup):
         rep = pgx.run(g, prog)
     ms = []
@@ -424,13 +433,20 @@ def bench_multi(args):
                                f"over {world} GPUs (edge-balanced ranges)",
                    "n": n, "m": m, "supersteps": rep.superstep_count,
                    "l2": "flushed (512 MiB write) between timed steps",
-                   "parallelism": f"partitioned x{world}, NCCL reduce per owner + allreduce"},
+                   "parallelism": f"partitioned x{world}: " + (
+                       "fused peer-memory combine (NVLink P2P red.min) + allreduce"
+                       if "peer" in (rep.exchanges or []) else
+                       "NCCL reduce_scatter / sparse all_to_all + allreduce"),
+                   "exchange_per_superstep": rep.exchanges,
+                   "process_group": backend},
         "e2e": {"value": round(edges / (e2e_ms * 1e-3) / 1e9, 4), "unit": "GTEPS",
                 "h2d_bytes_per_step": (n + 1) * 8 + m * 4,
                 "d2h_bytes_per_step": n * (8 if app == "pagerank" else 4),
                 "ms_per_step": round(e2e_ms, 3)},
-        # our kernels per timed step: pgx_scatter + pgx_apply_slice per superstep
-        "gpu_launches": 2 * rep.superstep_count * args.steps,
+        # our kernels per timed step: scatter + apply (+ reset_touched for
+        # the peer exchange) per superstep
+        "gpu_launches": (3 if "peer" in (rep.exchanges or []) else 2)
+                        * rep.superstep_count * args.steps,
         "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak * world,
                      "unit": "GB/s", "frac": round(achieved / (peak * world), 4),
                      "traffic": None, "peak_source": peak_src + f" x {world} GPUs"},
@@ -507,6 +523,8 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-per-config", action="store_true")
     ap.add_argument("--aux-steps", type=int, default=5)
+    ap.add_argument("--exchange", default="auto", choices=["auto", "peer", "hybrid", "dense"],
+                    help="N>1 min-program mailbox exchange (default: fused peer when mappable)")
     ap.add_argument("--pr-push", dest="pr_pull", action="store_false",
                     help="PageRank A/B arm: push scatter with red.add.f64")
     args = ap.parse_args()

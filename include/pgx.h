@@ -173,7 +173,9 @@ int pgx_pagerank_pull_run(int32_t n, int64_t m, const int32_t *row_ptr,
 /* with GLOBAL destination ids) and that slice of the mailbox.  Per    */
 /* superstep the host calls pgx_scatter (into a full-width local       */
 /* mailbox), reduces the slices onto their owners (NCCL min / sum via  */
-/* torch.distributed), then pgx_apply_slice / pgx_pr_apply_slice.      */
+/* torch.distributed), then pgx_apply_slice / pgx_pr_apply_slice --    */
+/* or, for min programs, pgx_scatter_peer, which combines straight     */
+/* into the owners' mailboxes over peer memory (no reduction).         */
 /* Replaces the same reference functions as the *_run entry points,    */
 /* one phase at a time.                                                */
 /* ---------------------------------------------------------------- */
@@ -211,6 +213,42 @@ int pgx_touched(int32_t n, int32_t lo, int32_t hi, const uint32_t *has_bits,
                 int64_t *count, void *scratch, uintptr_t stream);
 int pgx_scatter_pairs(const uint64_t *pairs, int64_t count, uint32_t *mailbox,
                       uintptr_t stream);
+
+/* Fused peer-memory exchange (min programs): the compute step and the
+ * collective in ONE kernel.  Like pgx_scatter(PGX_OP_MIN_U32, ...) into this
+ * rank's full-width `mailbox` (its local filter), and every message that
+ * passes the filter with a recipient outside [lo, hi) is also combined with
+ * a fire-and-forget red.min into the owner's slot, peer_mailboxes[owner] +
+ * v (device array of `world` base pointers: NVLink peer mappings from
+ * pgx_peer_open, or this process's own pointers); owners come from the
+ * device array bounds[world + 1].  The kernel ends with a system-scope
+ * fence, so the collective the caller issues after it on the stream (the
+ * counters all-reduce) orders every peer combine before the owners' apply.
+ * No mailbox reduction is needed afterwards.  Replaces send_hybrid /
+ * apply_cas (mailbox.py:147-199) across GPUs. */
+int pgx_scatter_peer(int dense, const int32_t *col_idx, const int32_t *src_eb,
+                     const int32_t *src_rs, const int32_t *src_ids,
+                     int32_t id_offset, const void *src_msg,
+                     const int32_t *tile_src, int32_t nsrc, int64_t edges,
+                     uint32_t *mailbox, uint32_t *has_bits, uint32_t neutral,
+                     const uint64_t *peer_mailboxes, const int32_t *bounds,
+                     int32_t world, int32_t lo, int32_t hi, uintptr_t stream);
+
+/* After a peer-exchange superstep: reset the foreign slots this rank
+ * touched (set has-bits outside [lo, hi)) to `neutral`, clear every
+ * has-bit.  Owned slots are consumed by pgx_apply_slice. */
+int pgx_reset_touched(int32_t n, int32_t lo, int32_t hi, uint32_t *has_bits,
+                      uint32_t *mailbox, uint32_t neutral, uintptr_t stream);
+
+/* Mailboxes other processes can map (CUDA IPC over NVLink / NVSwitch):
+ * pgx_peer_alloc = cudaMalloc + its IPC handle (PGX_IPC_HANDLE_BYTES,
+ * may be NULL); pgx_peer_open maps another process's handle (peer access
+ * enabled lazily); pgx_peer_close unmaps; pgx_peer_free frees. */
+#define PGX_IPC_HANDLE_BYTES 64
+int pgx_peer_alloc(size_t bytes, void **ptr, void *ipc_handle);
+int pgx_peer_open(const void *ipc_handle, void **ptr);
+int pgx_peer_close(void *ptr);
+int pgx_peer_free(void *ptr);
 
 /* size of the device counter block used by pgx_apply_slice (host out) */
 int pgx_slice_counters_bytes(size_t *bytes);

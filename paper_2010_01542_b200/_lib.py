@@ -23,6 +23,7 @@ PGX_OP_MIN_U32, PGX_OP_SUM_F64 = 0, 1
 PGX_STAT_HDR, PGX_STAT_FIELDS = 4, 8
 PGX_OPT_READ_FILTER, PGX_OPT_CTAS_PER_SM, PGX_OPT_CAS_LOOP, PGX_OPT_VERTEX_SCHED = 0, 1, 2, 3
 PGX_OPT_LAYOUT = 4
+PGX_IPC_HANDLE_BYTES = 64
 PGX_LAYOUT_EXTERNALISED, PGX_LAYOUT_INTERLEAVED = 0, 1
 
 
@@ -38,6 +39,8 @@ EXPORTS = (
     "pgx_pagerank_run", "pgx_pagerank_pull_run", "pgx_rmat_keys", "pgx_microbench",
     "pgx_slice_init", "pgx_scatter", "pgx_slice_counters_bytes", "pgx_apply_slice",
     "pgx_pr_apply_slice", "pgx_touched_scratch_bytes", "pgx_touched", "pgx_scatter_pairs",
+    "pgx_scatter_peer", "pgx_reset_touched", "pgx_peer_alloc", "pgx_peer_open",
+    "pgx_peer_close", "pgx_peer_free",
 )
 
 _lib = None
@@ -74,6 +77,13 @@ _SIGS = {
     "pgx_touched_scratch_bytes": (ctypes.c_int, [_i32, _p]),
     "pgx_touched": (ctypes.c_int, [_i32, _i32, _i32, _p, _p, ctypes.c_uint32, _p, _p, _p, _up]),
     "pgx_scatter_pairs": (ctypes.c_int, [_p, _i64, _p, _up]),
+    "pgx_scatter_peer": (ctypes.c_int, [ctypes.c_int, _p, _p, _p, _p, _i32, _p, _p, _i32, _i64,
+                                        _p, _p, ctypes.c_uint32, _p, _p, _i32, _i32, _i32, _up]),
+    "pgx_reset_touched": (ctypes.c_int, [_i32, _i32, _i32, _p, _p, ctypes.c_uint32, _up]),
+    "pgx_peer_alloc": (ctypes.c_int, [_sz, _p, _p]),
+    "pgx_peer_open": (ctypes.c_int, [_p, _p]),
+    "pgx_peer_close": (ctypes.c_int, [_p]),
+    "pgx_peer_free": (ctypes.c_int, [_p]),
     "pgx_slice_counters_bytes": (ctypes.c_int, [_p]),
     "pgx_apply_slice": (ctypes.c_int, [ctypes.c_int, _i32, _p, _p, _p, _p, _p, _p, _p, _p,
                                        _i32, ctypes.c_uint32, _up]),

@@ -280,6 +280,13 @@ struct ScatterArgs {
   int32_t nhubs;          // (sign bit | slot).  nhubs == 0: no hub cache
   int32_t cas_loop;       // ablation: CAS retry loop instead of red.min
   uint32_t neutral;       // min neutral of the mailbox (has-bit publication)
+  // fused peer-memory exchange (pgx_scatter_peer): a message that passes
+  // the local filter and whose recipient another rank owns is also
+  // combined into the owner's mailbox, peer_mb[owner] (NVLink P2P)
+  uint32_t *const *peer_mb;  // [world] mailbox base of every rank
+  const int32_t *bounds;     // [world + 1] owner ranges
+  int32_t world;
+  int32_t lo, hi;            // this rank's own range
 };
 
 // shared memory of the scatter: one source window per warp (+ the hub

@@ -26,7 +26,7 @@ namespace pgx {
 // and filtered against a per-CTA shared-memory copy of their mailbox;
 // only a CTA-local improvement goes to the global red.min.
 
-template <int OP, MsgSrc MS, int S = 0>
+template <int OP, MsgSrc MS, int S = 0, bool PEER = false>
 __device__ void scatter_phase(const ScatterArgs &a, char *smem, bool read_filter = true) {
   using Msg = typename std::conditional<OP == PGX_OP_SUM_F64, double, uint32_t>::type;
   constexpr bool kDense = MS != MsgSrc::kFrontier;
@@ -150,6 +150,14 @@ __device__ void scatter_phase(const ScatterArgs &a, char *smem, bool read_filter
               } else {
                 red_min_u32(slot<S>(mb, v), msg);
                 if (a.has && prev == a.neutral) red_or_b32(a.has + (v >> 5), 1u << (v & 31));
+              }
+              if (PEER && (v < a.lo || v >= a.hi)) {
+                // the local slot is this rank's filter; the owner's slot is
+                // the combined mailbox: one more fire-and-forget red.min,
+                // over NVLink when the owner is another GPU
+                int o = 0;
+                while (o + 1 < a.world && v >= __ldg(a.bounds + o + 1)) o++;
+                red_min_u32(a.peer_mb[o] + v, msg);
               }
             }
           }

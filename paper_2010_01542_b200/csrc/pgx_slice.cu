@@ -31,11 +31,15 @@ struct SliceCounters {       // device counters of one partitioned superstep
 #define PGX_SCATTER_MIN_BLOCKS PGX_MIN_BLOCKS
 #endif
 
-template <int OP, MsgSrc MS>
+template <int OP, MsgSrc MS, bool PEER = false>
 __global__ void __launch_bounds__(kBlock, PGX_SCATTER_MIN_BLOCKS) scatter_kernel(ScatterArgs a,
                                                                           int read_filter) {
   extern __shared__ __align__(16) char smem[];
-  scatter_phase<OP, MS>(a, smem, read_filter != 0);
+  scatter_phase<OP, MS, 0, PEER>(a, smem, read_filter != 0);
+  // the peer reds are performed at system scope before the kernel ends, so
+  // the collective that follows it on the stream orders them before the
+  // owners' apply
+  if (PEER) __threadfence_system();
 }
 
 template <int APP>
@@ -198,6 +202,25 @@ __global__ void __launch_bounds__(kCompactBlock) touched_write_kernel(
   }
 }
 
+// Peer exchange epilogue: the foreign slots this rank touched (its local
+// filter copies) go back to the neutral and every has-bit is cleared; the
+// owned slots were consumed by the apply.
+__global__ void reset_touched_kernel(uint32_t *has, int32_t n, int32_t lo, int32_t hi,
+                                     uint32_t *mailbox, uint32_t neutral) {
+  const int words = (n + 31) >> 5;
+  for (int wi = blockIdx.x * blockDim.x + threadIdx.x; wi < words;
+       wi += gridDim.x * blockDim.x) {
+    if (!has[wi]) continue;
+    uint32_t rem = foreign_bits(has, wi, n, lo, hi);
+    has[wi] = 0u;
+    while (rem) {
+      const int b = __ffs(rem) - 1;
+      rem &= rem - 1;
+      mailbox[(wi << 5) + b] = neutral;
+    }
+  }
+}
+
 __global__ void scatter_pairs_min_kernel(const unsigned long long *pairs, int64_t count,
                                          uint32_t *mailbox) {
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < count;
@@ -277,6 +300,112 @@ int pgx_scatter(int op, int dense, const int32_t *col_idx, const int32_t *src_eb
     return fail(PGX_EINVAL, "sum scatter needs the dense sender list");
   }
   PGX_CUDA(cudaGetLastError());
+  return PGX_OK;
+}
+
+int pgx_scatter_peer(int dense, const int32_t *col_idx, const int32_t *src_eb,
+                     const int32_t *src_rs, const int32_t *src_ids, int32_t id_offset,
+                     const void *src_msg, const int32_t *tile_src, int32_t nsrc, int64_t edges,
+                     uint32_t *mailbox, uint32_t *has_bits, uint32_t neutral,
+                     const uint64_t *peer_mailboxes, const int32_t *bounds, int32_t world,
+                     int32_t lo, int32_t hi, uintptr_t stream) {
+  if (edges < 0 || edges > INT32_MAX || nsrc < 0) return fail(PGX_EINVAL, "bad sizes");
+  if (world < 1 || lo < 0 || hi < lo || !peer_mailboxes || !bounds)
+    return fail(PGX_EINVAL, "bad peer arguments");
+  if (edges == 0) return PGX_OK;
+  if (!col_idx || !src_eb || !tile_src || !mailbox || !has_bits ||
+      (!dense && (!src_rs || !src_msg)) || (dense && !src_ids))
+    return fail(PGX_EINVAL, "null scatter pointer");
+  ScatterArgs a;
+  a.col = col_idx;
+  a.eb = src_eb;
+  a.rs = src_rs;
+  a.ids = src_ids;
+  a.msg = src_msg;
+  a.tile_src = tile_src;
+  a.nsrc = nsrc;
+  a.E = edges;
+  a.mailbox = mailbox;
+  a.has = has_bits;
+  a.id_offset = id_offset;
+  a.hub_ids = nullptr;
+  a.nhubs = 0;
+  a.cas_loop = 0;
+  a.neutral = neutral;
+  a.peer_mb = reinterpret_cast<uint32_t *const *>(peer_mailboxes);
+  a.bounds = bounds;
+  a.world = world;
+  a.lo = lo;
+  a.hi = hi;
+  const int64_t tiles = ceil_div(edges, kTile);
+  int sms = 148, dev = 0;
+  if (cudaGetDevice(&dev) == cudaSuccess)
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(ceil_div(tiles, kWarps),
+                                                               (int64_t)sms * PGX_SCATTER_MIN_BLOCKS));
+  cudaStream_t st = (cudaStream_t)stream;
+  const size_t smem = scatter_smem(PGX_OP_MIN_U32);
+  const int rf = g_opt[PGX_OPT_READ_FILTER];
+  if (!dense) {
+    PGX_CUDA(cudaFuncSetAttribute(scatter_kernel<PGX_OP_MIN_U32, MsgSrc::kFrontier, true>,
+                                  cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    scatter_kernel<PGX_OP_MIN_U32, MsgSrc::kFrontier, true><<<grid, kBlock, smem, st>>>(a, rf);
+  } else {
+    PGX_CUDA(cudaFuncSetAttribute(scatter_kernel<PGX_OP_MIN_U32, MsgSrc::kSourceId, true>,
+                                  cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    scatter_kernel<PGX_OP_MIN_U32, MsgSrc::kSourceId, true><<<grid, kBlock, smem, st>>>(a, rf);
+  }
+  PGX_CUDA(cudaGetLastError());
+  return PGX_OK;
+}
+
+int pgx_reset_touched(int32_t n, int32_t lo, int32_t hi, uint32_t *has_bits, uint32_t *mailbox,
+                      uint32_t neutral, uintptr_t stream) {
+  if (n < 1 || lo < 0 || hi < lo || hi > n || !has_bits || !mailbox)
+    return fail(PGX_EINVAL, "bad pgx_reset_touched arguments");
+  const int words = (int)ceil_div(n, 32);
+  const int grid = (int)std::min<int64_t>(ceil_div(words, 256), 148 * 8);
+  reset_touched_kernel<<<grid, 256, 0, (cudaStream_t)stream>>>(has_bits, n, lo, hi, mailbox,
+                                                               neutral);
+  PGX_CUDA(cudaGetLastError());
+  return PGX_OK;
+}
+
+int pgx_peer_alloc(size_t bytes, void **ptr, void *ipc_handle) {
+  if (!ptr || !bytes) return fail(PGX_EINVAL, "bad pgx_peer_alloc arguments");
+  *ptr = nullptr;
+  PGX_CUDA(cudaMalloc(ptr, bytes));
+  if (ipc_handle) {
+    cudaIpcMemHandle_t h;
+    const cudaError_t e = cudaIpcGetMemHandle(&h, *ptr);
+    if (e != cudaSuccess) {
+      cudaFree(*ptr);
+      *ptr = nullptr;
+      return cuda_fail(e, "cudaIpcGetMemHandle");
+    }
+    memcpy(ipc_handle, &h, sizeof h);
+  }
+  return PGX_OK;
+}
+
+int pgx_peer_open(const void *ipc_handle, void **ptr) {
+  if (!ipc_handle || !ptr) return fail(PGX_EINVAL, "bad pgx_peer_open arguments");
+  cudaIpcMemHandle_t h;
+  memcpy(&h, ipc_handle, sizeof h);
+  *ptr = nullptr;
+  PGX_CUDA(cudaIpcOpenMemHandle(ptr, h, cudaIpcMemLazyEnablePeerAccess));
+  return PGX_OK;
+}
+
+int pgx_peer_close(void *ptr) {
+  if (!ptr) return fail(PGX_EINVAL, "null pointer");
+  PGX_CUDA(cudaIpcCloseMemHandle(ptr));
+  return PGX_OK;
+}
+
+int pgx_peer_free(void *ptr) {
+  if (!ptr) return fail(PGX_EINVAL, "null pointer");
+  PGX_CUDA(cudaFree(ptr));
   return PGX_OK;
 }
 

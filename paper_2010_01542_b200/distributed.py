@@ -20,6 +20,17 @@ one GPU (CC labels / SSSP distances bit-exact, PageRank within 1e-9):
 * has-message after the reduction is ``mailbox != neutral``: CC / SSSP
   messages are < n <= 2^31 and never equal UINT32_MAX, and PageRank needs
   no flag (the paper's neutral-value caveat).
+* **fused peer exchange** (min programs, the default when every rank can
+  map every other rank's mailbox): the scatter kernel itself combines each
+  message that passes its local filter into the OWNER's mailbox slot over
+  NVLink peer memory (``pgx_scatter_peer``: one fire-and-forget
+  ``red.min`` per surviving foreign message, a system-scope fence at the
+  end), so the mailbox is never reduced by a collective: a one-element
+  all-reduce after the scatter orders the peers' combines before the
+  owners' apply.  Mailboxes are ``cudaMalloc`` blocks shared by CUDA IPC
+  (``pgx_peer_alloc`` / ``pgx_peer_open``); ranks that are threads of one
+  process use the raw pointers.  The choice is collective: if any rank
+  cannot map a peer, every rank falls back to the collective exchanges.
 * **sparse exchange** (SURVEY 8(f) row 3): late supersteps touch few
   mailbox slots, yet the dense reduction always moves n slots.  Every rank
   counts the slots it touched outside its own range (has-bits of the
@@ -36,6 +47,8 @@ libpgx.so on the rank's GPU (NCCL process group); tests/ drive the same
 
 from __future__ import annotations
 
+import ctypes
+import os
 import time
 from dataclasses import dataclass
 
@@ -89,13 +102,67 @@ class PartitionedRun:
         self.n, self.m = n, m
         self.lo = int(self.bounds[self.rank])
         self.hi = int(self.bounds[self.rank + 1])
-        self.sparse_ok = True  # allow the sparse exchange (A/B switch)
+        # min-program exchange: "auto" (peer if every rank maps every peer,
+        # else hybrid), "peer", "hybrid" (dense / sparse per superstep),
+        # "dense" (A/B switches)
+        self.exchange = "auto"
         self._coalesced = None  # NCCL uneven reduce_scatter available?
+        be = str(getattr(dist, "get_backend", lambda: "")())
+        # gloo has no CUDA all_gather: small collectives go through the host
+        self._host_coll = be == "gloo" and self.b.device.type == "cuda"
+        self._cdev = torch.device("cpu") if self._host_coll else self.b.device
+
+    @property
+    def sparse_ok(self) -> bool:
+        return self.exchange != "dense"
+
+    @sparse_ok.setter
+    def sparse_ok(self, ok: bool):
+        self.exchange = "auto" if ok else "dense"
+
+    def _coll_sync(self):
+        """Before a host-side collective: the rank's kernels have finished."""
+        if self._host_coll:
+            torch.cuda.current_stream(self.b.device).synchronize()
+
+    def _peer_setup(self) -> bool:
+        """Map every rank's mailbox on every rank (collective decision)."""
+        if self.exchange not in ("auto", "peer") or not hasattr(self.b, "peer_handle"):
+            want = False
+        else:
+            want = True
+        h = self.b.peer_handle() if want else None
+        handles = [None] * self.world
+        self.dist.all_gather_object(handles, h)
+        ok = all(x is not None for x in handles) and self.b.open_peers(handles, self.bounds)
+        t = torch.tensor([1 if ok else 0], dtype=torch.int64, device=self._cdev)
+        self._coll_sync()
+        self.dist.all_reduce(t, op=self.dist.ReduceOp.MIN)
+        ok = bool(t.item())
+        if not ok and self.exchange == "peer":
+            raise RuntimeError("peer exchange requested but a rank cannot map its peers")
+        self.b.peer_active = ok
+        return ok
+
+    def _fence(self):
+        """All ranks' peer combines land before any owner applies."""
+        t = torch.zeros(1, dtype=torch.int64, device=self._cdev)
+        self._coll_sync()
+        self.dist.all_reduce(t)
 
     # ---- collectives --------------------------------------------------
 
     def _reduce_slices(self, op):
         """Deliver every owner the reduction of its mailbox slice."""
+        if self._host_coll:  # gloo: stage the mailbox through the host
+            self._coll_sync()
+            full = self.b.mailbox.cpu()
+            for r in range(self.world):
+                part = full[int(self.bounds[r]):int(self.bounds[r + 1])]
+                if part.numel():
+                    self.dist.reduce(part, dst=r, op=op)
+            self.b.mailbox[self.lo:self.hi].copy_(full[self.lo:self.hi])
+            return
         full = self.b.mailbox
         parts = [full[int(self.bounds[r]):int(self.bounds[r + 1])] for r in range(self.world)]
         backend = getattr(self.dist, "get_backend", lambda: None)()
@@ -114,17 +181,18 @@ class PartitionedRun:
     def _exchange_min(self, op) -> str:
         """Dense per-owner reduction or sparse pair exchange (collective choice)."""
         touched = self.b.touched_count()
-        t = torch.tensor([touched], dtype=torch.int64, device=self.b.device)
+        t = torch.tensor([touched], dtype=torch.int64, device=self._cdev)
         self.dist.all_reduce(t, op=self.dist.ReduceOp.MAX)
-        if self.sparse_ok and 8 * int(t.item()) * 2 < 4 * self.n:
+        if self.exchange != "dense" and 8 * int(t.item()) * 2 < 4 * self.n:
             pairs, splits = self.b.compact_touched(self.bounds)
-            sc = torch.tensor(splits, dtype=torch.int64, device=self.b.device)
+            pairs = pairs.to(self._cdev)
+            sc = torch.tensor(splits, dtype=torch.int64, device=self._cdev)
             rc = torch.empty_like(sc)
             self.dist.all_to_all_single(rc, sc)
             recv_splits = rc.tolist()
-            recv = torch.empty(sum(recv_splits), dtype=torch.int64, device=self.b.device)
+            recv = torch.empty(sum(recv_splits), dtype=torch.int64, device=self._cdev)
             self.dist.all_to_all_single(recv, pairs, recv_splits, list(splits))
-            self.b.scatter_pairs(recv)
+            self.b.scatter_pairs(recv.to(self.b.device))
             return "sparse"
         self._reduce_slices(op)
         self.b.dense_exchanged()
@@ -132,15 +200,16 @@ class PartitionedRun:
 
     def _allreduce_counts(self, c: StepCounts) -> StepCounts:
         t = torch.tensor([c.recipients, c.broadcasts, c.senders, c.edges],
-                         dtype=torch.int64, device=self.b.device)
+                         dtype=torch.int64, device=self._cdev)
+        self._coll_sync()
         self.dist.all_reduce(t)
-        d = torch.tensor([c.dangling], dtype=torch.float64, device=self.b.device)
+        d = torch.tensor([c.dangling], dtype=torch.float64, device=self._cdev)
         self.dist.all_reduce(d)
         v = t.tolist()
         return StepCounts(v[0], v[1], v[2], v[3], float(d.item()))
 
     def _gather_values(self):
-        local = self.b.values()
+        local = self.b.values().to(self._cdev)
         sizes = np.diff(self.bounds)
         mx = int(sizes.max())
         pad = torch.zeros(mx, dtype=local.dtype, device=local.device)
@@ -154,7 +223,10 @@ class PartitionedRun:
     def run_min(self, app: str, source: int, max_steps: int):
         op = self.dist.ReduceOp.MIN
         n = self.n
+        peer = self._peer_setup()
         self.b.init_min(app, self.lo, self.hi)
+        if peer:  # every mailbox is neutral before any peer combines into it
+            self._fence()
         stats = []
         if app == "sssp":
             own = self.lo <= source < self.hi
@@ -173,7 +245,11 @@ class PartitionedRun:
             self.b.reset_mailbox()
             self.b.scatter_min(dense=(app == "components" and s == 0),
                                id_offset=self.lo)
-            exchange = self._exchange_min(op)
+            if peer:
+                self._fence()
+                exchange = "peer"
+            else:
+                exchange = self._exchange_min(op)
             at_cap = s + 1 == max_steps
             local = self.b.apply_min(app, count_only=at_cap)
             nxt = self._allreduce_counts(local)
@@ -201,7 +277,7 @@ class PartitionedRun:
         r0 = 1.0 / n                    # algorithms.py:50
         last = iterations - 1
         ndangling = self.b.init_pagerank(self.lo, self.hi, r0)
-        t = torch.tensor([ndangling], dtype=torch.int64, device=self.b.device)
+        t = torch.tensor([ndangling], dtype=torch.int64, device=self._cdev)
         self.dist.all_reduce(t)
         ndangling = int(t.item())
         dangling = r0 * ndangling       # algorithms.py:55
@@ -216,7 +292,7 @@ class PartitionedRun:
             self.b.scatter_sum()
             self._reduce_slices(op)
             local_d = self.b.apply_pagerank(base, damping, dangling / n, s == last)
-            d = torch.tensor([local_d], dtype=torch.float64, device=self.b.device)
+            d = torch.tensor([local_d], dtype=torch.float64, device=self._cdev)
             self.dist.all_reduce(d)
             dangling = float(d.item())
             stats.append(dict(index=s, active_count=n,
@@ -232,6 +308,30 @@ class PartitionedRun:
 # ----------------------------------------------------------------------
 # CUDA backend (libpgx phase kernels on this rank's GPU)
 # ----------------------------------------------------------------------
+
+class _DeviceArray:
+    """``__cuda_array_interface__`` of a raw device allocation (zero-copy
+    torch view)."""
+
+    def __init__(self, ptr: int, n: int, typestr: str):
+        self.__cuda_array_interface__ = {"shape": (n,), "typestr": typestr,
+                                         "data": (ptr, False), "version": 2,
+                                         "strides": None}
+
+
+class PeerMailbox:
+    """A rank's full-width min mailbox in a ``cudaMalloc`` block that the
+    other ranks map through CUDA IPC (pgx_peer_alloc)."""
+
+    def __init__(self, _lib, lib, n: int, device):
+        ptr = ctypes.c_void_p()
+        handle = ctypes.create_string_buffer(_lib.PGX_IPC_HANDLE_BYTES)
+        _lib.check(lib.pgx_peer_alloc(4 * max(n, 1), ctypes.byref(ptr), handle),
+                   "pgx_peer_alloc")
+        self.ptr = int(ptr.value)
+        self.handle = handle.raw
+        self.tensor = torch.as_tensor(_DeviceArray(self.ptr, n, "<i4"), device=device)
+
 
 class CudaBackend:
     """Owns the rank's local CSR, full-width mailbox and owned-slice state."""
@@ -285,8 +385,19 @@ class CudaBackend:
         self.tscratch = torch.empty(sb, dtype=torch.uint8, device=dev)
         self.tcount = torch.zeros(1, dtype=torch.int64, device=dev)
         self._full_reset = True
+        # fused peer exchange state (PartitionedRun._peer_setup)
+        self.peer_active = False
+        self._peer_mb = None
+        self._peer_sig = None
+        self._opened = []
 
     # ---- helpers ----
+    def _nnz(self) -> int:
+        """Senders with out-degree > 0 (graph workspace header; read once)."""
+        if getattr(self, "_nnz_cache", None) is None:
+            self._nnz_cache = int(self._g_hdr[0]) if self.len > 0 else 0
+        return self._nnz_cache
+
     def global_out_degree(self, v: int) -> int:
         return int(self.glob_deg[v])
 
@@ -299,10 +410,59 @@ class CudaBackend:
         return c, d
 
     # ---- min programs ----
+    # ---- fused peer exchange ----
+    def peer_handle(self):
+        """This rank's mappable mailbox (allocated once), or None."""
+        try:
+            if self._peer_mb is None:
+                self._peer_mb = PeerMailbox(self._lib, self.lib, self.n, self.device)
+        except Exception:
+            return None
+        return {"pid": os.getpid(), "ptr": self._peer_mb.ptr, "handle": self._peer_mb.handle}
+
+    def close_peers(self):
+        for p in self._opened:
+            self.lib.pgx_peer_close(ctypes.c_void_p(p))
+        self._opened = []
+        self._peer_sig = None
+
+    def open_peers(self, handles, bounds) -> bool:
+        """Device array of every rank's mailbox base (IPC-mapped, or the raw
+        pointer for ranks that are threads of this process)."""
+        sig = tuple((h["pid"], h["ptr"]) for h in handles)
+        if sig == self._peer_sig:
+            return True
+        self.close_peers()
+        ptrs = []
+        try:
+            for h in handles:
+                if h["pid"] == os.getpid():
+                    ptrs.append(h["ptr"])
+                    continue
+                p = ctypes.c_void_p()
+                self._lib.check(self.lib.pgx_peer_open(h["handle"], ctypes.byref(p)),
+                                "pgx_peer_open")
+                self._opened.append(int(p.value))
+                ptrs.append(int(p.value))
+        except Exception:
+            self.close_peers()
+            return False
+        self._peer_ptrs = torch.tensor(ptrs, dtype=torch.int64, device=self.device)
+        self._bounds32 = torch.tensor(np.asarray(bounds), dtype=torch.int32, device=self.device)
+        self._world = len(handles)
+        self._peer_sig = sig
+        return True
+
     def init_min(self, app, lo, hi):
         self.app = app
         self.lo = lo
-        self.mailbox = torch.empty(self.n, dtype=torch.int32, device=self.device)
+        if self.peer_active:
+            self.mailbox = self._peer_mb.tensor
+        else:
+            self.mailbox = torch.empty(self.n, dtype=torch.int32, device=self.device)
+        self.mailbox.fill_(EXCHANGE_NEUTRAL)
+        self.has.zero_()
+        self._full_reset = False
         self.val = torch.empty(max(self.len, 1), dtype=torch.int32, device=self.device)
         app_id = self._lib.PGX_APP_CC if app == "components" else self._lib.PGX_APP_SSSP
         self._lib.check(self.lib.pgx_slice_init(app_id, self.len, lo, self.val.data_ptr(),
@@ -325,6 +485,11 @@ class CudaBackend:
     def reset_mailbox(self):
         if self.app == "pagerank":
             self.mailbox.zero_()
+            return
+        if self.peer_active:  # foreign filter copies back to neutral, bits cleared
+            self._lib.check(self.lib.pgx_reset_touched(
+                self.n, self.lo_own, self.hi_own, self.has.data_ptr(), self.mailbox.data_ptr(),
+                EXCHANGE_NEUTRAL, self.stream.cuda_stream), "pgx_reset_touched")
             return
         # after a sparse exchange the foreign touched slots were reset by the
         # compaction and the own slice by the apply; after a dense one every
@@ -366,8 +531,22 @@ class CudaBackend:
     def scatter_min(self, dense: bool, id_offset: int):
         L, st = self.lib, self.stream.cuda_stream
         op = self._lib.PGX_OP_MIN_U32
+        if self.peer_active:
+            if dense:
+                src = (self._g_nz_eb.data_ptr(), None, self._g_nz_id.data_ptr(), id_offset, None,
+                       self._g_tile.data_ptr(), self._nnz(), self.m_local)
+            else:
+                src = (self.f_eb.data_ptr(), self.f_rs.data_ptr(), None, 0,
+                       self.f_msg.data_ptr(), self.f_tile.data_ptr(), self.nsrc, self.E)
+            rc = L.pgx_scatter_peer(int(dense), self.col.data_ptr(), *src,
+                                    self.mailbox.data_ptr(), self.has.data_ptr(),
+                                    EXCHANGE_NEUTRAL, self._peer_ptrs.data_ptr(),
+                                    self._bounds32.data_ptr(), self._world, self.lo_own,
+                                    self.hi_own, st)
+            self._lib.check(rc, "pgx_scatter_peer")
+            return
         if dense:
-            nnz = int(self._g_hdr[0])
+            nnz = self._nnz()
             rc = L.pgx_scatter(op, 1, self.col.data_ptr(), self._g_nz_eb.data_ptr(), None,
                                self._g_nz_id.data_ptr(), id_offset, None,
                                self._g_tile.data_ptr(), nnz, self.m_local,
@@ -412,7 +591,7 @@ class CudaBackend:
         return int((deg == 0).sum())
 
     def scatter_sum(self):
-        nnz = int(self._g_hdr[0])
+        nnz = self._nnz()
         self._lib.check(self.lib.pgx_scatter(
             self._lib.PGX_OP_SUM_F64, 1, self.col.data_ptr(), self._g_nz_eb.data_ptr(), None,
             self._g_nz_id.data_ptr(), 0, self.share.data_ptr(), self._g_tile.data_ptr(), nnz,
@@ -448,6 +627,7 @@ def run_partitioned(graph, program, low, config, dist):
         cached = graph._device[key] = (bounds, backend)
     bounds, backend = cached
     runner = PartitionedRun(backend, dist, bounds, n, m)
+    runner.exchange = os.environ.get("PGX_EXCHANGE", "auto")
     app = low["app"]
     if app == "pagerank":
         vals, stats, cap, wall = runner.run_pagerank(low["iterations"], low["damping"],
@@ -463,4 +643,5 @@ def run_partitioned(graph, program, low, config, dist):
         from types import SimpleNamespace
         values = program.extract(SimpleNamespace(state=values,
                                                  halted=np.ones(values.shape[0], bool)))
-    return RunReport(values, len(steps), steps, wall, cap, device_values=vals)
+    return RunReport(values, len(steps), steps, wall, cap, device_values=vals,
+                     exchanges=[s.get("exchange", "dense") for s in stats])

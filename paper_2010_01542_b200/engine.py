@@ -107,6 +107,7 @@ class RunReport:
     device_values: Any = None      # torch tensor on the device (u32 / f64)
     device_seconds: float = 0.0    # kernel time from the device timer
     ctas: int = 0                  # persistent CTAs of the run kernel
+    exchanges: Any = None          # partitioned runs: mailbox exchange per superstep
 
 
 class VertexContext:

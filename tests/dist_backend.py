@@ -1,13 +1,21 @@
 """CPU stand-in for CudaBackend -- TEST INFRASTRUCTURE ONLY.
 
 Mirrors the semantics of libpgx's phase kernels (pgx_scatter,
-pgx_apply_slice, pgx_pr_apply_slice) with numpy on CPU torch tensors, so
-that the partitioned driver (paper_2010_01542_b200.distributed.
-PartitionedRun: partitioning, per-owner reductions, counter all-reduce,
-halt test, value gather) runs over a gloo process group without a GPU.
+pgx_scatter_peer, pgx_reset_touched, pgx_apply_slice, pgx_pr_apply_slice)
+with numpy on CPU torch tensors, so that the partitioned driver
+(paper_2010_01542_b200.distributed.PartitionedRun: partitioning, per-owner
+reductions, peer exchange, counter all-reduce, halt test, value gather)
+runs over a gloo process group without a GPU.  The peer exchange maps the
+ranks' mailboxes as shared-memory files (the stand-in for CUDA IPC); an
+flock per owner serialises the read-modify-write of its slice (the GPU's
+red.min is atomic).
 """
 
 from __future__ import annotations
+
+import fcntl
+import os
+import tempfile
 
 import numpy as np
 import torch
@@ -29,6 +37,39 @@ class CpuBackend:
         self.front = (np.empty(0, np.int64), np.empty(0, np.int64))  # (local ids, msgs)
         self.has = np.zeros(self.n, bool)
         self._full_reset = True
+        self.peer_active = False
+        self._shm = None
+        self._peers = None
+
+    # ---- peer exchange (shared-memory stand-in for CUDA IPC) ----
+    def peer_handle(self):
+        if self._shm is None:
+            fd, path = tempfile.mkstemp(prefix="pgx_peer_", dir="/dev/shm"
+                                        if os.path.isdir("/dev/shm") else None)
+            os.close(fd)
+            self._shm = (path, np.memmap(path, dtype=np.int32, mode="w+",
+                                         shape=(max(self.n, 1),)))
+        return {"pid": os.getpid(), "path": self._shm[0]}
+
+    def open_peers(self, handles, bounds):
+        self._peers = [np.memmap(h["path"], dtype=np.int32, mode="r+", shape=(max(self.n, 1),))
+                       for h in handles]
+        self._locks = [open(h["path"], "rb") for h in handles]
+        self._bounds = np.asarray(bounds, np.int64)
+        self._me = [h["path"] for h in handles].index(self._shm[0])
+        return True
+
+    def _locked_min(self, owner, dst, m):
+        fcntl.flock(self._locks[owner], fcntl.LOCK_EX)
+        try:
+            np.minimum.at(self._peers[owner], dst, m)
+        finally:
+            fcntl.flock(self._locks[owner], fcntl.LOCK_UN)
+
+    def close(self):
+        if self._shm is not None:
+            os.unlink(self._shm[0])
+            self._shm = None
 
     def global_out_degree(self, v):
         return int(self.glob_deg[v])
@@ -47,7 +88,13 @@ class CpuBackend:
     # ---- min programs ----
     def init_min(self, app, lo, hi):
         self.app = app
-        self.mailbox = torch.full((self.n,), EXCHANGE_NEUTRAL, dtype=torch.int32)
+        if self.peer_active:
+            self.mailbox = torch.from_numpy(self._shm[1][:self.n])
+            self.mailbox.fill_(EXCHANGE_NEUTRAL)
+        else:
+            self.mailbox = torch.full((self.n,), EXCHANGE_NEUTRAL, dtype=torch.int32)
+        self.has[:] = False
+        self._full_reset = False
         if app == "components":
             self.val = np.arange(lo, hi, dtype=np.int64)
         else:
@@ -62,6 +109,10 @@ class CpuBackend:
     def reset_mailbox(self):
         if self.app == "pagerank":
             self.mailbox.zero_()
+            return
+        if self.peer_active:  # pgx_reset_touched
+            self.mailbox.numpy()[self._foreign()] = EXCHANGE_NEUTRAL
+            self.has[:] = False
             return
         if self._full_reset:
             self.mailbox.fill_(EXCHANGE_NEUTRAL)
@@ -99,8 +150,21 @@ class CpuBackend:
         else:
             lv, msg = self.front
         dst, m = self._edges_of(lv, msg)
+        m = m.astype(np.int32)
         mb = self.mailbox.numpy()
-        np.minimum.at(mb, dst, m.astype(np.int32))
+        if not self.peer_active:
+            np.minimum.at(mb, dst, m)
+            self.has[dst] = True
+            return
+        # pgx_scatter_peer: own slots and every owner's slot under its lock,
+        # the local copies of foreign slots (this rank's filter) unlocked
+        foreign = (dst < self.lo) | (dst >= self.hi)
+        np.minimum.at(mb, dst[foreign], m[foreign])
+        self._locked_min(self._me, dst[~foreign], m[~foreign])
+        owner = np.searchsorted(self._bounds[1:-1], dst[foreign], side="right")
+        for o in np.unique(owner):
+            sel = owner == o
+            self._locked_min(int(o), dst[foreign][sel], m[foreign][sel])
         self.has[dst] = True
 
     def apply_min(self, app, count_only):

@@ -2,7 +2,9 @@
 
 The driver (paper_2010_01542_b200.distributed.PartitionedRun) is the one
 the CUDA backend uses under torchrun; here the per-rank phases run on the
-CPU test backend (tests/dist_backend.py).  Results must equal the oracle's
+CPU test backend (tests/dist_backend.py), for every mailbox exchange: the
+collective ones (dense reduction, sparse pairs, chosen per superstep) and
+the fused peer exchange (shared-memory mailboxes standing in for CUDA IPC).  Results must equal the oracle's
 (and therefore the reference's): CC labels / SSSP distances exact, per-
 superstep active and message counts exact, PageRank within 1e-9.
 """
@@ -31,7 +33,7 @@ def _free_port():
         return s.getsockname()[1]
 
 
-def _worker(rank, world, port, jobs, out_dir, sparse_ok=True):
+def _worker(rank, world, port, jobs, out_dir, exchange="hybrid"):
     import sys
     here = os.path.dirname(os.path.abspath(__file__))
     sys.path.insert(0, here)
@@ -40,12 +42,14 @@ def _worker(rank, world, port, jobs, out_dir, sparse_ok=True):
     dist.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{port}",
                             rank=rank, world_size=world)
     results = []
+    backends = []
     for (off, tgt, app, kw) in jobs:
         n = off.size - 1
         bounds = partition_bounds(np.diff(off), world)
         be = CpuBackend(off, tgt, int(bounds[rank]), int(bounds[rank + 1]))
+        backends.append(be)
         run = PartitionedRun(be, dist, bounds, n, int(tgt.size))
-        run.sparse_ok = sparse_ok
+        run.exchange = exchange
         cap = kw.get("max_supersteps", 10_000)
         if app == "pagerank":
             vals, stats, hit, _ = run.run_pagerank(kw.get("iterations", 10),
@@ -58,6 +62,8 @@ def _worker(rank, world, port, jobs, out_dir, sparse_ok=True):
     if rank == 0:
         torch.save(results, os.path.join(out_dir, "results.pt"))
     dist.barrier()
+    for be in backends:
+        be.close()
     dist.destroy_process_group()
 
 
@@ -88,10 +94,11 @@ def _expected(off, tgt, app, kw):
                           max_steps=cap)
 
 
-@pytest.mark.parametrize("world,sparse_ok", [(2, True), (3, True), (2, False)])
-def test_partitioned_run_matches_oracle(world, sparse_ok, tmp_path):
+@pytest.mark.parametrize("world,exchange", [(2, "hybrid"), (3, "hybrid"), (2, "dense"),
+                                            (2, "peer"), (3, "peer")])
+def test_partitioned_run_matches_oracle(world, exchange, tmp_path):
     jobs = _jobs()
-    mp.start_processes(_worker, args=(world, _free_port(), jobs, str(tmp_path), sparse_ok),
+    mp.start_processes(_worker, args=(world, _free_port(), jobs, str(tmp_path), exchange),
                        nprocs=world, start_method="spawn")
     results = torch.load(os.path.join(tmp_path, "results.pt"), weights_only=False)
     modes = set()
@@ -105,8 +112,10 @@ def test_partitioned_run_matches_oracle(world, sparse_ok, tmp_path):
         assert [a for a, _ in stats] == want.active_counts, (app, kw)
         assert [m for _, m in stats] == want.messages_sent, (app, kw)
         assert hit == want.hit_superstep_cap
-    # both exchanges ran (sparse on the late supersteps) unless disabled
-    assert modes == ({"dense", "sparse"} if sparse_ok else {"dense"})
+    # hybrid: both collective exchanges ran (sparse on the late supersteps);
+    # peer: the min programs never reduce the mailbox (PageRank records none)
+    assert modes == {"hybrid": {"dense", "sparse"}, "dense": {"dense"},
+                     "peer": {"peer"}}[exchange]
 
 
 def test_partition_bounds_edge_balanced():

@@ -2,7 +2,9 @@
 
 W ranks run as threads (tests/thread_dist.py) sharing cuda:0; each owns a
 CudaBackend (local CSR, full-width mailbox, owned slice) and the driver is
-the production PartitionedRun.  Results must equal the oracle's (CC / SSSP
+the production PartitionedRun, with each mailbox exchange: the fused peer
+scatter (pgx_scatter_peer combining straight into the owners' mailboxes),
+the per-superstep dense / sparse collectives, dense only.  Results must equal the oracle's (CC / SSSP
 exact with per-superstep counts, PageRank within 1e-9) for W = 1, 2, 4.
 """
 
@@ -22,7 +24,7 @@ SPECS = [O.RmatSpec(14, 8, .57, .19, .19, 31, True),
          O.RmatSpec(13, 16, .45, .22, .22, 32, False)]
 
 
-def _run(off, tgt, app, kw, world, sparse_ok=True):
+def _run(off, tgt, app, kw, world, exchange="auto"):
     n = off.size - 1
     g = pgx.from_csr(torch.from_numpy(off).cuda(), torch.from_numpy(tgt).cuda())
     bounds = partition_bounds(np.diff(off), world)
@@ -30,7 +32,7 @@ def _run(off, tgt, app, kw, world, sparse_ok=True):
     def rank_fn(r, d):
         be = CudaBackend(g, int(bounds[r]), int(bounds[r + 1]), "cuda:0")
         run = PartitionedRun(be, d, bounds, n, int(tgt.size))
-        run.sparse_ok = sparse_ok
+        run.exchange = exchange
         cap = kw.get("max_supersteps", 10_000)
         if app == "pagerank":
             return run.run_pagerank(10, 0.85, cap)
@@ -40,8 +42,8 @@ def _run(off, tgt, app, kw, world, sparse_ok=True):
 
 @pytest.mark.parametrize("world", [1, 2, 4])
 @pytest.mark.parametrize("spec", SPECS, ids=["sym", "dir"])
-@pytest.mark.parametrize("sparse_ok", [True, False], ids=["hybrid-exchange", "dense-exchange"])
-def test_partitioned_cuda_matches_oracle(spec, world, sparse_ok):
+@pytest.mark.parametrize("exchange", ["peer", "hybrid", "dense"])
+def test_partitioned_cuda_matches_oracle(spec, world, exchange):
     n, off, tgt = O.rmat_csr(spec)
     src = int(np.argmax(np.diff(off)))
     for app, kw, want in (
@@ -49,7 +51,7 @@ def test_partitioned_cuda_matches_oracle(spec, world, sparse_ok):
             ("sssp", {"source": src}, O.run_sssp(n, off, tgt, src)),
             ("components", {"max_supersteps": 2}, O.run_cc(n, off, tgt, max_steps=2)),
             ("pagerank", {}, O.run_pagerank(n, off, tgt))):
-        vals, stats, hit, _ = _run(off, tgt, app, kw, world, sparse_ok)
+        vals, stats, hit, _ = _run(off, tgt, app, kw, world, exchange)
         v = vals.cpu().numpy()
         if app == "pagerank":
             assert np.max(np.abs(v - want.values) / np.abs(want.values)) <= 1e-9
@@ -59,3 +61,6 @@ def test_partitioned_cuda_matches_oracle(spec, world, sparse_ok):
         assert [s["active_count"] for s in stats] == want.active_counts, (app, world)
         assert [s["messages_sent"] for s in stats] == want.messages_sent, (app, world)
         assert hit == want.hit_superstep_cap
+        if app != "pagerank":
+            used = {s["exchange"] for s in stats}
+            assert used <= ({"peer"} if exchange == "peer" else {"dense", "sparse"})

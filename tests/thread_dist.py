@@ -97,6 +97,18 @@ class ThreadDist:
         self._bar.wait()
 
 
+    def all_gather_object(self, out, obj):
+        r = self.get_rank()
+        self._slots[r] = obj
+        self._bar.wait()
+        for i in range(self.world):
+            out[i] = self._slots[i]
+        self._bar.wait()
+
+    def barrier(self):
+        self._bar.wait()
+
+
 def run_ranks(world, fn):
     """Run fn(rank, dist) on `world` threads; returns the per-rank results."""
     d = ThreadDist(world)
