@@ -198,6 +198,19 @@ class PartitionedRun:
         self.b.dense_exchanged()
         return "dense"
 
+    def _gather_counts(self, local: torch.Tensor) -> StepCounts:
+        """Every rank's (recipients, broadcasts, senders, edges) in ONE
+        all-gather and one host read: the sums drive the halt test and the
+        statistics, the rank's own senders / edges size its next scatter."""
+        local = local.to(device=self._cdev, dtype=torch.int64)
+        parts = [torch.empty_like(local) for _ in range(self.world)]
+        self._coll_sync()
+        self.dist.all_gather(parts, local)
+        rows = torch.stack(parts).tolist()
+        self.b.set_frontier(rows[self.rank][2], rows[self.rank][3])
+        tot = [sum(r[i] for r in rows) for i in range(4)]
+        return StepCounts(*tot)
+
     def _allreduce_counts(self, c: StepCounts) -> StepCounts:
         t = torch.tensor([c.recipients, c.broadcasts, c.senders, c.edges],
                          dtype=torch.int64, device=self._cdev)
@@ -251,8 +264,7 @@ class PartitionedRun:
             else:
                 exchange = self._exchange_min(op)
             at_cap = s + 1 == max_steps
-            local = self.b.apply_min(app, count_only=at_cap)
-            nxt = self._allreduce_counts(local)
+            nxt = self._gather_counts(self.b.apply_min(app, count_only=at_cap))
             sent = cur.edges if app == "sssp" else cur.broadcasts
             stats.append(dict(index=s, active_count=active,
                               messages_sent=sent, edges=cur.edges,
@@ -560,7 +572,9 @@ class CudaBackend:
                                EXCHANGE_NEUTRAL, st)
         self._lib.check(rc, "pgx_scatter")
 
-    def apply_min(self, app, count_only: bool) -> StepCounts:
+    def apply_min(self, app, count_only: bool) -> torch.Tensor:
+        """K2 on the owned slice; returns the device vector (recipients,
+        broadcasts, senders, edges) -- no host synchronisation."""
         self.ctr.zero_()
         app_id = self._lib.PGX_APP_CC if app == "components" else self._lib.PGX_APP_SSSP
         sl = self.mailbox[self.lo:self.lo + self.len]
@@ -569,10 +583,12 @@ class CudaBackend:
             self.f_eb.data_ptr(), self.f_rs.data_ptr(), self.f_msg.data_ptr(),
             self.f_tile.data_ptr(), self.ctr.data_ptr(), int(count_only), EXCHANGE_NEUTRAL,
             self.stream.cuda_stream), "pgx_apply_slice")
-        c, _ = self._counters()
-        packed = c[0] & 0xFFFFFFFFFFFFFFFF
-        self.nsrc, self.E = packed >> 32, packed & 0xFFFFFFFF
-        return StepCounts(c[1], c[2], self.nsrc, self.E)
+        c = self.ctr[:24].view(torch.int64)  # packed, recip, bcast
+        packed = c[0]
+        return torch.stack([c[1], c[2], packed >> 32, packed & 0xFFFFFFFF])
+
+    def set_frontier(self, senders: int, edges: int):
+        self.nsrc, self.E = int(senders), int(edges)
 
     # ---- PageRank ----
     def init_pagerank(self, lo, hi, r0) -> int:

@@ -20,7 +20,7 @@ import tempfile
 import numpy as np
 import torch
 
-from paper_2010_01542_b200.distributed import EXCHANGE_NEUTRAL, StepCounts
+from paper_2010_01542_b200.distributed import EXCHANGE_NEUTRAL
 
 
 class CpuBackend:
@@ -172,14 +172,18 @@ class CpuBackend:
         has = sl != EXCHANGE_NEUTRAL
         rec = int(has.sum())
         if count_only:
-            return StepCounts(rec, 0, 0, 0)
+            return torch.tensor([rec, 0, 0, 0], dtype=torch.int64)
         self.mailbox.numpy()[self.lo:self.hi] = EXCHANGE_NEUTRAL
         imp = has & (sl < self.val)
         self.val[imp] = sl[imp]
         lv = np.flatnonzero(imp & (self.deg > 0))
         msg = sl[lv] + (1 if app == "sssp" else 0)
         self.front = (lv, msg)
-        return StepCounts(rec, int(imp.sum()), int(lv.size), int(self.deg[lv].sum()))
+        return torch.tensor([rec, int(imp.sum()), int(lv.size), int(self.deg[lv].sum())],
+                            dtype=torch.int64)
+
+    def set_frontier(self, senders, edges):
+        pass  # the CPU stand-in keeps its frontier as arrays
 
     # ---- PageRank ----
     def init_pagerank(self, lo, hi, r0):
