@@ -135,17 +135,36 @@ struct GridBarrier {
   unsigned gen;
 };
 
+// Two arrival schemes, chosen per kernel by measurement:
+//   kArriveRed: a monotonic arrival counter (zeroed before every launch);
+//     every CTA arrives with one fire-and-forget red.release and polls
+//     with ld.acquire until the whole generation arrived -- no atomic
+//     return value and no last-arriver hop on the critical path (CC / SSSP:
+//     C2 -2 %, C3 -2 %);
+//   kArriveAtomic: atomicAdd with return, the last arriver flips `gen`
+//     (PageRank: C4 is 0.7 % faster with it).
+enum BarrierKind { kArriveAtomic = 0, kArriveRed = 1 };
+
+template <int KIND = kArriveAtomic>
 __device__ __forceinline__ void grid_sync(GridBarrier *bar, unsigned &gen) {
   __syncthreads();
   if (threadIdx.x == 0) {
     __threadfence();
-    unsigned arrived = atomicAdd(&bar->count, 1u);
-    if (arrived == gridDim.x - 1) {
-      bar->count = 0;
-      __threadfence();
-      atomicExch(&bar->gen, gen + 1);
+    if (KIND == kArriveRed) {
+      const unsigned target = (gen + 1) * gridDim.x;
+      asm volatile("red.release.gpu.global.add.u32 [%0], %1;" ::"l"(&bar->count), "r"(1u)
+                   : "memory");
+      while (ld_acquire(&bar->count) < target) {
+      }
     } else {
-      while (ld_acquire(&bar->gen) == gen) {
+      const unsigned arrived = atomicAdd(&bar->count, 1u);
+      if (arrived == gridDim.x - 1) {
+        bar->count = 0;
+        __threadfence();
+        atomicExch(&bar->gen, gen + 1);
+      } else {
+        while (ld_acquire(&bar->gen) == gen) {
+        }
       }
     }
     __threadfence();

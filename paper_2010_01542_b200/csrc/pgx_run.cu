@@ -99,7 +99,7 @@ __global__ void __launch_bounds__(kBlock, PGX_MIN_BLOCKS) min_run_kernel(MinRunP
       p.ws.ctr[0].bcast = (unsigned)p.n;  // every vertex broadcasts its id
     }
   }
-  grid_sync(p.ws.bar, gen);
+  grid_sync<kArriveRed>(p.ws.bar, gen);
   if (APP == PGX_APP_SSSP && gtid == 0) *slot<S>(val, p.source) = 0u;
   if (gtid == 0) p.stats[PGX_STAT_HDR + 7] = (int64_t)globaltimer();
 
@@ -144,7 +144,7 @@ __global__ void __launch_bounds__(kBlock, PGX_MIN_BLOCKS) min_run_kernel(MinRunP
       StepCounters z = {};
       p.ws.ctr[s + 1] = z;
     }
-    grid_sync(p.ws.bar, gen);
+    grid_sync<kArriveRed>(p.ws.bar, gen);
     const uint64_t t_scatter = globaltimer();
 
     // ---- apply(s+1): consume + compute + frontier build; at the cap the
@@ -158,7 +158,7 @@ __global__ void __launch_bounds__(kBlock, PGX_MIN_BLOCKS) min_run_kernel(MinRunP
       if (bc) atomicAdd(&p.ws.ctr[s + 1].bcast, bc);
       if (rc) atomicAdd(&p.ws.ctr[s].recip, rc);
     }
-    grid_sync(p.ws.bar, gen);
+    grid_sync<kArriveRed>(p.ws.bar, gen);
 
     // ---- stats + halt test (engine.py:284-300) ----
     const unsigned nrecip = p.ws.ctr[s].recip;
