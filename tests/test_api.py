@@ -1,6 +1,8 @@
 """Host-side mirror of the pregelite API (CPU): graph construction
 semantics, cache format, partition rule, program validation, lowering."""
 
+import os
+
 import numpy as np
 import pytest
 import torch
@@ -140,3 +142,52 @@ def test_empty_graph_runs_without_device():
     assert r.values.dtype == np.int64
     with pytest.raises(pgx.ConfigError):
         pgx.run(e, pgx.sssp(0))
+
+
+GOLDEN = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden")
+
+
+def _reference_caches():
+    import json
+    return json.load(open(os.path.join(GOLDEN, "reference_cache.json")))["graphs"]
+
+
+@pytest.mark.parametrize("name", sorted(_reference_caches()))
+def test_cache_files_written_by_the_reference(name, tmp_path):
+    """load_cache reads pregelite's own snapshots (graph.py:298-373) and
+    save_cache writes them back byte for byte."""
+    want = _reference_caches()[name]
+    path = os.path.join(GOLDEN, f"reference_cache_{name}.pglcsr")
+    g = pgx.load_cache(path)
+    assert g.vertex_count == want["n"] and g.edge_count == want["m"]
+    assert g.out_offsets.tolist() == want["out_offsets"]
+    assert g.out_targets.tolist() == want["out_targets"]
+    assert g.in_offsets.tolist() == want["in_offsets"]
+    assert g.in_targets.tolist() == want["in_targets"]
+    assert str(g.out_targets.cpu().numpy().dtype) == want["id_dtype"]
+    if want["id_map"] is None:
+        assert g.id_map is None
+    else:
+        assert list(g.id_map) == want["id_map"]
+    out = tmp_path / "again.pglcsr"
+    pgx.save_cache(g, out)
+    assert out.read_bytes() == open(path, "rb").read()
+
+
+def test_cache_of_our_graphs_matches_the_reference_bytes(tmp_path):
+    """The same graphs built with this package's from_edges / load_edge_list
+    serialise to the reference's exact bytes."""
+    ours = {
+        "dup_loops_d": pgx.from_edges([0, 0, 0, 1, 2, 2, 4], [0, 1, 1, 2, 2, 0, 1], 5),
+        "tri_tail_u": pgx.from_edges([0, 1, 2, 3], [1, 2, 0, 4], 6, undirected=True),
+        "ids64_d": pgx.from_edges([3, 1, 2, 0], [0, 0, 3, 2], 4, id_dtype=np.int64),
+        "empty3": pgx.from_edges([], [], 3),
+    }
+    el = tmp_path / "edges.txt"
+    el.write_text("# sparse ids\n1000 7\n7 42\n42 1000\n99 7\n")
+    ours["edgelist_idmap_u"] = pgx.load_edge_list(str(el), undirected=True)
+    for name, g in ours.items():
+        out = tmp_path / f"{name}.pglcsr"
+        pgx.save_cache(g, out)
+        ref = open(os.path.join(GOLDEN, f"reference_cache_{name}.pglcsr"), "rb").read()
+        assert out.read_bytes() == ref, name
