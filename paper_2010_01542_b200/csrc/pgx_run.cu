@@ -303,6 +303,11 @@ __global__ void __launch_bounds__(kBlock, PGX_MIN_BLOCKS) pagerank_run_kernel(Pr
   }
 }
 
+#ifndef PGX_PR_UNROLL
+#define PGX_PR_UNROLL 2
+#endif
+constexpr int kPrUnroll = PGX_PR_UNROLL;
+
 struct PrPullParams {
   int32_t n;
   int64_t m;
@@ -375,25 +380,45 @@ __global__ void __launch_bounds__(kBlock, PGX_MIN_BLOCKS) pagerank_pull_kernel(P
     const uint64_t t_fold = globaltimer();
 
     // ---- compute (algorithms.py:61-73): rank, next share, dangling mass
+    // kPrUnroll vertices per thread and iteration, every load independent
+    // (folded[v] is read unconditionally), so a thread keeps 5 * kPrUnroll
+    // loads in flight instead of one dependent chain per vertex
     const double dn = __ddiv_rn(dangling, dn_n);
     double my_d = 0.0;
-    for (unsigned v = gtid; v < (unsigned)p.n; v += nthreads) {
-      const int es = p.in_row_ptr[v], ee = p.in_row_ptr[v + 1];
-      double f = 0.0;
-      if (ee > es) {
-        const int64_t t0 = es / kTile, t1 = (ee - 1) / kTile;
-        if (t0 == t1) {
-          f = folded[v];
-        } else {
-          f = p.ws.tail[t0];
-          for (int64_t t = t0 + 1; t <= t1; t++) f = __dadd_rn(f, p.ws.head[t]);
+    for (unsigned v0 = gtid; v0 < (unsigned)p.n; v0 += kPrUnroll * nthreads) {
+      int es[kPrUnroll], ee[kPrUnroll], r0[kPrUnroll], r1[kPrUnroll];
+      double fv[kPrUnroll];
+#pragma unroll
+      for (int j = 0; j < kPrUnroll; j++) {
+        const unsigned v = v0 + j * nthreads;
+        if (v < (unsigned)p.n) {
+          es[j] = p.in_row_ptr[v];
+          ee[j] = p.in_row_ptr[v + 1];
+          r0[j] = p.row_ptr[v];
+          r1[j] = p.row_ptr[v + 1];
+          fv[j] = folded[v];
         }
       }
-      const double r = __dadd_rn(p.base, __dmul_rn(p.damping, __dadd_rn(f, dn)));
-      p.rank[v] = r;
-      const int deg = p.row_ptr[v + 1] - p.row_ptr[v];
-      if (deg == 0) my_d = __dadd_rn(my_d, r);
-      else if (s != last) share_nxt[v] = __ddiv_rn(r, (double)deg);
+#pragma unroll
+      for (int j = 0; j < kPrUnroll; j++) {
+        const unsigned v = v0 + j * nthreads;
+        if (v >= (unsigned)p.n) continue;
+        double f = 0.0;
+        if (ee[j] > es[j]) {
+          const int64_t t0 = es[j] / kTile, t1 = (ee[j] - 1) / kTile;
+          if (t0 == t1) {
+            f = fv[j];
+          } else {
+            f = p.ws.tail[t0];
+            for (int64_t t = t0 + 1; t <= t1; t++) f = __dadd_rn(f, p.ws.head[t]);
+          }
+        }
+        const double r = __dadd_rn(p.base, __dmul_rn(p.damping, __dadd_rn(f, dn)));
+        p.rank[v] = r;
+        const int deg = r1[j] - r0[j];
+        if (deg == 0) my_d = __dadd_rn(my_d, r);
+        else if (s != last) share_nxt[v] = __ddiv_rn(r, (double)deg);
+      }
     }
     const double bsum = block_sum<double>(my_d, s_red);
     if (threadIdx.x == 0) p.ws.partials[blockIdx.x] = bsum;
