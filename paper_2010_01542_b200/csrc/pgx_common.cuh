@@ -19,6 +19,9 @@
 #ifndef PGX_MIN_BLOCKS
 #define PGX_MIN_BLOCKS 2     // persistent CTAs of 512 threads per SM (64 regs)
 #endif
+#ifndef PGX_PREFETCH
+#define PGX_PREFETCH 1       // dense scatter: L2 bulk prefetch of the next tile's ids
+#endif
 #ifndef PGX_PASS
 #define PGX_PASS 4           // 32-edge rounds in flight per scatter pass
 #endif

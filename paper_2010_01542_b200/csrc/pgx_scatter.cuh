@@ -53,6 +53,17 @@ __device__ void scatter_phase(const ScatterArgs &a, char *smem, bool read_filter
   for (int64_t t = gwarp; t < ntiles; t += nwarps) {
     const int64_t e0 = t * kTile;
     const int64_t e1 = min(a.E, e0 + kTile);
+#if PGX_PREFETCH
+    // the warp's next tile: its neighbour ids (dense: one contiguous 1 KB
+    // run of col_idx) are pulled into L2 while this tile is processed
+    if (kDense && lane == 0 && t + nwarps < ntiles) {
+      const int64_t en = (t + nwarps) * kTile;
+      const int bytes = (int)(min(a.E - en, (int64_t)kTile) * 4) & ~15;
+      if (bytes > 0)
+        asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(a.col + en), "r"(bytes)
+                     : "memory");
+    }
+#endif
     const int i0 = a.tile_src[t];
     const int i1 = (t + 1 < ntiles) ? a.tile_src[t + 1] : a.nsrc - 1;
     const int k = i1 - i0 + 1;  // <= kTile + 1
