@@ -50,6 +50,7 @@ from __future__ import annotations
 import ctypes
 import os
 import time
+import weakref
 from dataclasses import dataclass
 
 import numpy as np
@@ -343,6 +344,8 @@ class PeerMailbox:
         self.ptr = int(ptr.value)
         self.handle = handle.raw
         self.tensor = torch.as_tensor(_DeviceArray(self.ptr, n, "<i4"), device=device)
+        # freed with its owner (the backend drops it only after its last run)
+        weakref.finalize(self, lib.pgx_peer_free, ctypes.c_void_p(self.ptr))
 
 
 class CudaBackend:
@@ -402,6 +405,14 @@ class CudaBackend:
         self._peer_mb = None
         self._peer_sig = None
         self._opened = []
+        # peer mappings are closed when the backend goes away
+        weakref.finalize(self, CudaBackend._close_all, self.lib, self._opened)
+
+    @staticmethod
+    def _close_all(lib, opened):
+        for p in opened:
+            lib.pgx_peer_close(ctypes.c_void_p(p))
+        opened.clear()
 
     # ---- helpers ----
     def _nnz(self) -> int:
@@ -433,9 +444,7 @@ class CudaBackend:
         return {"pid": os.getpid(), "ptr": self._peer_mb.ptr, "handle": self._peer_mb.handle}
 
     def close_peers(self):
-        for p in self._opened:
-            self.lib.pgx_peer_close(ctypes.c_void_p(p))
-        self._opened = []
+        CudaBackend._close_all(self.lib, self._opened)  # in place: the finalizer's list
         self._peer_sig = None
 
     def open_peers(self, handles, bounds) -> bool:
