@@ -53,15 +53,35 @@ def measured_peaks():
 # algorithmic bytes (BASELINE.md section 2 / SURVEY.md 8(d))
 # ----------------------------------------------------------------------
 
-def algorithmic_bytes(app: str, n: int, m: int, steps) -> int:
+def algorithmic_bytes_per_step(app: str, n: int, m: int, steps) -> list:
+    """PR 12m + 48n per superstep; CC / SSSP
+    16 #F_s + 8 E_s + 12 R_s + 8 #F_{s+1} + n/4."""
     if app == "pagerank":
-        return len(steps) * (12 * m + 48 * n)
-    total = 0
+        return [12 * m + 48 * n] * len(steps)
+    out = []
     for s, st in enumerate(steps):
         f_next = steps[s + 1].broadcasters if s + 1 < len(steps) else 0
-        total += 16 * st.broadcasters + 8 * st.edges + 12 * st.recipients \
-            + 8 * f_next + n // 4
-    return total
+        out.append(16 * st.broadcasters + 8 * st.edges + 12 * st.recipients
+                   + 8 * f_next + n // 4)
+    return out
+
+
+def algorithmic_bytes(app: str, n: int, m: int, steps) -> int:
+    return sum(algorithmic_bytes_per_step(app, n, m, steps))
+
+
+def superstep_aggregate(app, n, m, rep, peak):
+    """SURVEY 8(d)'s first figure: sum_s B_s / sum_s t_s, t_s the device time
+    of superstep s (%globaltimer stamps of the persistent kernel), next to
+    the loop figure (B_total / kernel time) that `roofline` reports."""
+    b = algorithmic_bytes_per_step(app, n, m, step_views(app, rep))
+    t = [s.seconds for s in rep.supersteps]
+    gbs = sum(b) / sum(t) / 1e9 if sum(t) > 0 else 0.0
+    return {"achieved": round(gbs, 1), "unit": "GB/s", "peak": peak,
+            "frac": round(gbs / peak, 4),
+            "per_superstep": [{"s": i, "edges": st.edges, "us": round(ts * 1e6, 1),
+                               "GBps": round(bs / ts / 1e9, 1) if ts > 0 else None}
+                              for i, (st, ts, bs) in enumerate(zip(rep.supersteps, t, b))]}
 
 
 class StepView:
@@ -334,6 +354,7 @@ def bench_gpu(args):
                      "frac_of_8TBs": round(achieved / HBM_NORTH_STAR_GBS, 4),
                      "alg_bytes_per_step": alg_bytes,
                      "kernel": "min_run_kernel / pagerank_run_kernel (persistent)"},
+        "superstep_aggregate": superstep_aggregate(app, n, m, rep, peak),
         "scattered_roofline": {
             "bound": "random 4/8-byte L2 accesses (>= 1 per edge)",
             "achieved": round(value / world, 2), "peak": ceiling, "unit": "G accesses/s",
