@@ -33,6 +33,9 @@ from . import _lib
 from .errors import GraphLoadError
 
 _CACHE_MAGIC = b"PGLCSR1\n"
+_LITTLE = np.little_endian
+_TORCH_OF = {np.dtype(np.int64): torch.int64, np.dtype(np.int32): torch.int32,
+             np.dtype(np.int16): torch.int16}
 
 
 def _as_tensor(a, dtype=torch.int64, device=None) -> torch.Tensor:
@@ -439,47 +442,66 @@ def save_cache(graph: Graph, path) -> None:
     os.replace(tmp, path)
 
 
-def load_cache(path) -> Graph:
-    """graph.py:325-373: read and validate a PGLCSR1 snapshot."""
+def load_cache(path, *, device=None, pin_memory: bool = False) -> Graph:
+    """graph.py:325-373: read and validate a PGLCSR1 snapshot.
+
+    The reference reads the whole file into one blob and copies every array
+    out of it.  Here each array is read straight into its own host tensor
+    (``readinto``, no intermediate copy) -- page-locked when ``pin_memory``
+    is set or a CUDA ``device`` is given, in which case the arrays are then
+    uploaded asynchronously and the CSR is validated on the device.  The
+    checks and their error messages are the reference's.
+    """
     path = os.fspath(path)
     try:
-        with open(path, "rb") as fh:
-            blob = fh.read()
+        fh = open(path, "rb")
     except OSError as e:
         raise GraphLoadError(f"{path}: {e.strerror}") from e
-    if len(blob) < 40 or blob[:8] != _CACHE_MAGIC:
-        raise GraphLoadError(f"{path}: not a graph cache (bad magic/version)")
-    try:
-        id_dt = np.dtype(blob[8:16].rstrip(b"\x00").decode("ascii"))
-    except (TypeError, UnicodeDecodeError) as e:
-        raise GraphLoadError(f"{path}: unreadable id dtype tag") from e
-    n, m = (int(x) for x in np.frombuffer(blob[16:32], dtype="<u8"))
-    has_id_map = blob[32] == 1
-    pos = 40
-
-    def take(count, dtype):
-        nonlocal pos
-        nbytes = count * dtype.itemsize
-        if pos + nbytes > len(blob):
+    with fh:
+        head = fh.read(40)
+        size = os.fstat(fh.fileno()).st_size
+        if len(head) < 32 or head[:8] != _CACHE_MAGIC:
+            raise GraphLoadError(f"{path}: not a graph cache (bad magic/version)")
+        if len(head) < 40:
             raise GraphLoadError(f"{path}: truncated graph cache")
-        arr = np.frombuffer(blob, dtype=dtype, count=count, offset=pos).copy()
-        pos += nbytes
-        return arr
-
-    out_off = take(n + 1, np.dtype("<i8"))
-    out_tgt = take(m, id_dt)
-    in_off = take(n + 1, np.dtype("<i8"))
-    in_tgt = take(m, id_dt)
-    id_map = take(n, np.dtype("<i8")) if has_id_map else None
-    if pos != len(blob):
-        raise GraphLoadError(f"{path}: trailing bytes in graph cache")
+        try:
+            id_dt = np.dtype(head[8:16].rstrip(b"\x00").decode("ascii"))
+        except (TypeError, UnicodeDecodeError) as e:
+            raise GraphLoadError(f"{path}: unreadable id dtype tag") from e
+        if id_dt.newbyteorder("=") not in _TORCH_OF:
+            raise GraphLoadError(f"{path}: unsupported id dtype {id_dt}")
+        n, m = (int(x) for x in np.frombuffer(head[16:32], dtype="<u8"))
+        has_id_map = head[32] == 1
+        dev = torch.device(device) if device is not None else None
+        pin = pin_memory or (dev is not None and dev.type == "cuda")
+        i8 = np.dtype("<i8")
+        parts = [(n + 1, i8), (m, id_dt), (n + 1, i8), (m, id_dt)]
+        if has_id_map:
+            parts.append((n, i8))
+        need = 40 + sum(c * d.itemsize for c, d in parts)
+        if size < need:
+            raise GraphLoadError(f"{path}: truncated graph cache")
+        if size > need:
+            raise GraphLoadError(f"{path}: trailing bytes in graph cache")
+        arrays = []
+        for count, dt in parts:
+            t = torch.empty(count, dtype=_TORCH_OF[dt.newbyteorder("=")], pin_memory=pin)
+            buf = memoryview(t.numpy()).cast("B")
+            if fh.readinto(buf) != len(buf):
+                raise GraphLoadError(f"{path}: truncated graph cache")
+            if dt.byteorder == ">" or (dt.byteorder == "=" and not _LITTLE):
+                t = t.numpy().byteswap().view(dt.newbyteorder("="))
+                t = torch.from_numpy(t)
+            arrays.append(t)
+    out_off, out_tgt, in_off, in_tgt = arrays[:4]
+    id_map = arrays[4].numpy() if has_id_map else None
+    if dev is not None:
+        out_off, out_tgt, in_off, in_tgt = (a.to(dev, non_blocking=True)
+                                            for a in (out_off, out_tgt, in_off, in_tgt))
     for offs in (out_off, in_off):
-        if offs[0] != 0 or offs[-1] != m or np.any(np.diff(offs) < 0):
+        if int(offs[0]) != 0 or int(offs[-1]) != m or bool((torch.diff(offs) < 0).any()):
             raise GraphLoadError(f"{path}: corrupt offsets in graph cache")
-    if m and (out_tgt.max() >= n or in_tgt.max() >= n
-              or out_tgt.min() < 0 or in_tgt.min() < 0):
+    if m and (int(out_tgt.max()) >= n or int(in_tgt.max()) >= n
+              or int(out_tgt.min()) < 0 or int(in_tgt.min()) < 0):
         raise GraphLoadError(f"{path}: target id out of range in graph cache")
-    g = Graph(n, torch.from_numpy(out_off), torch.from_numpy(out_tgt.astype(id_dt.newbyteorder("="))),
-              torch.from_numpy(in_off), torch.from_numpy(in_tgt.astype(id_dt.newbyteorder("="))),
-              id_map=id_map, source_path=path)
-    return g
+    return Graph(n, out_off, out_tgt, in_off, in_tgt, id_map=id_map, source_path=path)

@@ -191,3 +191,16 @@ def test_cache_of_our_graphs_matches_the_reference_bytes(tmp_path):
         pgx.save_cache(g, out)
         ref = open(os.path.join(GOLDEN, f"reference_cache_{name}.pglcsr"), "rb").read()
         assert out.read_bytes() == ref, name
+
+
+def test_load_cache_rejects_short_and_odd_files(tmp_path):
+    src = os.path.join(GOLDEN, "reference_cache_dup_loops_d.pglcsr")
+    blob = open(src, "rb").read()
+    cases = {"short36": (blob[:36], "truncated"), "short20": (blob[:20], "bad magic"),
+             "cut": (blob[:-4], "truncated"), "extra": (blob + b"\0" * 8, "trailing"),
+             "dtype": (blob[:8] + b"<f8".ljust(8, b"\0") + blob[16:], "unsupported id dtype")}
+    for name, (data, msg) in cases.items():
+        p = tmp_path / name
+        p.write_bytes(data)
+        with pytest.raises(pgx.GraphLoadError, match=msg):
+            pgx.load_cache(p)

@@ -240,3 +240,25 @@ def test_c4_pagerank_vs_oracle(graphs, mode):
     assert rel_err(rep.values, want.values) <= PR_RTOL
     assert [s.messages_sent for s in rep.supersteps] == [3_751_426] * 9 + [0]
     assert abs(rep.values[0] - 0.0001216244232021811) / 0.0001216244232021811 <= PR_RTOL
+
+
+def test_load_cache_pinned_and_on_device(tmp_path):
+    """load_cache(device=...) reads into page-locked buffers and uploads;
+    the device CSR equals the host one and runs through the engine."""
+    import os
+    g = rmat_graph("C1")
+    p = tmp_path / "c1.pglcsr"
+    pgx.save_cache(g, p)
+    host = pgx.load_cache(p)
+    pinned = pgx.load_cache(p, pin_memory=True)
+    dev = pgx.load_cache(p, device="cuda")
+    assert pinned.out_targets.is_pinned() and dev.out_targets.is_cuda
+    for a in ("out_offsets", "out_targets", "in_offsets", "in_targets"):
+        assert torch.equal(getattr(host, a), getattr(pinned, a))
+        assert torch.equal(getattr(host, a), getattr(dev, a).cpu())
+    want = pgx.run(host, pgx.pagerank()).values
+    assert np.array_equal(pgx.run(dev, pgx.pagerank()).values, want)
+    golden = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden",
+                          "reference_cache_edgelist_idmap_u.pglcsr")
+    d = pgx.load_cache(golden, device="cuda")
+    assert d.id_map is not None and d.out_targets.is_cuda
