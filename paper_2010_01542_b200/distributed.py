@@ -358,13 +358,16 @@ class CudaBackend:
         self.device = torch.device(device)
         self.stream = torch.cuda.current_stream(self.device)
         dev = self.device
-        off = graph.out_offsets.to(dev)
-        tgt = graph.out_targets.to(dev)
+        # slice where the graph lives and upload only this rank's rows (a
+        # pinned host graph stays pinned under slicing: one DMA per array)
+        off = graph.out_offsets
         self.n = graph.vertex_count
-        self.glob_deg = torch.diff(off)
-        base = int(off[lo])
-        self.row_ptr = (off[lo:hi + 1] - base).to(torch.int32).contiguous()
-        self.col = tgt[base:int(off[hi])].to(torch.int32).contiguous()
+        self._glob_off = off
+        base, end = int(off[lo]), int(off[hi])
+        self.row_ptr = (off[lo:hi + 1] - base).to(dev, non_blocking=True) \
+            .to(torch.int32).contiguous()
+        self.col = graph.out_targets[base:end].to(dev, non_blocking=True) \
+            .to(torch.int32).contiguous()
         self.len = hi - lo
         self.m_local = int(self.col.numel())
         st = self.stream.cuda_stream
@@ -422,10 +425,12 @@ class CudaBackend:
         return self._nnz_cache
 
     def global_out_degree(self, v: int) -> int:
-        return int(self.glob_deg[v])
+        return int(self._glob_off[v + 1]) - int(self._glob_off[v])
 
     def global_nonzero_degree(self) -> int:
-        return int((self.glob_deg > 0).sum())
+        if getattr(self, "_nnz_global", None) is None:
+            self._nnz_global = int((torch.diff(self._glob_off) > 0).sum())
+        return self._nnz_global
 
     def _counters(self):
         c = self.ctr[:32].view(torch.int64).tolist()

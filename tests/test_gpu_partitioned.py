@@ -64,3 +64,25 @@ def test_partitioned_cuda_matches_oracle(spec, world, exchange):
         if app != "pagerank":
             used = {s["exchange"] for s in stats}
             assert used <= ({"peer"} if exchange == "peer" else {"dense", "sparse"})
+
+
+@pytest.mark.parametrize("exchange", ["peer", "hybrid"])
+def test_partitioned_from_pinned_host_graph(exchange):
+    """Each rank uploads only its own rows of a page-locked host graph (the
+    end-to-end path of bench.py under torchrun)."""
+    spec = SPECS[0]
+    n, off, tgt = O.rmat_csr(spec)
+    host = pgx.from_csr(torch.from_numpy(off), torch.from_numpy(tgt)).pin_memory()
+    bounds = partition_bounds(np.diff(off), 2)
+    want = O.run_cc(n, off, tgt)
+
+    def rank_fn(r, d):
+        be = CudaBackend(host, int(bounds[r]), int(bounds[r + 1]), "cuda:0")
+        assert be.col.numel() == int(off[bounds[r + 1]] - off[bounds[r]])
+        run = PartitionedRun(be, d, bounds, n, int(tgt.size))
+        run.exchange = exchange
+        return run.run_min("components", 0, 10_000)
+    vals, stats, hit, _ = run_ranks(2, rank_fn)[0]
+    assert np.array_equal(vals.cpu().numpy().view(np.uint32).astype(np.int64),
+                          want.values.astype(np.int64))
+    assert [s["active_count"] for s in stats] == want.active_counts
