@@ -284,7 +284,9 @@ def bench_gpu(args):
     host = g.pin_memory()
     e2e_ms = []
     h2d = (n + 1) * 8 + m * 4
-    d2h = n * (8 if app == "pagerank" else 4)
+    # the result tensor read back: f64 ranks, int64 labels (the reference's
+    # CC dtype, algorithms.py:111, widened on the device), u32 distances
+    d2h = n * (4 if app == "sssp" else 8)
     for i in range(args.warmup + args.e2e_steps):
         host.drop_device_cache()
         flush_l2(flush)
@@ -462,7 +464,7 @@ def bench_multi(args):
                    "process_group": backend},
         "e2e": {"value": round(edges / (e2e_ms * 1e-3) / 1e9, 4), "unit": "GTEPS",
                 "h2d_bytes_per_step": (n + 1) * 8 + m * 4,
-                "d2h_bytes_per_step": n * (8 if app == "pagerank" else 4),
+                "d2h_bytes_per_step": n * (4 if app == "sssp" else 8),
                 "ms_per_step": round(e2e_ms, 3)},
         # our kernels per timed step: scatter + apply (+ reset_touched for
         # the peer exchange) per superstep
