@@ -127,7 +127,15 @@ class PartitionedRun:
             torch.cuda.current_stream(self.b.device).synchronize()
 
     def _peer_setup(self) -> bool:
-        """Map every rank's mailbox on every rank (collective decision)."""
+        """Map every rank's mailbox on every rank (collective decision).
+
+        The outcome is cached on the rank's backend (cached per graph, so
+        every rank of a job holds the same cache state): later runs on the
+        same backend skip the handle exchange."""
+        cached = getattr(self.b, "_peer_decision", None)
+        if cached is not None and cached[0] == self.exchange:
+            self.b.peer_active = cached[1]
+            return cached[1]
         if self.exchange not in ("auto", "peer") or not hasattr(self.b, "peer_handle"):
             want = False
         else:
@@ -143,6 +151,7 @@ class PartitionedRun:
         if not ok and self.exchange == "peer":
             raise RuntimeError("peer exchange requested but a rank cannot map its peers")
         self.b.peer_active = ok
+        self.b._peer_decision = (self.exchange, ok)
         return ok
 
     def _fence(self):
