@@ -63,10 +63,13 @@ constexpr int kListCap = kApplyListBytes / (int)sizeof(int32_t);
 // Returns (recipients counted) << 32 | (broadcasts) for this thread.  With
 // `count_only` the bitmask is only counted (superstep cap reached: the
 // pending messages must stay unconsumed, engine.py:299-300).
-template <int APP, int S = 0>
+// BFS = true (unit-weight SSSP, see scatter_phase): every flagged recipient
+// received the uniform message `bfs_msg`; the mailbox is not used.
+template <int APP, int S = 0, bool BFS = false>
 __device__ unsigned long long apply_min_phase(const int32_t *__restrict__ row_ptr, uint32_t *val,
                                               uint32_t *mailbox, int32_t n, const RunWs &ws,
-                                              StepCounters *ctr, char *smem, bool count_only) {
+                                              StepCounters *ctr, char *smem, bool count_only,
+                                              uint32_t bfs_msg = 0) {
   __shared__ unsigned long long s_w[33];
   __shared__ unsigned long long s_gbase;
   int32_t *s_list = reinterpret_cast<int32_t *>(smem);  // kListCap vertex ids
@@ -127,7 +130,7 @@ __device__ unsigned long long apply_min_phase(const int32_t *__restrict__ row_pt
 #pragma unroll
         for (int j = 0; j < kApplyItems; j++) {
           if (v[j] >= 0) {
-            m[j] = *slot<S>(mailbox, v[j]);
+            m[j] = BFS ? bfs_msg : *slot<S>(mailbox, v[j]);
             cv[j] = *slot<S>(val, v[j]);
             rs[j] = row_ptr[v[j]];
             re[j] = row_ptr[v[j] + 1];
@@ -138,7 +141,7 @@ __device__ unsigned long long apply_min_phase(const int32_t *__restrict__ row_pt
         for (int j = 0; j < kApplyItems; j++) {
           deg[j] = 0;
           if (v[j] >= 0) {
-            *slot<S>(mailbox, v[j]) = kNeutralMin;  // consume (mailbox.py:112-117)
+            if (!BFS) *slot<S>(mailbox, v[j]) = kNeutralMin;  // consume (mailbox.py:112-117)
             if (m[j] < cv[j]) {
               *slot<S>(val, v[j]) = m[j];
               bcast++;

@@ -60,7 +60,7 @@ struct MinRunParams {
 // S = 0: externalised SoA (value = the caller's output array); S = 1:
 // interleaved {mailbox, value} records (layout.py's INTERLEAVED), values
 // copied out to the caller's array at the end of the run.
-template <int APP, int S>
+template <int APP, int S, bool BFS = false>
 __global__ void __launch_bounds__(kBlock, PGX_MIN_BLOCKS) min_run_kernel(MinRunParams p) {
   extern __shared__ __align__(16) char smem[];
   __shared__ unsigned s_red[32];
@@ -101,6 +101,9 @@ __global__ void __launch_bounds__(kBlock, PGX_MIN_BLOCKS) min_run_kernel(MinRunP
   }
   grid_sync<kArriveRed>(p.ws.bar, gen);
   if (APP == PGX_APP_SSSP && gtid == 0) *slot<S>(val, p.source) = 0u;
+  // unit-weight SSSP on the shipped arm: the has-bit filter (scatter_phase);
+  // the host launches the BFS instantiation only for the default options
+  constexpr bool bfs = BFS && APP == PGX_APP_SSSP && S == 0;
   if (gtid == 0) p.stats[PGX_STAT_HDR + 7] = (int64_t)globaltimer();
 
   for (int s = 0;; s++) {
@@ -137,6 +140,8 @@ __global__ void __launch_bounds__(kBlock, PGX_MIN_BLOCKS) min_run_kernel(MinRunP
       a.E = (int64_t)(packed & 0xFFFFFFFFull);
       if (p.vertex_sched)
         scatter_vertex_phase<MsgSrc::kFrontier, S>(a, p.read_filter);
+      else if (bfs)
+        scatter_phase<PGX_OP_MIN_U32, MsgSrc::kFrontier, 0, false, true>(a, smem);
       else
         scatter_phase<PGX_OP_MIN_U32, MsgSrc::kFrontier, S>(a, smem, p.read_filter);
     }
@@ -151,7 +156,10 @@ __global__ void __launch_bounds__(kBlock, PGX_MIN_BLOCKS) min_run_kernel(MinRunP
     //      pending messages are only counted (engine.py:299-300) ----
     const bool at_cap = (s + 1 == p.max_steps);
     const unsigned long long rb =
-        apply_min_phase<APP, S>(p.row_ptr, val, mailbox, p.n, p.ws, &p.ws.ctr[s + 1], smem, at_cap);
+        bfs ? apply_min_phase<APP, 0, true>(p.row_ptr, val, mailbox, p.n, p.ws, &p.ws.ctr[s + 1],
+                                            smem, at_cap, (uint32_t)s + 1u)
+            : apply_min_phase<APP, S>(p.row_ptr, val, mailbox, p.n, p.ws, &p.ws.ctr[s + 1], smem,
+                                      at_cap);
     const unsigned bc = block_sum<unsigned>((unsigned)(rb & 0xFFFFFFFFull), s_red);
     const unsigned rc = block_sum<unsigned>((unsigned)(rb >> 32), s_red);
     if (threadIdx.x == 0) {
@@ -303,6 +311,9 @@ __global__ void __launch_bounds__(kBlock, PGX_MIN_BLOCKS) pagerank_run_kernel(Pr
   }
 }
 
+#ifndef PGX_SSSP_BFS
+#define PGX_SSSP_BFS 1
+#endif
 #ifndef PGX_PR_UNROLL
 #define PGX_PR_UNROLL 2
 #endif
@@ -506,11 +517,14 @@ static int min_run(int app, int32_t n, int64_t m, const int32_t *row_ptr, const 
   const size_t smem = scatter_smem(PGX_OP_MIN_U32, nhubs);
   int grid = 0;
   void *args[] = {&p};
+  const bool bfs = PGX_SSSP_BFS && !p.interleaved && p.read_filter && !p.cas_loop &&
+                   !p.vertex_sched && nhubs == 0;
   void (*kern)(MinRunParams) =
-      app == PGX_APP_SSSP ? (p.interleaved ? min_run_kernel<PGX_APP_SSSP, 1>
-                                           : min_run_kernel<PGX_APP_SSSP, 0>)
-                          : (p.interleaved ? min_run_kernel<PGX_APP_CC, 1>
-                                           : min_run_kernel<PGX_APP_CC, 0>);
+      app == PGX_APP_SSSP
+          ? (p.interleaved ? min_run_kernel<PGX_APP_SSSP, 1>
+                           : bfs ? min_run_kernel<PGX_APP_SSSP, 0, true>
+                                 : min_run_kernel<PGX_APP_SSSP, 0>)
+          : (p.interleaved ? min_run_kernel<PGX_APP_CC, 1> : min_run_kernel<PGX_APP_CC, 0>);
   rc = coop_grid(kern, smem, &grid);
   if (rc) return rc;
   PGX_CUDA(cudaLaunchCooperativeKernel((void *)kern, grid, kBlock, args, smem, st));
