@@ -146,3 +146,37 @@ def test_randomized_gpu_vs_oracle(case):
         want = O.run_pagerank(n, off, tgt)
         assert np.max(np.abs(pr.values - want.values) / np.abs(want.values)) <= 1e-9
         assert pr.superstep_count == want.superstep_count
+
+
+def _big_cases():
+    k = 300_001
+    yield "star_out_300k", np.zeros(k - 1, int), np.arange(1, k), k, False
+    yield "star_in_300k", np.arange(1, k), np.zeros(k - 1, int), k, False
+    yield "star_sym_300k", np.zeros(k - 1, int), np.arange(1, k), k, True
+    n = 20_003  # a long chain: 20k tiny supersteps, n not a multiple of 32
+    yield "chain_20k", np.arange(n - 1), np.arange(1, n), n, True
+    rng = np.random.default_rng(7)
+    n = 100_003
+    hubs = rng.integers(0, 50, 400_000)
+    yield "hubby_dir", hubs, rng.integers(0, n, 400_000), n, False
+
+
+@pytest.mark.parametrize("case", list(_big_cases()), ids=lambda c: c[0])
+def test_large_hub_rows_and_long_runs_vs_oracle(case):
+    """Rows spanning thousands of 256-edge tiles, in-hubs receiving 300k
+    messages per superstep, and 20k-superstep runs: CC / SSSP exact with
+    per-superstep counts (the unit-weight SSSP bitmap kernel included)."""
+    name, src, dst, n, und = case
+    off, tgt = O.csr_from_edges(src, dst, n, und)
+    g = pgx.from_csr(torch.from_numpy(off).cuda(), torch.from_numpy(tgt).cuda())
+    cap = 30_000
+    for source in (0, n - 1):
+        sp = pgx.run(g, pgx.sssp(source), pgx.EngineConfig(max_supersteps=cap))
+        want = O.run_sssp(n, off, tgt, source, cap)
+        assert np.array_equal(sp.values, want.values), (name, source)
+        assert [s.active_count for s in sp.supersteps] == want.active_counts
+        assert [s.messages_sent for s in sp.supersteps] == want.messages_sent
+    cc = pgx.run(g, pgx.connected_components(), pgx.EngineConfig(max_supersteps=cap))
+    want = O.run_cc(n, off, tgt, max_steps=cap)
+    assert np.array_equal(cc.values, want.values)
+    assert [s.active_count for s in cc.supersteps] == want.active_counts
