@@ -5,7 +5,7 @@ CudaBackend (local CSR, full-width mailbox, owned slice) and the driver is
 the production PartitionedRun, with each mailbox exchange: the fused peer
 scatter (pgx_scatter_peer combining straight into the owners' mailboxes),
 the per-superstep dense / sparse collectives, dense only.  Results must equal the oracle's (CC / SSSP
-exact with per-superstep counts, PageRank within 1e-9) for W = 1, 2, 4.
+exact with per-superstep counts, PageRank within 1e-9) for W = 1, 2, 4, 8.
 """
 
 import numpy as np
@@ -40,7 +40,7 @@ def _run(off, tgt, app, kw, world, exchange="auto"):
     return run_ranks(world, rank_fn)[0]
 
 
-@pytest.mark.parametrize("world", [1, 2, 4])
+@pytest.mark.parametrize("world", [1, 2, 4, 8])
 @pytest.mark.parametrize("spec", SPECS, ids=["sym", "dir"])
 @pytest.mark.parametrize("exchange", ["peer", "hybrid", "dense"])
 def test_partitioned_cuda_matches_oracle(spec, world, exchange):
