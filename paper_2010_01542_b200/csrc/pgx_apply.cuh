@@ -13,7 +13,7 @@ namespace pgx {
 // sparse apply for the min programs (SSSP / CC), driven by the
 // has-message bitmask: consume every flagged mailbox (vertex order),
 // adopt an improvement, append improved vertices to the next frontier
-// with their edge prefix.  One 64-bit atomic per block chunk reserves
+// with their edge prefix.  One 64-bit atomic per apply batch reserves
 // (frontier slots, edge range); the tile map is written as a side effect.
 // ------------------------------------------------------------------
 

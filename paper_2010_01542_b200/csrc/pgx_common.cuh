@@ -129,9 +129,9 @@ __device__ __forceinline__ __attribute__((unused)) unsigned lanemask_lt() {
   return m;
 }
 
-// Sense-counting grid barrier for a co-resident (cooperative) grid.  The
-// gpu-scope fences on both sides also invalidate L1 (CCTL.IVALL), so the
-// weak, L1-cacheable mailbox reads of the next phase never see values
+// Grid barrier for a co-resident (cooperative) grid.  The gpu-scope
+// fences on both sides also invalidate L1 (CCTL.IVALL), so the weak,
+// L1-cacheable mailbox / has-bit reads of the next phase never see values
 // from before the barrier.
 struct GridBarrier {
   unsigned count;

@@ -21,10 +21,12 @@
 //                       (pgx_scatter.cuh).
 //   externalisation  -> SoA: value[], mailbox[], has-bitmask, frontier SoA.
 //   edge-centric     -> the frontier is built with its exclusive edge
-//                       prefix (one 64-bit packed atomic per block chunk,
+//                       prefix (one 64-bit packed atomic per apply batch,
 //                       pgx_apply.cuh); the scatter walks fixed 256-edge warp
 //                       tiles of that edge space -- exact edge balance, hub
 //                       rows split across tiles.
+// Unit-weight SSSP filters on the has-message bitmap instead of the mailbox
+// (every message of a superstep is equal; pgx_scatter.cuh, BFS = true).
 // PageRank's default lowering is the reference's pull fold (pgx_gather.cuh).
 #include "pgx_apply.cuh"
 #include "pgx_common.cuh"
