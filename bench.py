@@ -426,6 +426,7 @@ def bench_multi(args):
     total_ms = float(t.item())
     edges = sum(s.edges for s in rep.supersteps)
     value = edges * args.steps / (total_ms * 1e-3) / 1e9
+    ex = set(rep.exchanges or [])
     peak, peak_src = measured_peaks()
     alg = algorithmic_bytes(app, n, m, step_views(app, rep))
     achieved = alg / (total_ms / args.steps * 1e-3) / 1e9
@@ -456,10 +457,12 @@ def bench_multi(args):
                                f"over {world} GPUs (edge-balanced ranges)",
                    "n": n, "m": m, "supersteps": rep.superstep_count,
                    "l2": "flushed (512 MiB write) between timed steps",
-                   "parallelism": f"partitioned x{world}: " + (
-                       "fused peer-memory combine (NVLink P2P red.min) + allreduce"
-                       if "peer" in (rep.exchanges or []) else
-                       "NCCL reduce_scatter / sparse all_to_all + allreduce"),
+                   "parallelism": f"partitioned x{world}: " + " + ".join(
+                       x for x, used in (
+                           ("NCCL reduce_scatter (large supersteps)", "dense" in ex),
+                           ("sparse all_to_all", "sparse" in ex),
+                           ("fused peer-memory combine (NVLink P2P red.min)", "peer" in ex))
+                       if used) + ", counters all-gather",
                    "exchange_per_superstep": rep.exchanges,
                    "process_group": backend},
         "e2e": {"value": round(edges / (e2e_ms * 1e-3) / 1e9, 4), "unit": "GTEPS",
@@ -468,8 +471,8 @@ def bench_multi(args):
                 "ms_per_step": round(e2e_ms, 3)},
         # our kernels per timed step: scatter + apply (+ reset_touched for
         # the peer exchange) per superstep
-        "gpu_launches": (3 if "peer" in (rep.exchanges or []) else 2)
-                        * rep.superstep_count * args.steps,
+        "gpu_launches": sum(3 if e == "peer" else 2 for e in (rep.exchanges or []))
+                        * args.steps,
         "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak * world,
                      "unit": "GB/s", "frac": round(achieved / (peak * world), 4),
                      "traffic": None, "peak_source": peak_src + f" x {world} GPUs"},

@@ -246,9 +246,9 @@ class PartitionedRun:
     def run_min(self, app: str, source: int, max_steps: int):
         op = self.dist.ReduceOp.MIN
         n = self.n
-        peer = self._peer_setup()
+        peer_ok = self._peer_setup()
         self.b.init_min(app, self.lo, self.hi)
-        if peer:  # every mailbox is neutral before any peer combines into it
+        if peer_ok:  # every mailbox is neutral before any peer combines into it
             self._fence()
         stats = []
         if app == "sssp":
@@ -265,14 +265,19 @@ class PartitionedRun:
         for s in range(max_steps):
             ts = time.perf_counter()
             cur = nxt
+            # "auto": the fused peer exchange for supersteps that traverse at
+            # most n/2 edges (remote combines ~ surviving foreign messages),
+            # the dense collective (n slots per rank) for the big ones
+            use_peer = peer_ok and (self.exchange == "peer" or 2 * cur.edges <= n)
             self.b.reset_mailbox()
             self.b.scatter_min(dense=(app == "components" and s == 0),
-                               id_offset=self.lo)
-            if peer:
+                               id_offset=self.lo, peer=use_peer)
+            if use_peer:
                 self._fence()
                 exchange = "peer"
             else:
                 exchange = self._exchange_min(op)
+            self.b.exchanged(exchange)
             at_cap = s + 1 == max_steps
             nxt = self._gather_counts(self.b.apply_min(app, count_only=at_cap))
             sent = cur.edges if app == "sssp" else cur.broadcasts
@@ -411,7 +416,7 @@ class CudaBackend:
         sb = _lib.out_size(self.lib.pgx_touched_scratch_bytes, self.n)
         self.tscratch = torch.empty(sb, dtype=torch.uint8, device=dev)
         self.tcount = torch.zeros(1, dtype=torch.int64, device=dev)
-        self._full_reset = True
+        self._last = None
         # fused peer exchange state (PartitionedRun._peer_setup)
         self.peer_active = False
         self._peer_mb = None
@@ -497,13 +502,13 @@ class CudaBackend:
             self.mailbox = torch.empty(self.n, dtype=torch.int32, device=self.device)
         self.mailbox.fill_(EXCHANGE_NEUTRAL)
         self.has.zero_()
-        self._full_reset = False
         self.val = torch.empty(max(self.len, 1), dtype=torch.int32, device=self.device)
         app_id = self._lib.PGX_APP_CC if app == "components" else self._lib.PGX_APP_SSSP
         self._lib.check(self.lib.pgx_slice_init(app_id, self.len, lo, self.val.data_ptr(),
                                                 self.row_ptr.data_ptr(), None, 0.0,
                                                 self.stream.cuda_stream), "pgx_slice_init")
         self.nsrc, self.E = 0, 0
+        self._last = None  # exchange of the previous superstep
 
     def seed_source(self, local_v: int):
         rs = int(self.row_ptr[local_v])
@@ -518,24 +523,29 @@ class CudaBackend:
             self.nsrc, self.E = 1, deg
 
     def reset_mailbox(self):
+        """Undo what the previous superstep's exchange left behind.  The
+        owned slice is always neutral here (the apply consumed it), and it
+        is never written: a peer may already be combining into it."""
         if self.app == "pagerank":
             self.mailbox.zero_()
             return
-        if self.peer_active:  # foreign filter copies back to neutral, bits cleared
+        if self._last == "peer":  # foreign filter copies back to neutral, bits cleared
             self._lib.check(self.lib.pgx_reset_touched(
                 self.n, self.lo_own, self.hi_own, self.has.data_ptr(), self.mailbox.data_ptr(),
                 EXCHANGE_NEUTRAL, self.stream.cuda_stream), "pgx_reset_touched")
             return
-        # after a sparse exchange the foreign touched slots were reset by the
-        # compaction and the own slice by the apply; after a dense one every
-        # non-owned slot holds stale partial values
-        if self._full_reset:
-            self.mailbox.fill_(EXCHANGE_NEUTRAL)
-        self.has.zero_()
-        self._full_reset = False
+        if self._last == "dense":  # every foreign slot holds a stale partial
+            self.mailbox[:self.lo_own].fill_(EXCHANGE_NEUTRAL)
+            self.mailbox[self.hi_own:].fill_(EXCHANGE_NEUTRAL)
+        # sparse: the compaction reset the foreign touched slots
+        if self._last is not None:
+            self.has.zero_()
+
+    def exchanged(self, kind: str):
+        self._last = kind
 
     def dense_exchanged(self):
-        self._full_reset = True
+        pass  # recorded by exchanged("dense")
 
     def touched_count(self) -> int:
         self._lib.check(self.lib.pgx_touched(
@@ -563,10 +573,10 @@ class CudaBackend:
                                                    self.mailbox.data_ptr(),
                                                    self.stream.cuda_stream), "pgx_scatter_pairs")
 
-    def scatter_min(self, dense: bool, id_offset: int):
+    def scatter_min(self, dense: bool, id_offset: int, peer: bool = False):
         L, st = self.lib, self.stream.cuda_stream
         op = self._lib.PGX_OP_MIN_U32
-        if self.peer_active:
+        if peer:
             if dense:
                 src = (self._g_nz_eb.data_ptr(), None, self._g_nz_id.data_ptr(), id_offset, None,
                        self._g_tile.data_ptr(), self._nnz(), self.m_local)

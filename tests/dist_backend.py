@@ -36,7 +36,7 @@ class CpuBackend:
         self.deg = np.diff(self.row_ptr)
         self.front = (np.empty(0, np.int64), np.empty(0, np.int64))  # (local ids, msgs)
         self.has = np.zeros(self.n, bool)
-        self._full_reset = True
+        self._last = None
         self.peer_active = False
         self._shm = None
         self._peers = None
@@ -94,7 +94,7 @@ class CpuBackend:
         else:
             self.mailbox = torch.full((self.n,), EXCHANGE_NEUTRAL, dtype=torch.int32)
         self.has[:] = False
-        self._full_reset = False
+        self._last = None
         if app == "components":
             self.val = np.arange(lo, hi, dtype=np.int64)
         else:
@@ -110,17 +110,19 @@ class CpuBackend:
         if self.app == "pagerank":
             self.mailbox.zero_()
             return
-        if self.peer_active:  # pgx_reset_touched
-            self.mailbox.numpy()[self._foreign()] = EXCHANGE_NEUTRAL
-            self.has[:] = False
-            return
-        if self._full_reset:
-            self.mailbox.fill_(EXCHANGE_NEUTRAL)
+        mb = self.mailbox.numpy()
+        if self._last == "peer":  # pgx_reset_touched
+            mb[self._foreign()] = EXCHANGE_NEUTRAL
+        elif self._last == "dense":  # foreign slots only: the owned slice is neutral
+            mb[:self.lo] = EXCHANGE_NEUTRAL
+            mb[self.hi:] = EXCHANGE_NEUTRAL
         self.has[:] = False
-        self._full_reset = False
+
+    def exchanged(self, kind):
+        self._last = kind
 
     def dense_exchanged(self):
-        self._full_reset = True
+        pass
 
     def _foreign(self):
         idx = np.flatnonzero(self.has)
@@ -143,7 +145,7 @@ class CpuBackend:
         np.minimum.at(self.mailbox.numpy(), (p >> 32).astype(np.int64),
                       (p & 0xFFFFFFFF).astype(np.int32))
 
-    def scatter_min(self, dense, id_offset):
+    def scatter_min(self, dense, id_offset, peer=False):
         if dense:
             lv = np.flatnonzero(self.deg > 0)
             msg = lv + id_offset
@@ -152,7 +154,7 @@ class CpuBackend:
         dst, m = self._edges_of(lv, msg)
         m = m.astype(np.int32)
         mb = self.mailbox.numpy()
-        if not self.peer_active:
+        if not peer:
             np.minimum.at(mb, dst, m)
             self.has[dst] = True
             return

@@ -95,7 +95,8 @@ def _expected(off, tgt, app, kw):
 
 
 @pytest.mark.parametrize("world,exchange", [(2, "hybrid"), (3, "hybrid"), (2, "dense"),
-                                            (2, "peer"), (3, "peer")])
+                                            (2, "peer"), (3, "peer"), (2, "auto"),
+                                            (3, "auto")])
 def test_partitioned_run_matches_oracle(world, exchange, tmp_path):
     jobs = _jobs()
     mp.start_processes(_worker, args=(world, _free_port(), jobs, str(tmp_path), exchange),
@@ -114,8 +115,13 @@ def test_partitioned_run_matches_oracle(world, exchange, tmp_path):
         assert hit == want.hit_superstep_cap
     # hybrid: both collective exchanges ran (sparse on the late supersteps);
     # peer: the min programs never reduce the mailbox (PageRank records none)
-    assert modes == {"hybrid": {"dense", "sparse"}, "dense": {"dense"},
-                     "peer": {"peer"}}[exchange]
+    # auto: the dense collective for the big supersteps, the peer exchange
+    # for the rest (every transition between the two is exercised)
+    if exchange == "auto":
+        assert {"dense", "peer"} <= modes <= {"dense", "sparse", "peer"}
+    else:
+        assert modes == {"hybrid": {"dense", "sparse"}, "dense": {"dense"},
+                         "peer": {"peer"}}[exchange]
 
 
 def test_partition_bounds_edge_balanced():

@@ -42,7 +42,7 @@ def _run(off, tgt, app, kw, world, exchange="auto"):
 
 @pytest.mark.parametrize("world", [1, 2, 4, 8])
 @pytest.mark.parametrize("spec", SPECS, ids=["sym", "dir"])
-@pytest.mark.parametrize("exchange", ["peer", "hybrid", "dense"])
+@pytest.mark.parametrize("exchange", ["auto", "peer", "hybrid", "dense"])
 def test_partitioned_cuda_matches_oracle(spec, world, exchange):
     n, off, tgt = O.rmat_csr(spec)
     src = int(np.argmax(np.diff(off)))
@@ -63,7 +63,8 @@ def test_partitioned_cuda_matches_oracle(spec, world, exchange):
         assert hit == want.hit_superstep_cap
         if app != "pagerank":
             used = {s["exchange"] for s in stats}
-            assert used <= ({"peer"} if exchange == "peer" else {"dense", "sparse"})
+            assert used <= {"peer": {"peer"}, "auto": {"dense", "sparse", "peer"}}.get(
+                exchange, {"dense", "sparse"})
 
 
 @pytest.mark.parametrize("exchange", ["peer", "hybrid"])
