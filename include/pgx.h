@@ -158,7 +158,9 @@ int pgx_pagerank_run(int32_t n, int64_t m, const int32_t *row_ptr,
  * mode for PR (algorithms.py:80; fold engine.py:425-457): every vertex
  * folds its in-neighbours' shares, no atomics.  Needs the in-CSR
  * (in_row_ptr / in_col, rows sorted by source id) and its graph workspace
- * from pgx_graph_prepare(in_row_ptr); row_ptr gives the out-degrees. */
+ * from pgx_graph_prepare(in_row_ptr); row_ptr gives the out-degrees.
+ * in_col must be 32-byte aligned (256-bit id loads); every other array
+ * needs only its element alignment. */
 int pgx_pagerank_pull_run(int32_t n, int64_t m, const int32_t *row_ptr,
                           const int32_t *in_row_ptr, const int32_t *in_col,
                           const void *in_graph_ws, int32_t iterations,

@@ -600,6 +600,8 @@ int pgx_pagerank_pull_run(int32_t n, int64_t m, const int32_t *row_ptr,
   int rc = check_graph(n, m, in_row_ptr, in_col, in_graph_ws);
   if (rc) return rc;
   if (!row_ptr) return fail(PGX_EINVAL, "null out-CSR offsets");
+  if (reinterpret_cast<uintptr_t>(in_col) % 32)  // 256-bit id loads in the fold
+    return fail(PGX_EINVAL, "in_col must be 32-byte aligned");
   if (iterations < 1) return fail(PGX_EINVAL, "iterations must be >= 1");
   if (!(damping >= 0.0 && damping <= 1.0)) return fail(PGX_EINVAL, "damping must be in [0, 1]");
   if (max_supersteps < 1) return fail(PGX_EINVAL, "superstep cap must be >= 1");

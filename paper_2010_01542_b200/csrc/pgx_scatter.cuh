@@ -62,11 +62,15 @@ __device__ void scatter_phase(const ScatterArgs &a, char *smem, bool read_filter
     // the warp's next tile: its neighbour ids (dense: one contiguous 1 KB
     // run of col_idx) are pulled into L2 while this tile is processed
     if (kDense && lane == 0 && t + nwarps < ntiles) {
+      // the bulk prefetch needs 16-byte granules: widen the range (col_idx
+      // itself may be any 4-byte-aligned view, e.g. a rank's slice)
       const int64_t en = (t + nwarps) * kTile;
-      const int bytes = (int)(min(a.E - en, (int64_t)kTile) * 4) & ~15;
-      if (bytes > 0)
-        asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(a.col + en), "r"(bytes)
-                     : "memory");
+      const uint64_t p0 = reinterpret_cast<uint64_t>(a.col + en) & ~15ull;
+      const uint64_t p1 =
+          (reinterpret_cast<uint64_t>(a.col + min(a.E, en + kTile)) + 15ull) & ~15ull;
+      asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p0),
+                   "r"((unsigned)(p1 - p0))
+                   : "memory");
     }
 #endif
     const int i0 = a.tile_src[t];

@@ -84,3 +84,14 @@ def test_interleaved_layout_sizes_the_record_array():
     finally:
         _lib.set_option(_lib.PGX_OPT_LAYOUT, _lib.PGX_LAYOUT_EXTERNALISED)
     assert aos.value - soa.value >= 4 * (1 << 20)
+
+
+def test_pull_pagerank_rejects_a_misaligned_in_col():
+    """The fold loads neighbour ids 32 bytes at a time: a misaligned in_col
+    is refused with PGX_EINVAL before anything touches the device."""
+    lib = _lib.load()
+    fake = 1 << 20  # never dereferenced: the argument checks come first
+    rc = lib.pgx_pagerank_pull_run(10, 20, fake, fake, fake + 4, fake, 10, 0.85, 0.015, 0.1,
+                                   10, fake, fake, 1 << 20, fake, 0)
+    assert rc == _lib.PGX_EINVAL
+    assert b"32-byte aligned" in lib.pgx_last_error()

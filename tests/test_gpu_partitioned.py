@@ -87,3 +87,25 @@ def test_partitioned_from_pinned_host_graph(exchange):
     assert np.array_equal(vals.cpu().numpy().view(np.uint32).astype(np.int64),
                           want.values.astype(np.int64))
     assert [s["active_count"] for s in stats] == want.active_counts
+
+
+@pytest.mark.parametrize("exchange", ["auto", "hybrid"])
+def test_partition_slices_at_unaligned_offsets(exchange):
+    """Rank boundaries whose first edge offset is not a multiple of 4: each
+    rank's col_idx is then an unaligned view of the targets."""
+    n, off, tgt = O.rmat_csr(SPECS[0])
+    g = pgx.from_csr(torch.from_numpy(off).cuda(), torch.from_numpy(tgt).cuda())
+    k = next(v for v in range(n // 3, n) if off[v] % 4 == 1)
+    k2 = next(v for v in range(2 * n // 3, n) if off[v] % 4 == 3)
+    bounds = np.array([0, k, k2, n], dtype=np.int64)
+    want = O.run_cc(n, off, tgt)
+
+    def rank_fn(r, d):
+        be = CudaBackend(g, int(bounds[r]), int(bounds[r + 1]), "cuda:0")
+        run = PartitionedRun(be, d, bounds, n, int(tgt.size))
+        run.exchange = exchange
+        return run.run_min("components", 0, 10_000)
+    vals, stats, hit, _ = run_ranks(3, rank_fn)[0]
+    assert np.array_equal(vals.cpu().numpy().view(np.uint32).astype(np.int64),
+                          want.values.astype(np.int64))
+    assert [s["active_count"] for s in stats] == want.active_counts

@@ -180,3 +180,20 @@ def test_large_hub_rows_and_long_runs_vs_oracle(case):
     want = O.run_cc(n, off, tgt, max_steps=cap)
     assert np.array_equal(cc.values, want.values)
     assert [s.active_count for s in cc.supersteps] == want.active_counts
+
+
+def test_unaligned_views_of_the_csr():
+    """col_idx may be any 4-byte-aligned view (a user's slice, a rank's
+    share of the targets): the dense superstep's L2 bulk prefetch widens
+    its range to 16-byte granules instead of faulting."""
+    n, off, tgt = O.rmat_csr(O.RmatSpec(12, 8, .57, .19, .19, 5, True))
+    want = O.run_cc(n, off, tgt)
+    for shift in (1, 2, 3):
+        buf = torch.zeros(tgt.size + shift, dtype=torch.int32, device="cuda")
+        buf[shift:] = torch.from_numpy(tgt).cuda()
+        view = buf[shift:]
+        assert view.data_ptr() % 16 != 0
+        g = pgx.from_csr(torch.from_numpy(off).cuda(), view)
+        rep = pgx.run(g, pgx.connected_components())
+        assert np.array_equal(rep.values, want.values)
+        assert [s.active_count for s in rep.supersteps] == want.active_counts
