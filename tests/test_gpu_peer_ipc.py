@@ -7,7 +7,8 @@ foreign messages straight into it -- the code path torchrun uses on an
 NVLink / NVSwitch node, where the mapping crosses GPUs.  No kernel waits on
 another rank: ranks synchronise only through host collectives.  Results
 must equal the oracle's: labels / distances exact, per-superstep counts
-exact, and every superstep must have used the peer exchange.
+exact; runs forced to "peer" use it in every superstep, "auto" runs mix it
+with the dense collective.
 """
 
 import os
@@ -48,13 +49,16 @@ def _worker(rank, world, port, out_dir):
     be = CudaBackend(g, int(bounds[rank]), int(bounds[rank + 1]), "cuda:0")
     out = {}
     src = int(np.argmax(np.diff(off)))
-    for app, kw in (("components", {}), ("sssp", {"source": src}),
-                    ("components", {"max_supersteps": 3})):
-        run = PartitionedRun(be, dist, bounds, n, int(tgt.size))
-        run.exchange = "peer"
+    for ex, app, kw in (("peer", "components", {}), ("peer", "sssp", {"source": src}),
+                        ("peer", "components", {"max_supersteps": 3}),
+                        ("auto", "components", {}), ("auto", "sssp", {"source": src})):
+        be2 = be if ex == "peer" else CudaBackend(g, int(bounds[rank]), int(bounds[rank + 1]),
+                                                  "cuda:0")
+        run = PartitionedRun(be2, dist, bounds, n, int(tgt.size))
+        run.exchange = ex
         vals, stats, hit, _ = run.run_min(app, kw.get("source", 0),
                                           kw.get("max_supersteps", 10_000))
-        out[(app, kw.get("max_supersteps"))] = (
+        out[(ex, app, kw.get("max_supersteps"))] = (
             vals.cpu().numpy().view(np.uint32).astype(np.int64),
             [s["active_count"] for s in stats], [s["messages_sent"] for s in stats],
             hit, {s["exchange"] for s in stats}, len(be._opened))
@@ -74,7 +78,7 @@ def test_peer_exchange_across_processes(tmp_path):
     out = torch.load(os.path.join(tmp_path, "peer.pt"), weights_only=False)
     n, off, tgt = O.rmat_csr(SPEC)
     src = int(np.argmax(np.diff(off)))
-    for (app, cap), (vals, active, sent, hit, modes, opened) in (
+    for (ex, app, cap), (vals, active, sent, hit, modes, opened) in (
             (k, v) for k, v in out.items() if k != "api"):
         want = (O.run_cc(n, off, tgt, max_steps=cap or 10_000) if app == "components"
                 else O.run_sssp(n, off, tgt, src))
@@ -82,6 +86,9 @@ def test_peer_exchange_across_processes(tmp_path):
         assert active == want.active_counts, app
         assert sent == want.messages_sent, app
         assert hit == want.hit_superstep_cap
-        assert modes == {"peer"}
+        if ex == "peer":
+            assert modes == {"peer"}
+        else:  # dense collective for the big supersteps, peer for the tail
+            assert "peer" in modes and modes <= {"dense", "sparse", "peer"}
         assert opened == world - 1  # the other rank's mailbox came through IPC
     assert np.array_equal(out["api"], O.run_cc(n, off, tgt).values.astype(np.int64))
