@@ -549,6 +549,17 @@ int pgx_cc_run(int32_t n, int64_t m, const int32_t *row_ptr, const int32_t *col_
                  max_supersteps, labels, run_ws, run_ws_bytes, stats, stream);
 }
 
+#if PGX_COUNT_OPS
+// debug build only: read and reset the scatter's operation counters
+int pgx_debug_counts(unsigned long long *out) {
+  PGX_CUDA(cudaDeviceSynchronize());
+  PGX_CUDA(cudaMemcpyFromSymbol(out, g_pgx_ops, sizeof(unsigned long long) * 3));
+  const unsigned long long z[3] = {0ull, 0ull, 0ull};
+  PGX_CUDA(cudaMemcpyToSymbol(g_pgx_ops, z, sizeof z));
+  return PGX_OK;
+}
+#endif
+
 int pgx_hub_capacity(int32_t *capacity) {
   if (!capacity) return fail(PGX_EINVAL, "null out pointer");
   *capacity = kHubs;

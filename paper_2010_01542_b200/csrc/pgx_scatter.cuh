@@ -26,6 +26,19 @@ namespace pgx {
 // and filtered against a per-CTA shared-memory copy of their mailbox;
 // only a CTA-local improvement goes to the global red.min.
 
+// Debug build only (-DPGX_COUNT_OPS=1, tools/count_ops.py): per-TU device
+// counters of the scatter's operations -- [0] red.min, [1] has-bit red.or,
+// [2] edges -- read and reset by pgx_debug_counts (not part of pgx.h).
+#ifndef PGX_COUNT_OPS
+#define PGX_COUNT_OPS 0
+#endif
+#if PGX_COUNT_OPS
+static __device__ unsigned long long g_pgx_ops[3];
+#define PGX_COUNT(i) (c_ops[i]++)
+#else
+#define PGX_COUNT(i) ((void)0)
+#endif
+
 // BFS = true: unit-weight SSSP, where every message of a superstep has the
 // same value (the superstep index + 1), so the min-combined mailbox carries
 // no information beyond "received": the filter reads the has-message bit
@@ -50,6 +63,9 @@ __device__ void scatter_phase(const ScatterArgs &a, char *smem, bool read_filter
   const int64_t gwarp = (int64_t)blockIdx.x * kWarps + warp;
   const int64_t nwarps = (int64_t)gridDim.x * kWarps;
   uint32_t *s_hub = reinterpret_cast<uint32_t *>(smem + scatter_windows_smem(OP));
+#if PGX_COUNT_OPS
+  unsigned long long c_ops[3] = {0ull, 0ull, 0ull};
+#endif
   if (OP == PGX_OP_MIN_U32 && a.nhubs > 0) {  // block-uniform
     for (int i = threadIdx.x; i < a.nhubs; i += blockDim.x) s_hub[i] = kNeutralMin;
     __syncthreads();
@@ -137,8 +153,11 @@ __device__ void scatter_phase(const ScatterArgs &a, char *smem, bool read_filter
 #pragma unroll
         for (int r = 0; r < kPass; r++) {
           const int x = w[r];
-          if (x != kInvalidEdge && !((hw[r] >> (x & 31)) & 1u))
+          if (x != kInvalidEdge) PGX_COUNT(2);
+          if (x != kInvalidEdge && !((hw[r] >> (x & 31)) & 1u)) {
             red_or_b32(a.has + (x >> 5), 1u << (x & 31));
+            PGX_COUNT(1);
+          }
         }
       } else if (OP == PGX_OP_MIN_U32) {
         // hybrid combiner, fire-and-forget: read-filter (the mailbox.py:159
@@ -160,6 +179,7 @@ __device__ void scatter_phase(const ScatterArgs &a, char *smem, bool read_filter
         for (int r = 0; r < kPass; r++) {
           const int x = w[r];
           const uint32_t msg = (uint32_t)mv[r];
+          if (x != kInvalidEdge) PGX_COUNT(2);
           if (x != kInvalidEdge && msg < old[r]) {
             int v = x;
             uint32_t prev = old[r];
@@ -182,7 +202,11 @@ __device__ void scatter_phase(const ScatterArgs &a, char *smem, bool read_filter
                 if (a.has && prev == a.neutral) atomicOr(a.has + (v >> 5), 1u << (v & 31));
               } else {
                 red_min_u32(slot<S>(mb, v), msg);
-                if (a.has && prev == a.neutral) red_or_b32(a.has + (v >> 5), 1u << (v & 31));
+                PGX_COUNT(0);
+                if (a.has && prev == a.neutral) {
+                  red_or_b32(a.has + (v >> 5), 1u << (v & 31));
+                  PGX_COUNT(1);
+                }
               }
               if (PEER && (v < a.lo || v >= a.hi)) {
                 // the local slot is this rank's filter; the owner's slot is
@@ -203,6 +227,10 @@ __device__ void scatter_phase(const ScatterArgs &a, char *smem, bool read_filter
       }
     }
   }
+#if PGX_COUNT_OPS
+  for (int i = 0; i < 3; i++)
+    if (c_ops[i]) atomicAdd(&g_pgx_ops[i], c_ops[i]);
+#endif
 }
 
 
