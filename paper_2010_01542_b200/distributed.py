@@ -216,7 +216,7 @@ class PartitionedRun:
         parts = [torch.empty_like(local) for _ in range(self.world)]
         self._coll_sync()
         self.dist.all_gather(parts, local)
-        rows = torch.stack(parts).tolist()
+        rows = [self.b.decode_counts(r) for r in torch.stack(parts).tolist()]
         self.b.set_frontier(rows[self.rank][2], rows[self.rank][3])
         tot = [sum(r[i] for r in rows) for i in range(4)]
         return StepCounts(*tot)
@@ -606,8 +606,8 @@ class CudaBackend:
         self._lib.check(rc, "pgx_scatter")
 
     def apply_min(self, app, count_only: bool) -> torch.Tensor:
-        """K2 on the owned slice; returns the device vector (recipients,
-        broadcasts, senders, edges) -- no host synchronisation."""
+        """K2 on the owned slice; returns the raw device counter block
+        (decode_counts) -- no host synchronisation, no extra kernels."""
         self.ctr.zero_()
         app_id = self._lib.PGX_APP_CC if app == "components" else self._lib.PGX_APP_SSSP
         sl = self.mailbox[self.lo:self.lo + self.len]
@@ -616,9 +616,13 @@ class CudaBackend:
             self.f_eb.data_ptr(), self.f_rs.data_ptr(), self.f_msg.data_ptr(),
             self.f_tile.data_ptr(), self.ctr.data_ptr(), int(count_only), EXCHANGE_NEUTRAL,
             self.stream.cuda_stream), "pgx_apply_slice")
-        c = self.ctr[:24].view(torch.int64)  # packed, recip, bcast
-        packed = c[0]
-        return torch.stack([c[1], c[2], packed >> 32, packed & 0xFFFFFFFF])
+        return self.ctr[:24].view(torch.int64)  # the raw block: packed, recip, bcast
+
+    @staticmethod
+    def decode_counts(row):
+        """(recipients, broadcasts, senders, edges) of a raw counter block."""
+        packed = row[0] & 0xFFFFFFFFFFFFFFFF
+        return row[1], row[2], packed >> 32, packed & 0xFFFFFFFF
 
     def set_frontier(self, senders: int, edges: int):
         self.nsrc, self.E = int(senders), int(edges)

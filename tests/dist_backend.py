@@ -184,6 +184,10 @@ class CpuBackend:
         return torch.tensor([rec, int(imp.sum()), int(lv.size), int(self.deg[lv].sum())],
                             dtype=torch.int64)
 
+    @staticmethod
+    def decode_counts(row):
+        return tuple(row)
+
     def set_frontier(self, senders, edges):
         pass  # the CPU stand-in keeps its frontier as arrays
 
