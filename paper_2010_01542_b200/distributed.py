@@ -188,8 +188,12 @@ class PartitionedRun:
             if part.numel():
                 self.dist.reduce(part, dst=r, op=op)
 
-    def _exchange_min(self, op) -> str:
+    def _exchange_min(self, op, allow_sparse: bool = True) -> str:
         """Dense per-owner reduction or sparse pair exchange (collective choice)."""
+        if not allow_sparse:  # a big superstep: dense, no count, no host sync
+            self._reduce_slices(op)
+            self.b.dense_exchanged()
+            return "dense"
         touched = self.b.touched_count()
         t = torch.tensor([touched], dtype=torch.int64, device=self._cdev)
         self.dist.all_reduce(t, op=self.dist.ReduceOp.MAX)
@@ -275,8 +279,8 @@ class PartitionedRun:
             if use_peer:
                 self._fence()
                 exchange = "peer"
-            else:
-                exchange = self._exchange_min(op)
+            else:  # auto with the peer path mapped: only big supersteps get here
+                exchange = self._exchange_min(op, allow_sparse=not peer_ok)
             self.b.exchanged(exchange)
             at_cap = s + 1 == max_steps
             nxt = self._gather_counts(self.b.apply_min(app, count_only=at_cap))
