@@ -122,6 +122,7 @@ __device__ unsigned long long apply_min_phase(const int32_t *__restrict__ row_pt
         for (int j = 0; j < kApplyItems; j++) {
           const int idx = b0 + j * kBlock + threadIdx.x;
           v[j] = (idx < cnt) ? s_list[idx] : -1;
+          PGX_ASSERT(v[j] < n);
         }
 #if PGX_APPLY_SPEC
         // every load of the batch in one round trip: the row pointers are
@@ -191,6 +192,7 @@ __device__ unsigned long long apply_min_phase(const int32_t *__restrict__ row_pt
             if (deg[j] > 0) {
               const unsigned pos = (unsigned)(run >> 32);
               const int eb = (int)(run & 0xFFFFFFFFull);
+              PGX_ASSERT(pos < (unsigned)n && (int64_t)eb + deg[j] <= (int64_t)INT32_MAX);
               ws.f_eb[pos] = eb;
               ws.f_rs[pos] = rs[j];
               f_msg[pos] = (APP == PGX_APP_SSSP) ? m[j] + 1u : m[j];

@@ -26,6 +26,21 @@
 #define PGX_PASS 4           // 32-edge rounds in flight per scatter pass
 #endif
 
+// Checked build (-DPGX_DEBUG_CHECKS=1): every index the hot phases compute
+// is bounds-checked on the device; a violation prints and traps (the run
+// fails with a CUDA error).  compute-sanitizer is not available on the
+// test pool, so the GPU suite runs against this build instead.
+#ifndef PGX_DEBUG_CHECKS
+#define PGX_DEBUG_CHECKS 0
+#endif
+#define PGX_ASSERT(c)                                                      \
+  do {                                                                     \
+    if (PGX_DEBUG_CHECKS && !(c)) {                                        \
+      printf("PGX_ASSERT failed %s:%d: %s\n", __FILE__, __LINE__, #c);     \
+      __trap();                                                            \
+    }                                                                      \
+  } while (0)
+
 namespace pgx {
 
 constexpr int kBlock = 512;          // threads per CTA
@@ -302,6 +317,7 @@ struct ScatterArgs {
   int32_t nhubs;          // (sign bit | slot).  nhubs == 0: no hub cache
   int32_t cas_loop;       // ablation: CAS retry loop instead of red.min
   uint32_t neutral;       // min neutral of the mailbox (has-bit publication)
+  int32_t n;              // vertex bound of col_idx values (checked builds)
   // fused peer-memory exchange (pgx_scatter_peer): a message that passes
   // the local filter and whose recipient another rank owns is also
   // combined into the owner's mailbox, peer_mb[owner] (NVLink P2P)

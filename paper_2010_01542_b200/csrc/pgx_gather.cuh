@@ -27,6 +27,7 @@ struct GatherArgs {
   int64_t E;
   const double *share;      // shares broadcast last superstep
   double *folded, *head, *tail;
+  int32_t n;                // vertex bound of in_col values (checked builds)
 };
 
 __device__ __forceinline__ void gather_phase(const GatherArgs &a, char *smem) {
@@ -45,6 +46,7 @@ __device__ __forceinline__ void gather_phase(const GatherArgs &a, char *smem) {
     const int i0 = a.tile_src[t];
     const int i1 = (t + 1 < ntiles) ? a.tile_src[t + 1] : a.nsrc - 1;
     const int k = i1 - i0 + 1;
+    PGX_ASSERT(i0 >= 0 && k >= 1 && k <= kTile + 1 && i1 < a.nsrc);
     __syncwarp();
     for (int j = lane; j <= k; j += 32) {
       const int i = i0 + j;
@@ -72,7 +74,10 @@ __device__ __forceinline__ void gather_phase(const GatherArgs &a, char *smem) {
     }
     double x[8];
 #pragma unroll
-    for (int j = 0; j < 8; j++) x[j] = (col[j] >= 0) ? __ldg(a.share + col[j]) : 0.0;
+    for (int j = 0; j < 8; j++) {
+      PGX_ASSERT(col[j] < a.n);
+      x[j] = (col[j] >= 0) ? __ldg(a.share + col[j]) : 0.0;
+    }
     // row holding a0: largest idx with s_eb[idx] <= a0 (binary search over
     // the <= 258 staged row starts), then the starts of the next 8 rows as
     // a boundary bitmask over the lane's 9 positions a0..a0+8, so the walk

@@ -119,6 +119,7 @@ __global__ void __launch_bounds__(kBlock, PGX_MIN_BLOCKS) min_run_kernel(MinRunP
     a.nhubs = p.nhubs;
     a.cas_loop = p.cas_loop;
     a.neutral = kNeutralMin;
+    a.n = p.n;
     if (APP == PGX_APP_CC && s == 0) {
       a.eb = p.g.nz_eb;
       a.rs = nullptr;
@@ -263,6 +264,7 @@ __global__ void __launch_bounds__(kBlock, PGX_MIN_BLOCKS) pagerank_run_kernel(Pr
   a.nhubs = 0;
   a.cas_loop = 0;
   a.neutral = 0u;
+  a.n = p.n;
   const unsigned long long ndangling = p.ws.misc[0];
   double dangling = __dmul_rn(p.r0, (double)ndangling);  // algorithms.py:55
   const int64_t nspread = (int64_t)p.n - (int64_t)ndangling;
@@ -382,6 +384,7 @@ __global__ void __launch_bounds__(kBlock, PGX_MIN_BLOCKS) pagerank_pull_kernel(P
   g.folded = folded;
   g.head = p.ws.head;
   g.tail = p.ws.tail;
+  g.n = p.n;
 
   for (int s = 0;; s++) {
     if (blockIdx.x == 0 && threadIdx.x == 0)

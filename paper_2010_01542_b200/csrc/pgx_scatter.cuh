@@ -92,6 +92,7 @@ __device__ void scatter_phase(const ScatterArgs &a, char *smem, bool read_filter
     const int i0 = a.tile_src[t];
     const int i1 = (t + 1 < ntiles) ? a.tile_src[t + 1] : a.nsrc - 1;
     const int k = i1 - i0 + 1;  // <= kTile + 1
+    PGX_ASSERT(i0 >= 0 && k >= 1 && k <= kTile + 1 && i1 < a.nsrc);
     __syncwarp();
     for (int j = lane; j <= k; j += 32) {
       const int i = i0 + j;
@@ -132,6 +133,7 @@ __device__ void scatter_phase(const ScatterArgs &a, char *smem, bool read_filter
         cur += __popc(bm);
         w[r] = kInvalidEdge;
         if (e < e1) {
+          PGX_ASSERT(src >= 0 && src < k);
           int64_t pos = e;
           if (kDense) {
             mv[r] = s_msg[src];
@@ -141,6 +143,7 @@ __device__ void scatter_phase(const ScatterArgs &a, char *smem, bool read_filter
             mv[r] = (Msg)om.y;
           }
           w[r] = ld_stream(a.col + pos, pol);
+          PGX_ASSERT(w[r] < 0 || w[r] < a.n);
         }
       }
       if (OP == PGX_OP_MIN_U32 && BFS) {

@@ -275,6 +275,7 @@ int pgx_scatter(int op, int dense, const int32_t *col_idx, const int32_t *src_eb
   a.nhubs = 0;
   a.cas_loop = 0;
   a.neutral = neutral;
+  a.n = INT32_MAX;  // the slice ABI has no vertex count: unchecked
   const int64_t tiles = ceil_div(edges, kTile);
   int sms = 148, dev = 0;
   if (cudaGetDevice(&dev) == cudaSuccess)
@@ -332,6 +333,7 @@ int pgx_scatter_peer(int dense, const int32_t *col_idx, const int32_t *src_eb,
   a.nhubs = 0;
   a.cas_loop = 0;
   a.neutral = neutral;
+  a.n = INT32_MAX;  // the slice ABI has no vertex count: unchecked
   a.peer_mb = reinterpret_cast<uint32_t *const *>(peer_mailboxes);
   a.bounds = bounds;
   a.world = world;

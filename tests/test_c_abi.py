@@ -17,7 +17,7 @@ from paper_2010_01542_b200 import _lib
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 SRC = os.path.join(ROOT, "tests", "c_abi", "pgx_c_smoke.c")
-LIBDIR = os.path.dirname(_lib.LIB_PATH)
+LIBDIR = os.path.join(ROOT, "paper_2010_01542_b200")  # the in-tree libpgx.so
 CUDA = "/usr/local/cuda"
 
 
