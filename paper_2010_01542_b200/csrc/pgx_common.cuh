@@ -22,6 +22,9 @@
 #ifndef PGX_PREFETCH
 #define PGX_PREFETCH 1       // dense scatter: L2 bulk prefetch of the next tile's ids
 #endif
+#ifndef PGX_DYN_TILES
+#define PGX_DYN_TILES 1      // warps claim tiles from a per-CTA counter (strided tiles)
+#endif
 #ifndef PGX_PASS
 #define PGX_PASS 4           // 32-edge rounds in flight per scatter pass
 #endif

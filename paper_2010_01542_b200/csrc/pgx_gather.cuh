@@ -37,10 +37,23 @@ __device__ __forceinline__ void gather_phase(const GatherArgs &a, char *smem) {
   int32_t *s_id = reinterpret_cast<int32_t *>(smem) + kWarps * kSlots + warp * kSlots;
   const uint64_t pol = evict_first_policy();
   const int64_t ntiles = (a.E + kTile - 1) / kTile;
+#if PGX_DYN_TILES  // the scatter's tile schedule (pgx_scatter.cuh)
+  __shared__ unsigned s_tctr;
+  if (threadIdx.x == 0) s_tctr = 0u;
+  __syncthreads();
+  auto claim = [&]() -> int64_t {
+    unsigned c = 0u;
+    if (lane == 0) c = atomicAdd(&s_tctr, 1u);
+    c = __shfl_sync(0xFFFFFFFFu, c, 0);
+    const int64_t tt = (int64_t)blockIdx.x + (int64_t)c * gridDim.x;
+    return tt < ntiles ? tt : -1;
+  };
+  for (int64_t t = claim(); t >= 0; t = claim()) {
+#else
   const int64_t gwarp = (int64_t)blockIdx.x * kWarps + warp;
   const int64_t nwarps = (int64_t)gridDim.x * kWarps;
-
   for (int64_t t = gwarp; t < ntiles; t += nwarps) {
+#endif
     const int64_t e0 = t * kTile;
     const int64_t e1 = min(a.E, e0 + kTile);
     const int i0 = a.tile_src[t];

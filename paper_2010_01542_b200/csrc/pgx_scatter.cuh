@@ -60,8 +60,6 @@ __device__ void scatter_phase(const ScatterArgs &a, char *smem, bool read_filter
   const uint64_t pol = evict_first_policy();
   const int64_t ntiles = (a.E + kTile - 1) / kTile;
   const unsigned upto = (lane == 31) ? 0xFFFFFFFFu : ((2u << lane) - 1u);
-  const int64_t gwarp = (int64_t)blockIdx.x * kWarps + warp;
-  const int64_t nwarps = (int64_t)gridDim.x * kWarps;
   uint32_t *s_hub = reinterpret_cast<uint32_t *>(smem + scatter_windows_smem(OP));
 #if PGX_COUNT_OPS
   unsigned long long c_ops[3] = {0ull, 0ull, 0ull};
@@ -71,16 +69,42 @@ __device__ void scatter_phase(const ScatterArgs &a, char *smem, bool read_filter
     __syncthreads();
   }
 
-  for (int64_t t = gwarp; t < ntiles; t += nwarps) {
+#if PGX_DYN_TILES
+  // Tile schedule: CTA b owns tiles b, b + grid, b + 2 grid, ... (spread
+  // over the whole edge space, like a static stride) and its warps claim
+  // them one at a time from a shared-memory counter (no global atomics), so
+  // a slow tile delays only its own warp's next claim, not a fixed share.
+  __shared__ unsigned s_tctr;
+  if (threadIdx.x == 0) s_tctr = 0u;
+  __syncthreads();
+  auto claim = [&]() -> int64_t {
+    unsigned c = 0u;
+    if (lane == 0) c = atomicAdd(&s_tctr, 1u);
+    c = __shfl_sync(0xFFFFFFFFu, c, 0);
+    const int64_t tt = (int64_t)blockIdx.x + (int64_t)c * gridDim.x;
+    return tt < ntiles ? tt : -1;
+  };
+  int64_t t = claim();
+#else
+  const int64_t gwarp = (int64_t)blockIdx.x * kWarps + warp;
+  const int64_t nwarps = (int64_t)gridDim.x * kWarps;
+  int64_t t = gwarp < ntiles ? gwarp : -1;
+#endif
+  while (t >= 0) {
+#if PGX_DYN_TILES
+    const int64_t tnext = claim();  // one ahead: its ids can be prefetched
+#else
+    const int64_t tnext = t + nwarps < ntiles ? t + nwarps : -1;
+#endif
     const int64_t e0 = t * kTile;
     const int64_t e1 = min(a.E, e0 + kTile);
 #if PGX_PREFETCH
     // the warp's next tile: its neighbour ids (dense: one contiguous 1 KB
     // run of col_idx) are pulled into L2 while this tile is processed
-    if (kDense && lane == 0 && t + nwarps < ntiles) {
+    if (kDense && lane == 0 && tnext >= 0) {
       // the bulk prefetch needs 16-byte granules: widen the range (col_idx
       // itself may be any 4-byte-aligned view, e.g. a rank's slice)
-      const int64_t en = (t + nwarps) * kTile;
+      const int64_t en = tnext * kTile;
       const uint64_t p0 = reinterpret_cast<uint64_t>(a.col + en) & ~15ull;
       const uint64_t p1 =
           (reinterpret_cast<uint64_t>(a.col + min(a.E, en + kTile)) + 15ull) & ~15ull;
@@ -229,6 +253,7 @@ __device__ void scatter_phase(const ScatterArgs &a, char *smem, bool read_filter
           if (w[r] != kInvalidEdge) atomicAdd(mb + w[r], (double)mv[r]);
       }
     }
+    t = tnext;
   }
 #if PGX_COUNT_OPS
   for (int i = 0; i < 3; i++)
