@@ -206,8 +206,12 @@ def ncu_traffic(tag: str):
     """DRAM bytes per launch of the headline kernel from the committed ncu
     summary (profiles/ncu_<tag>_*.json, newest), else None."""
     import glob
-    files = sorted(glob.glob(os.path.join(ROOT, "profiles", f"ncu_{tag}_*.json")),
-                   )
+    import re
+
+    def version(f):  # numeric: _v10 is newer than _v9
+        m = re.search(r"_v(\d+)\.json$", f)
+        return int(m.group(1)) if m else -1
+    files = sorted(glob.glob(os.path.join(ROOT, "profiles", f"ncu_{tag}_*.json")), key=version)
     if not files:
         return None, None
     try:
