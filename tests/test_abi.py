@@ -95,3 +95,8 @@ def test_pull_pagerank_rejects_a_misaligned_in_col():
                                    10, fake, fake, 1 << 20, fake, 0)
     assert rc == _lib.PGX_EINVAL
     assert b"32-byte aligned" in lib.pgx_last_error()
+
+
+def test_integration_doc_covers_every_entry_point():
+    doc = open(os.path.join(ROOT, "INTEGRATION.md")).read()
+    assert [s for s in _lib.EXPORTS if s not in doc] == []
