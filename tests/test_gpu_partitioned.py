@@ -109,3 +109,28 @@ def test_partition_slices_at_unaligned_offsets(exchange):
     assert np.array_equal(vals.cpu().numpy().view(np.uint32).astype(np.int64),
                           want.values.astype(np.int64))
     assert [s["active_count"] for s in stats] == want.active_counts
+
+
+@pytest.mark.parametrize("world", [2, 4])
+def test_partitioned_c2_full_size_known_answer(world):
+    """BASELINE config C2 (65M edges) through the partitioned superstep:
+    the labels hash and per-superstep counts of BASELINE.md, bit-exact."""
+    import hashlib
+    from paper_2010_01542_b200.rmat import rmat_graph
+    g = rmat_graph("C2")
+    n, m = g.vertex_count, g.edge_count
+    bounds = partition_bounds(torch.diff(g.out_offsets).cpu().numpy(), world)
+
+    def rank_fn(r, d):
+        be = CudaBackend(g, int(bounds[r]), int(bounds[r + 1]), "cuda:0")
+        run = PartitionedRun(be, d, bounds, n, m)
+        return run.run_min("components", 0, 10_000)
+    vals, stats, hit, _ = run_ranks(world, rank_fn)[0]
+    lab = vals.cpu().numpy().view(np.uint32)
+    assert hashlib.sha256(lab.astype("<u4").tobytes()).hexdigest() == \
+        "c4e2cc1d7b5db62b9818e1cd41611649a294c5623d7e29804c175f904c40bf98"
+    assert [s["active_count"] for s in stats] == \
+        [4194304, 2009754, 2004276, 1499157, 208894, 2173, 23]
+    assert [s["edges"] for s in stats] == \
+        [65242574, 64803511, 28608953, 348075, 2192, 23, 0]
+    assert {s["exchange"] for s in stats} == {"dense", "peer"}
