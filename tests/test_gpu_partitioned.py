@@ -134,3 +134,37 @@ def test_partitioned_c2_full_size_known_answer(world):
     assert [s["edges"] for s in stats] == \
         [65242574, 64803511, 28608953, 348075, 2192, 23, 0]
     assert {s["exchange"] for s in stats} == {"dense", "peer"}
+
+
+def test_partitioned_c3_and_c4_full_size():
+    """C3 SSSP (distances hash of BASELINE.md) and C4 PageRank (per-vertex
+    relative error <= 1e-9 against the single-GPU pull run, rank[0] of
+    BASELINE.md) through the partitioned superstep with 3 ranks."""
+    import hashlib
+    from paper_2010_01542_b200.rmat import rmat_graph
+    world = 3
+    for cfg in ("C3", "C4"):
+        g = rmat_graph(cfg)
+        n, m = g.vertex_count, g.edge_count
+        bounds = partition_bounds(torch.diff(g.out_offsets).cpu().numpy(), world)
+
+        def rank_fn(r, d):
+            be = CudaBackend(g, int(bounds[r]), int(bounds[r + 1]), "cuda:0")
+            run = PartitionedRun(be, d, bounds, n, m)
+            if cfg == "C3":
+                return run.run_min("sssp", 0, 10_000)
+            return run.run_pagerank(10, 0.85, 10_000)
+        vals, stats, hit, _ = run_ranks(world, rank_fn)[0]
+        if cfg == "C3":
+            d = vals.cpu().numpy().view(np.uint32)
+            assert hashlib.sha256(d.astype("<u4").tobytes()).hexdigest() == \
+                "bd08774026f70bbd29b80c977187f880654c0d8cbd2b42ba0988fed279ffa1e2"
+            assert [s["messages_sent"] for s in stats] == \
+                [97364, 36379100, 27861844, 339319, 2142, 6, 0]
+        else:
+            got = vals.cpu().numpy()
+            want = pgx.run(g, pgx.pagerank()).values
+            assert np.max(np.abs(got - want) / np.abs(want)) <= 1e-9
+            assert abs(got[0] - 0.0001216244232021811) / 0.0001216244232021811 <= 1e-9
+        del g
+        torch.cuda.empty_cache()
