@@ -43,3 +43,34 @@ def test_c5_components_known_answer():
         [1844208942, 1838211760, 801105854, 5102558, 15802, 43, 0]
     del g, rep
     torch.cuda.empty_cache()
+
+
+def test_c5_partitioned_known_answer():
+    """C5 -- BASELINE.json's 1/2/4/8-GPU config -- through the partitioned
+    superstep with 2 ranks (threads sharing the one GPU of the test box; the
+    default exchange: dense collective for the big supersteps, fused peer
+    exchange for the rest): the same labels hash and per-superstep counts."""
+    if torch.cuda.get_device_properties(0).total_memory < 120 * 2 ** 30:
+        pytest.skip("needs a 180 GB B200")
+    import sys, os
+    sys.path.insert(0, os.path.dirname(os.path.abspath(__file__)))
+    from thread_dist import run_ranks
+    from paper_2010_01542_b200.distributed import (CudaBackend, PartitionedRun,
+                                                   partition_bounds)
+    torch.cuda.empty_cache()
+    g = rmat_graph("C5")
+    n, m = g.vertex_count, g.edge_count
+    bounds = partition_bounds(torch.diff(g.out_offsets).cpu().numpy(), 2)
+
+    def rank_fn(r, d):
+        be = CudaBackend(g, int(bounds[r]), int(bounds[r + 1]), "cuda:0")
+        return PartitionedRun(be, d, bounds, n, m).run_min("components", 0, 10_000)
+    vals, stats, hit, _ = run_ranks(2, rank_fn)[0]
+    assert sha(vals.view(torch.int32), "<u4") == \
+        "2667f2ecc3e6e7cb00c5c53f2b8af394b2802cbd19de2a9e1b8122490b4b1154"
+    assert [s["active_count"] for s in stats] == \
+        [67108864, 31691446, 31654625, 24001955, 2770014, 15744, 43]
+    assert [s["edges"] for s in stats] == \
+        [1844208942, 1838211760, 801105854, 5102558, 15802, 43, 0]
+    del g
+    torch.cuda.empty_cache()
