@@ -76,7 +76,7 @@ __global__ void __launch_bounds__(kBlock, PGX_MIN_BLOCKS) min_run_kernel(MinRunP
   // ---- setup (algorithms.py:96-97 / 129-134) + superstep-0 senders ----
   for (unsigned v = gtid; v < (unsigned)p.n; v += nthreads) {
     *slot<S>(val, v) = (APP == PGX_APP_CC) ? v : kNeutralMin;
-    *slot<S>(mailbox, v) = kNeutralMin;
+    if (!BFS) *slot<S>(mailbox, v) = kNeutralMin;  // the bitmap kernel has no mailbox
   }
   for (unsigned wi = gtid; wi < (unsigned)(p.n / 32 + 2); wi += nthreads) p.ws.has[wi] = 0u;
   if (blockIdx.x == 0 && threadIdx.x == 0) {
