@@ -168,3 +168,54 @@ def test_partitioned_c3_and_c4_full_size():
             assert abs(got[0] - 0.0001216244232021811) / 0.0001216244232021811 <= 1e-9
         del g
         torch.cuda.empty_cache()
+
+
+def _adversarial(rng):
+    yield "star_out", np.zeros(499, int), np.arange(1, 500), 500, False
+    yield "star_in", np.arange(1, 500), np.zeros(499, int), 500, False
+    yield "isolated_heavy", np.array([3, 3, 7]), np.array([7, 9, 3]), 4000, True
+    yield "tiny_many_ranks", np.array([0, 1]), np.array([1, 2]), 3, True
+    for i in range(8):
+        n = int(rng.integers(2, 5000))
+        m = int(rng.integers(0, 8 * n))
+        if i % 2:
+            p = 1.0 / np.arange(1, n + 1) ** 1.1
+            p /= p.sum()
+            src, dst = rng.choice(n, m, p=p), rng.choice(n, m, p=p)
+        else:
+            src, dst = rng.integers(0, n, m), rng.integers(0, n, m)
+        yield f"random{i}", src, dst, n, bool(i % 3 == 0)
+
+
+@pytest.mark.parametrize("case", list(_adversarial(np.random.default_rng(99))),
+                         ids=lambda c: c[0])
+def test_partitioned_randomized_vs_oracle(case):
+    """Adversarial shapes for the partition: ranks whose range is empty,
+    hubs owning a whole range, isolated vertices, more ranks than vertices;
+    CC / SSSP exact with per-superstep counts, PageRank <= 1e-9."""
+    name, src, dst, n, und = case
+    off, tgt = O.csr_from_edges(src, dst, n, und)
+    g = pgx.from_csr(torch.from_numpy(off).cuda(), torch.from_numpy(tgt).cuda())
+    source = int(np.argmax(np.diff(off)))
+    want = {"components": O.run_cc(n, off, tgt), "sssp": O.run_sssp(n, off, tgt, source),
+            "pagerank": O.run_pagerank(n, off, tgt)}
+    for world, exchange in ((2, "auto"), (3, "peer"), (5, "hybrid"), (7, "auto")):
+        bounds = partition_bounds(np.diff(off), world)
+        for app in ("components", "sssp", "pagerank"):
+            def rank_fn(r, d):
+                be = CudaBackend(g, int(bounds[r]), int(bounds[r + 1]), "cuda:0")
+                run = PartitionedRun(be, d, bounds, n, int(tgt.size))
+                run.exchange = exchange
+                if app == "pagerank":
+                    return run.run_pagerank(10, 0.85, 10_000)
+                return run.run_min(app, source, 10_000)
+            vals, stats, hit, _ = run_ranks(world, rank_fn)[0]
+            w = want[app]
+            v = vals.cpu().numpy()
+            if app == "pagerank":
+                assert np.max(np.abs(v - w.values) / np.abs(w.values)) <= 1e-9, (name, world)
+            else:
+                assert np.array_equal(v.view(np.uint32).astype(np.int64),
+                                      w.values.astype(np.int64)), (name, world, app)
+                assert [s["active_count"] for s in stats] == w.active_counts, (name, world, app)
+                assert [s["messages_sent"] for s in stats] == w.messages_sent, (name, world, app)
