@@ -111,8 +111,8 @@ def _adversarial_graphs(rng):
     yield "dup_edges", np.repeat([0, 1, 2], 50), np.repeat([1, 2, 0], 50), 3, False
     yield "two_hubs", np.r_[np.zeros(600, int), np.full(600, 1)], \
         np.r_[np.arange(600) + 2, np.arange(600) + 2], 602, False
-    for i in range(10):
-        n = int(rng.integers(2, 3000))
+    for i in range(25):
+        n = int(rng.integers(2, 3000 if i < 10 else 30_000))
         m = int(rng.integers(0, 6 * n))
         skew = rng.random() < 0.5
         if skew:
