@@ -33,7 +33,7 @@
 extern "C" {
 #endif
 
-#define PGX_ABI_VERSION 2
+#define PGX_ABI_VERSION 3
 
 #define PGX_OK 0
 #define PGX_EINVAL (-1)   /* bad argument / unsupported configuration */
@@ -79,7 +79,9 @@ const char *pgx_last_error(void);
 #define PGX_OPT_CAS_LOOP 2      /* ablation: CAS retry loop per message (lock-style) */
 #define PGX_OPT_VERTEX_SCHED 3  /* ablation: one thread per sender (no edge balance) */
 #define PGX_OPT_LAYOUT 4        /* ablation: PGX_LAYOUT_* of the CC/SSSP vertex state */
-#define PGX_OPT_COUNT 5
+#define PGX_OPT_SEG_MIN_EDGES 5 /* segmented scatter when a superstep's senders hold at least
+                                   m * value / 1024 edges (0 = every superstep, 1025 = never; default 512) */
+#define PGX_OPT_COUNT 6
 
 /* PGX_OPT_LAYOUT values (LayoutMode, layout.py:31-33).  EXTERNALISED is the
  * default SoA (value[], mailbox[] apart).  INTERLEAVED keeps one {mailbox,
@@ -110,6 +112,57 @@ int pgx_graph_workspace_bytes(int64_t n, int64_t m, size_t *bytes);
 int pgx_graph_prepare(int32_t n, int64_t m, const int32_t *row_ptr,
                       void *graph_ws, size_t graph_ws_bytes,
                       uintptr_t stream);
+
+/* ---------------------------------------------------------------- */
+/* destination-segmented index (the dense supersteps' edge order) --   */
+/* graph preparation for the segmented scatter of pgx_cc_run_ex /      */
+/* pgx_sssp_run_ex, which combines every message of a dense superstep  */
+/* in a shared-memory copy of its recipient's mailbox segment (the     */
+/* paper's hybrid combiner, mailbox.py:180-199, for all recipients).   */
+/* The edges are regrouped by destination segment (2^seg_log2          */
+/* consecutive ids), CSR order kept inside a segment; an ENTRY is one  */
+/* source's run of edges into one segment.                             */
+/* ---------------------------------------------------------------- */
+
+typedef struct PgxSegIndex {
+  int32_t seg_log2;         /* segment = vertex >> seg_log2 (<= 16)        */
+  int32_t nent;             /* entries                                     */
+  int32_t nitems;           /* work items                                  */
+  int32_t reserved;
+  const int32_t *ent_src;   /* [nent]   source of each entry               */
+  const int32_t *ent_eb;    /* [nent+1] first edge (segment order); [nent] = m */
+  const uint16_t *col16;    /* [m+256]  destination - segment base         */
+  const int32_t *tile_ent;  /* [ceil(m/256)+1] entry holding edge 256 t    */
+  const int32_t *items;     /* [nitems][4] {segment, e0, e1, owns segment},
+                               16-byte aligned, largest first              */
+} PgxSegIndex;
+
+/* default segment size (8192 vertices: a 32 KB shared-memory mailbox) */
+#define PGX_SEG_LOG2_DEFAULT 13
+
+/* workspace bytes of pgx_seg_count / pgx_seg_build (nent < 0: the count
+ * step only) and the capacity the items array needs (host outs) */
+int pgx_seg_workspace_bytes(int32_t n, int64_t m, int64_t nent,
+                            int32_t seg_log2, size_t *bytes);
+int pgx_seg_max_items(int32_t n, int64_t m, int32_t seg_log2,
+                      int32_t *max_items);
+
+/* step 1 (syncs): the number of entries into *nent (host out).  graph_ws
+ * is the pgx_graph_prepare workspace of (row_ptr, col_idx). */
+int pgx_seg_count(int32_t n, int64_t m, const int32_t *row_ptr,
+                  const int32_t *col_idx, const void *graph_ws,
+                  int32_t seg_log2, void *ws, size_t ws_bytes,
+                  int64_t *nent, uintptr_t stream);
+
+/* step 2 (syncs): fill the caller's arrays (sizes as in PgxSegIndex;
+ * items: pgx_seg_max_items x 4 int32) and *nitems (host out).  Items are
+ * cut for `ctas` persistent CTAs (0: the run kernels' grid). */
+int pgx_seg_build(int32_t n, int64_t m, const int32_t *row_ptr,
+                  const int32_t *col_idx, const void *graph_ws,
+                  int32_t seg_log2, int64_t nent, void *ws, size_t ws_bytes,
+                  int32_t *ent_src, int32_t *ent_eb, uint16_t *col16,
+                  int32_t *tile_ent, int32_t *items, int32_t *nitems,
+                  int32_t ctas, uintptr_t stream);
 
 /* ---------------------------------------------------------------- */
 /* whole runs on one GPU: one persistent cooperative kernel per run,   */
@@ -143,6 +196,21 @@ int pgx_cc_run(int32_t n, int64_t m, const int32_t *row_ptr,
                const int32_t *hub_ids, int32_t nhubs,
                int32_t max_supersteps, uint32_t *labels, void *run_ws,
                size_t run_ws_bytes, int64_t *stats, uintptr_t stream);
+
+/* the same runs with a segmented index (NULL: K1 for every superstep):
+ * supersteps whose senders hold enough edges (PGX_OPT_SEG_MIN_EDGES) run
+ * the segmented shared-memory scatter.  Results and statistics are
+ * identical; the index must describe (row_ptr, col_idx). */
+int pgx_sssp_run_ex(int32_t n, int64_t m, const int32_t *row_ptr,
+                    const int32_t *col_idx, const void *graph_ws,
+                    const PgxSegIndex *seg, int32_t source,
+                    int32_t max_supersteps, uint32_t *dist, void *run_ws,
+                    size_t run_ws_bytes, int64_t *stats, uintptr_t stream);
+int pgx_cc_run_ex(int32_t n, int64_t m, const int32_t *row_ptr,
+                  const int32_t *col_idx, const void *graph_ws,
+                  const PgxSegIndex *seg, int32_t max_supersteps,
+                  uint32_t *labels, void *run_ws, size_t run_ws_bytes,
+                  int64_t *stats, uintptr_t stream);
 
 /* pagerank(iterations, damping) -- algorithms.py:27-84 (fp64, sum).
  * base = (1 - damping) / n and r0 = 1 / n are passed in as computed by

@@ -16,13 +16,15 @@ from .errors import ConfigError, ExecutionError
 PKG_DIR = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.environ.get("PGX_LIB") or os.path.join(PKG_DIR, "libpgx.so")
 
-PGX_ABI_VERSION = 2
+PGX_ABI_VERSION = 3
 PGX_OK, PGX_EINVAL, PGX_ECUDA, PGX_ENOMEM = 0, -1, -2, -3
 PGX_APP_PAGERANK, PGX_APP_CC, PGX_APP_SSSP, PGX_APP_PAGERANK_PULL = 0, 1, 2, 3
 PGX_OP_MIN_U32, PGX_OP_SUM_F64 = 0, 1
 PGX_STAT_HDR, PGX_STAT_FIELDS = 4, 8
 PGX_OPT_READ_FILTER, PGX_OPT_CTAS_PER_SM, PGX_OPT_CAS_LOOP, PGX_OPT_VERTEX_SCHED = 0, 1, 2, 3
 PGX_OPT_LAYOUT = 4
+PGX_OPT_SEG_MIN_EDGES = 5
+PGX_SEG_LOG2_DEFAULT = 13
 PGX_IPC_HANDLE_BYTES = 64
 PGX_LAYOUT_EXTERNALISED, PGX_LAYOUT_INTERLEAVED = 0, 1
 
@@ -40,8 +42,19 @@ EXPORTS = (
     "pgx_slice_init", "pgx_scatter", "pgx_slice_counters_bytes", "pgx_apply_slice",
     "pgx_pr_apply_slice", "pgx_touched_scratch_bytes", "pgx_touched", "pgx_scatter_pairs",
     "pgx_scatter_peer", "pgx_reset_touched", "pgx_peer_alloc", "pgx_peer_open",
-    "pgx_peer_close", "pgx_peer_free",
+    "pgx_peer_close", "pgx_peer_free", "pgx_seg_workspace_bytes", "pgx_seg_max_items",
+    "pgx_seg_count", "pgx_seg_build", "pgx_sssp_run_ex", "pgx_cc_run_ex",
 )
+
+
+class PgxSegIndex(ctypes.Structure):
+    """include/pgx.h PgxSegIndex: the destination-segmented index."""
+
+    _fields_ = [("seg_log2", ctypes.c_int32), ("nent", ctypes.c_int32),
+                ("nitems", ctypes.c_int32), ("reserved", ctypes.c_int32),
+                ("ent_src", ctypes.c_void_p), ("ent_eb", ctypes.c_void_p),
+                ("col16", ctypes.c_void_p), ("tile_ent", ctypes.c_void_p),
+                ("items", ctypes.c_void_p)]
 
 _lib = None
 
@@ -90,6 +103,14 @@ _SIGS = {
     "pgx_pr_apply_slice": (ctypes.c_int, [_i32, _p, _p, _p, _p, _f64, _f64, _f64, _i32, _p,
                                           _up]),
     "pgx_microbench": (ctypes.c_int, [ctypes.c_int, _p, _i64, _i64, _u64, _p, _up]),
+    "pgx_seg_workspace_bytes": (ctypes.c_int, [_i32, _i64, _i64, _i32, _p]),
+    "pgx_seg_max_items": (ctypes.c_int, [_i32, _i64, _i32, _p]),
+    "pgx_seg_count": (ctypes.c_int, [_i32, _i64, _p, _p, _p, _i32, _p, _sz, _p, _up]),
+    "pgx_seg_build": (ctypes.c_int, [_i32, _i64, _p, _p, _p, _i32, _i64, _p, _sz, _p, _p, _p,
+                                     _p, _p, _p, _i32, _up]),
+    "pgx_sssp_run_ex": (ctypes.c_int, [_i32, _i64, _p, _p, _p, _p, _i32, _i32, _p, _p, _sz, _p,
+                                       _up]),
+    "pgx_cc_run_ex": (ctypes.c_int, [_i32, _i64, _p, _p, _p, _p, _i32, _p, _p, _sz, _p, _up]),
     "pgx_rmat_keys": (ctypes.c_int, [_i32, _i64, _i64, _f64, _f64, _f64, _u64, _i32,
                                      _i64, _i64, _p, _i64, _p, _up]),
 }

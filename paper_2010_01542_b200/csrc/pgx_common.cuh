@@ -258,6 +258,7 @@ struct RunWs {
   void *mailbox;           // [n]   u32 (min) or f64 (sum); pull PR: folded sums
   double *share2;          // pull PR: second share buffer
   double *head, *tail;     // pull PR: per-tile partials of tile-spanning rows
+  uint32_t *snd[2];        // [n/32+2] x 2 senders bitmaps (segmented scatter; min apps)
 };
 
 inline size_t run_ws_layout(int app, int64_t n, int64_t m, int32_t max_steps, RunWs *ws,
@@ -279,6 +280,7 @@ inline size_t run_ws_layout(int app, int64_t n, int64_t m, int32_t max_steps, Ru
   // interleaved layout (min programs): {mailbox, value} records
   w.mailbox = take(W * (size_t)(n + 1) * (interleaved && !pr ? 2 : 1));
   w.share2 = w.head = w.tail = nullptr;
+  w.snd[0] = w.snd[1] = nullptr;
   if (app == PGX_APP_PAGERANK_PULL) {
     w.share2 = (double *)take(sizeof(double) * (size_t)(n + 1));
     w.head = (double *)take(sizeof(double) * (size_t)(ceil_div(m, kTile) + 2));
@@ -289,6 +291,8 @@ inline size_t run_ws_layout(int app, int64_t n, int64_t m, int32_t max_steps, Ru
     w.f_rs = (int32_t *)take(sizeof(int32_t) * (size_t)(n + 1));
     w.has = (uint32_t *)take(sizeof(uint32_t) * (size_t)(n / 32 + 2));
     w.tile_src = (int32_t *)take(sizeof(int32_t) * (size_t)(ceil_div(m, kTile) + 2));
+    w.snd[0] = (uint32_t *)take(sizeof(uint32_t) * (size_t)(n / 32 + 2));
+    w.snd[1] = (uint32_t *)take(sizeof(uint32_t) * (size_t)(n / 32 + 2));
   } else {
     w.f_eb = w.f_rs = w.tile_src = nullptr;
     w.has = nullptr;

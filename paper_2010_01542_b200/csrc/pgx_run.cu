@@ -32,6 +32,7 @@
 #include "pgx_common.cuh"
 #include "pgx_gather.cuh"
 #include "pgx_scatter.cuh"
+#include "pgx_seg.cuh"
 
 namespace pgx {
 namespace {
@@ -57,6 +58,11 @@ struct MinRunParams {
   const int32_t *hub_ids;
   int32_t nhubs;
   int64_t *stats;
+  // segmented scatter (pgx_seg.cuh) for supersteps whose senders hold at
+  // least seg_min_edges edges; use_seg = 0: K1 only
+  PgxSegIndex seg;
+  int32_t use_seg;
+  int64_t seg_min_edges;
 };
 
 // S = 0: externalised SoA (value = the caller's output array); S = 1:
@@ -78,7 +84,11 @@ __global__ void __launch_bounds__(kBlock, PGX_MIN_BLOCKS) min_run_kernel(MinRunP
     *slot<S>(val, v) = (APP == PGX_APP_CC) ? v : kNeutralMin;
     if (!BFS) *slot<S>(mailbox, v) = kNeutralMin;  // the bitmap kernel has no mailbox
   }
-  for (unsigned wi = gtid; wi < (unsigned)(p.n / 32 + 2); wi += nthreads) p.ws.has[wi] = 0u;
+  for (unsigned wi = gtid; wi < (unsigned)(p.n / 32 + 2); wi += nthreads) {
+    p.ws.has[wi] = 0u;
+    p.ws.snd[0][wi] = 0u;
+    p.ws.snd[1][wi] = 0u;
+  }
   if (blockIdx.x == 0 && threadIdx.x == 0) {
     p.stats[0] = p.stats[1] = 0;
     p.stats[2] = gridDim.x;
@@ -102,7 +112,11 @@ __global__ void __launch_bounds__(kBlock, PGX_MIN_BLOCKS) min_run_kernel(MinRunP
     }
   }
   grid_sync<kArriveRed>(p.ws.bar, gen);
-  if (APP == PGX_APP_SSSP && gtid == 0) *slot<S>(val, p.source) = 0u;
+  if (APP == PGX_APP_SSSP && gtid == 0) {
+    *slot<S>(val, p.source) = 0u;
+    if (p.row_ptr[p.source + 1] > p.row_ptr[p.source])  // the superstep-0 sender
+      p.ws.snd[0][p.source >> 5] = 1u << (p.source & 31);
+  }
   // unit-weight SSSP on the shipped arm: the has-bit filter (scatter_phase);
   // the host launches the BFS instantiation only for the default options
   constexpr bool bfs = BFS && APP == PGX_APP_SSSP && S == 0;
@@ -110,6 +124,37 @@ __global__ void __launch_bounds__(kBlock, PGX_MIN_BLOCKS) min_run_kernel(MinRunP
 
   for (int s = 0;; s++) {
     // ---- scatter(s): senders push along out-edges into the mailbox ----
+    const unsigned long long packed_s = p.ws.ctr[s].packed;
+    const int64_t edges_s = (APP == PGX_APP_CC && s == 0) ? p.m
+                                                          : (int64_t)(packed_s & 0xFFFFFFFFull);
+    if (p.use_seg) {
+      // senders bitmap of superstep s + 1 (written by the next apply): last
+      // read by scatter(s - 1), clear it unless that superstep had no senders
+      if (s >= 1 && (p.ws.ctr[s - 1].packed >> 32) != 0ull) {
+        uint32_t *nx = p.ws.snd[(s + 1) & 1];
+        for (unsigned wi = gtid; wi < (unsigned)(p.n / 32 + 2); wi += nthreads) nx[wi] = 0u;
+      }
+    }
+    if (p.use_seg && edges_s >= p.seg_min_edges && edges_s > 0) {
+      // dense superstep: the segmented shared-memory scatter (pgx_seg.cuh)
+      SegPass sp;
+      sp.ix = p.seg;
+      sp.m = p.m;
+      sp.n = p.n;
+      sp.snd = p.ws.snd[s & 1];
+      sp.val = val;
+      sp.uniform = (uint32_t)s + 1u;
+      sp.mailbox = mailbox;
+      sp.has = p.ws.has;
+      sp.item_ctr = reinterpret_cast<unsigned *>(&p.ws.ctr[s].pad[0]);
+      sp.write_mailbox = !bfs;
+      if (APP == PGX_APP_CC && s == 0)
+        seg_scatter_phase<kSegSourceId>(sp, smem);
+      else if (bfs)
+        seg_scatter_phase<kSegUniform>(sp, smem);
+      else
+        seg_scatter_phase<kSegLabel>(sp, smem);
+    } else {
     ScatterArgs a;
     a.col = p.col;
     a.mailbox = mailbox;
@@ -148,6 +193,7 @@ __global__ void __launch_bounds__(kBlock, PGX_MIN_BLOCKS) min_run_kernel(MinRunP
       else
         scatter_phase<PGX_OP_MIN_U32, MsgSrc::kFrontier, S>(a, smem, p.read_filter);
     }
+    }
     if (blockIdx.x == 0 && threadIdx.x == 0) {
       StepCounters z = {};
       p.ws.ctr[s + 1] = z;
@@ -158,11 +204,12 @@ __global__ void __launch_bounds__(kBlock, PGX_MIN_BLOCKS) min_run_kernel(MinRunP
     // ---- apply(s+1): consume + compute + frontier build; at the cap the
     //      pending messages are only counted (engine.py:299-300) ----
     const bool at_cap = (s + 1 == p.max_steps);
+    uint32_t *snd_out = p.use_seg ? p.ws.snd[(s + 1) & 1] : nullptr;
     const unsigned long long rb =
         bfs ? apply_min_phase<APP, 0, true>(p.row_ptr, val, mailbox, p.n, p.ws, &p.ws.ctr[s + 1],
-                                            smem, at_cap, (uint32_t)s + 1u)
+                                            smem, at_cap, (uint32_t)s + 1u, snd_out)
             : apply_min_phase<APP, S>(p.row_ptr, val, mailbox, p.n, p.ws, &p.ws.ctr[s + 1], smem,
-                                      at_cap);
+                                      at_cap, 0u, snd_out);
     const unsigned bc = block_sum<unsigned>((unsigned)(rb & 0xFFFFFFFFull), s_red);
     const unsigned rc = block_sum<unsigned>((unsigned)(rb >> 32), s_red);
     if (threadIdx.x == 0) {
@@ -489,9 +536,19 @@ int pgx_run_workspace_bytes(int app, int64_t n, int64_t m, int32_t max_superstep
 static int min_run(int app, int32_t n, int64_t m, const int32_t *row_ptr, const int32_t *col_idx,
                    const void *graph_ws, const int32_t *hub_ids, int32_t nhubs,
                    int32_t source, int32_t max_supersteps, uint32_t *val,
-                   void *run_ws, size_t run_ws_bytes, int64_t *stats, uintptr_t stream) {
+                   void *run_ws, size_t run_ws_bytes, int64_t *stats, uintptr_t stream,
+                   const PgxSegIndex *seg = nullptr) {
   if (nhubs < 0 || nhubs > kHubs || (nhubs > 0 && !hub_ids))
     return fail(PGX_EINVAL, "hub count must be in [0, pgx_hub_capacity()]");
+  if (seg) {
+    if (seg->seg_log2 < 5 || seg->seg_log2 > 16 || seg->nent < 1 || seg->nent > m ||
+        seg->nitems < 1 || !seg->ent_src || !seg->ent_eb || !seg->col16 || !seg->tile_ent ||
+        !seg->items || reinterpret_cast<uintptr_t>(seg->items) % 16 ||
+        reinterpret_cast<uintptr_t>(seg->col16) % 16)
+      return fail(PGX_EINVAL, "malformed segmented index");
+  }
+  if (g_opt[PGX_OPT_VERTEX_SCHED] && nhubs > 0)
+    return fail(PGX_EINVAL, "the vertex-scheduled ablation arm has no hub cache");
   int rc = check_graph(n, m, row_ptr, col_idx, graph_ws);
   if (rc) return rc;
   if (max_supersteps < 1) return fail(PGX_EINVAL, "superstep cap must be >= 1");
@@ -519,11 +576,19 @@ static int min_run(int app, int32_t n, int64_t m, const int32_t *row_ptr, const 
   p.stats = stats;
   cudaStream_t st = (cudaStream_t)stream;
   PGX_CUDA(cudaMemsetAsync(p.ws.bar, 0, 64, st));
-  const size_t smem = scatter_smem(PGX_OP_MIN_U32, nhubs);
-  int grid = 0;
-  void *args[] = {&p};
   const bool bfs = PGX_SSSP_BFS && !p.interleaved && p.read_filter && !p.cas_loop &&
                    !p.vertex_sched && nhubs == 0;
+  // the segmented scatter runs on the shipped arm only (SoA, read-filter,
+  // fire-and-forget combines, edge-balanced tiles, no hub cache)
+  p.use_seg = seg && m > 0 && !p.interleaved && p.read_filter && !p.cas_loop && !p.vertex_sched &&
+              nhubs == 0 && g_opt[PGX_OPT_SEG_MIN_EDGES] <= 1024;
+  if (p.use_seg) p.seg = *seg;
+  else memset(&p.seg, 0, sizeof p.seg);
+  p.seg_min_edges = (m * (int64_t)g_opt[PGX_OPT_SEG_MIN_EDGES]) / 1024;
+  size_t smem = scatter_smem(PGX_OP_MIN_U32, nhubs);
+  if (p.use_seg) smem = std::max(smem, seg_smem_bytes(p.seg.seg_log2) + 16);
+  int grid = 0;
+  void *args[] = {&p};
   void (*kern)(MinRunParams) =
       app == PGX_APP_SSSP
           ? (p.interleaved ? min_run_kernel<PGX_APP_SSSP, 1>
@@ -542,6 +607,22 @@ int pgx_sssp_run(int32_t n, int64_t m, const int32_t *row_ptr, const int32_t *co
                  int64_t *stats, uintptr_t stream) {
   return min_run(PGX_APP_SSSP, n, m, row_ptr, col_idx, graph_ws, hub_ids, nhubs, source,
                  max_supersteps, dist, run_ws, run_ws_bytes, stats, stream);
+}
+
+int pgx_sssp_run_ex(int32_t n, int64_t m, const int32_t *row_ptr, const int32_t *col_idx,
+                    const void *graph_ws, const PgxSegIndex *seg, int32_t source,
+                    int32_t max_supersteps, uint32_t *dist, void *run_ws, size_t run_ws_bytes,
+                    int64_t *stats, uintptr_t stream) {
+  return min_run(PGX_APP_SSSP, n, m, row_ptr, col_idx, graph_ws, nullptr, 0, source,
+                 max_supersteps, dist, run_ws, run_ws_bytes, stats, stream, seg);
+}
+
+int pgx_cc_run_ex(int32_t n, int64_t m, const int32_t *row_ptr, const int32_t *col_idx,
+                  const void *graph_ws, const PgxSegIndex *seg, int32_t max_supersteps,
+                  uint32_t *labels, void *run_ws, size_t run_ws_bytes, int64_t *stats,
+                  uintptr_t stream) {
+  return min_run(PGX_APP_CC, n, m, row_ptr, col_idx, graph_ws, nullptr, 0, 0, max_supersteps,
+                 labels, run_ws, run_ws_bytes, stats, stream, seg);
 }
 
 int pgx_cc_run(int32_t n, int64_t m, const int32_t *row_ptr, const int32_t *col_idx,

@@ -18,6 +18,7 @@ honoured (applied to the final state on the host, engine.py:310-311).
 
 from __future__ import annotations
 
+import ctypes
 import time
 from dataclasses import dataclass, field
 from enum import Enum
@@ -79,6 +80,12 @@ class EngineConfig:
     #: the hub encoding from the second run on a device CSR (amortised graph
     #: preprocessing), "on" always, "off" never
     hub_cache: str = "off"
+    #: destination-segmented index for the dense supersteps of CC / SSSP
+    #: (shared-memory combine of every message, pgx_seg.cuh): "auto" builds
+    #: it for graphs that live on the GPU (graph preprocessing amortised
+    #: over runs; host graphs uploaded for one run use K1 throughout),
+    #: "on" always, "off" never.  Results and statistics are identical.
+    segments: str = "auto"
 
 
 @dataclass(frozen=True)
@@ -162,6 +169,8 @@ def _validate(program: VertexProgram, config: EngineConfig) -> None:
         raise ConfigError(f"bad pagerank_mode: {config.pagerank_mode!r}")
     if config.hub_cache not in ("auto", "on", "off"):
         raise ConfigError(f"bad hub_cache: {config.hub_cache!r}")
+    if config.segments not in ("auto", "on", "off"):
+        raise ConfigError(f"bad segments: {config.segments!r}")
     if program.comm_mode is CommMode.PUSH and program.combine is None:
         raise ConfigError("push-mode programs must declare a combine function")
     if config.combiner is CombinerKind.CAS and program.comm_mode is CommMode.PUSH \
@@ -223,6 +232,7 @@ class LaunchPlan:
     stream: Any
     pull: bool = False
     hubs: bool = False
+    seg: Any = None          # _lib.PgxSegIndex when the segmented scatter is on
 
     def _hub_args(self):
         c = self.csr
@@ -256,6 +266,18 @@ class LaunchPlan:
                                       self.values.data_ptr(), self.ws.data_ptr(),
                                       self.ws_bytes, self.stats.data_ptr(), sp)
             _lib.check(rc, "pgx_pagerank_run")
+        elif self.app == "components" and self.seg is not None:
+            rc = lib.pgx_cc_run_ex(c.n, c.m, c.row_ptr.data_ptr(), c.col_idx.data_ptr(),
+                                   c.ws.data_ptr(), ctypes.byref(self.seg), self.max_steps,
+                                   self.values.data_ptr(), self.ws.data_ptr(), self.ws_bytes,
+                                   self.stats.data_ptr(), sp)
+            _lib.check(rc, "pgx_cc_run_ex")
+        elif self.app == "sssp" and self.seg is not None:
+            rc = lib.pgx_sssp_run_ex(c.n, c.m, c.row_ptr.data_ptr(), c.col_idx.data_ptr(),
+                                     c.ws.data_ptr(), ctypes.byref(self.seg), self.low["source"],
+                                     self.max_steps, self.values.data_ptr(), self.ws.data_ptr(),
+                                     self.ws_bytes, self.stats.data_ptr(), sp)
+            _lib.check(rc, "pgx_sssp_run_ex")
         elif self.app == "components":
             col, hub_ids, nh = self._hub_args()
             rc = lib.pgx_cc_run(c.n, c.m, c.row_ptr.data_ptr(), col, c.ws.data_ptr(),
@@ -300,6 +322,17 @@ def plan_run(graph: Graph, program: VertexProgram,
                                   (config.hub_cache == "auto" and csr.runs >= 1))
     if hubs:
         csr.ensure_hubs(stream)
+    seg = None
+    # "auto": CC on device-resident graphs.  Unit-weight SSSP keeps K1: its
+    # has-bitmap filter already hits L1, and its frontier
+    # supersteps (a hub's 36M edges from 97K senders on C3) would pay a scan
+    # of every entry
+    if app != "pagerank" and not hubs and csr.m > 0 and (
+            config.segments == "on" or
+            (config.segments == "auto" and app == "components"
+             and graph.device.type == "cuda")):
+        csr.ensure_segments(stream)
+        seg = csr.seg
     csr.runs += 1
     app_id = _lib.PGX_APP_PAGERANK_PULL if pull else _APP_ID[app]
     ws_bytes = _lib.out_size(lib.pgx_run_workspace_bytes, app_id, n, m, max_steps)
@@ -309,7 +342,8 @@ def plan_run(graph: Graph, program: VertexProgram,
                             dtype=torch.int64, device=dev)
         vdt = torch.float64 if app == "pagerank" else torch.int32
         values = torch.empty(n, dtype=vdt, device=dev)
-    return LaunchPlan(app, csr, values, stats, ws, ws_bytes, max_steps, low, stream, pull, hubs)
+    return LaunchPlan(app, csr, values, stats, ws, ws_bytes, max_steps, low, stream, pull, hubs,
+                      seg)
 
 
 def collect(plan: LaunchPlan, program: VertexProgram, wall: float | None = None) -> RunReport:

@@ -64,6 +64,51 @@ class DeviceCSR:
     hub_col: torch.Tensor | None = None      # col_idx with hub edges encoded
     hub_ids: torch.Tensor | None = None      # hub slot -> vertex
     runs: int = 0                            # device runs on this CSR
+    seg: object = None                       # _lib.PgxSegIndex (segmented scatter)
+    seg_arrays: tuple = ()                   # the tensors seg points into
+
+    def ensure_segments(self, stream=None, seg_log2: int | None = None) -> None:
+        """Build the destination-segmented index (pgx_seg_count /
+        pgx_seg_build: run detection, stable radix sort by segment, 16-bit
+        destinations, tile map, work items) once per graph and device.
+        Graph preprocessing, like the tile map and the in-CSR."""
+        if self.seg is not None or self.m == 0:
+            return
+        dev = self.row_ptr.device
+        st = torch.cuda.current_stream(dev) if stream is None else stream
+        lib = _lib.load()
+        L = _lib.PGX_SEG_LOG2_DEFAULT if seg_log2 is None else int(seg_log2)
+        n, m = self.n, self.m
+        with torch.cuda.device(dev), torch.cuda.stream(st):
+            sp = st.cuda_stream
+            ws = torch.empty(_lib.out_size(lib.pgx_seg_workspace_bytes, n, m, -1, L),
+                             dtype=torch.uint8, device=dev)
+            nent = ctypes.c_int64(0)
+            _lib.check(lib.pgx_seg_count(n, m, self.row_ptr.data_ptr(), self.col_idx.data_ptr(),
+                                         self.ws.data_ptr(), L, ws.data_ptr(), ws.numel(),
+                                         ctypes.byref(nent), sp), "pgx_seg_count")
+            ne = int(nent.value)
+            del ws
+            ws = torch.empty(_lib.out_size(lib.pgx_seg_workspace_bytes, n, m, ne, L),
+                             dtype=torch.uint8, device=dev)
+            cap = ctypes.c_int32(0)
+            _lib.check(lib.pgx_seg_max_items(n, m, L, ctypes.byref(cap)), "pgx_seg_max_items")
+            ent_src = torch.empty(ne, dtype=torch.int32, device=dev)
+            ent_eb = torch.empty(ne + 1, dtype=torch.int32, device=dev)
+            col16 = torch.empty(m + 256, dtype=torch.int16, device=dev)
+            tile_ent = torch.empty((m + 255) // 256 + 1, dtype=torch.int32, device=dev)
+            items = torch.empty(4 * int(cap.value), dtype=torch.int32, device=dev)
+            nitems = ctypes.c_int32(0)
+            _lib.check(lib.pgx_seg_build(n, m, self.row_ptr.data_ptr(), self.col_idx.data_ptr(),
+                                         self.ws.data_ptr(), L, ne, ws.data_ptr(), ws.numel(),
+                                         ent_src.data_ptr(), ent_eb.data_ptr(), col16.data_ptr(),
+                                         tile_ent.data_ptr(), items.data_ptr(),
+                                         ctypes.byref(nitems), 0, sp), "pgx_seg_build")
+            del ws
+        self.seg_arrays = (ent_src, ent_eb, col16, tile_ent, items)
+        self.seg = _lib.PgxSegIndex(L, ne, int(nitems.value), 0, ent_src.data_ptr(),
+                                    ent_eb.data_ptr(), col16.data_ptr(), tile_ent.data_ptr(),
+                                    items.data_ptr())
 
     def ensure_hubs(self, stream=None) -> None:
         """Encode the hub recipients for the scatter's shared-memory combiner.

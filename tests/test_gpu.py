@@ -49,18 +49,34 @@ def rel_err(got, want):
     return float(np.max(np.abs(got - want) / np.abs(want)))
 
 
-@pytest.mark.parametrize("mode", ["pull", "push", "hubs"])
+@pytest.fixture
+def seg_threshold():
+    """Set PGX_OPT_SEG_MIN_EDGES for one test, restore the shipped value."""
+    from paper_2010_01542_b200 import _lib
+    yield lambda v: _lib.set_option(_lib.PGX_OPT_SEG_MIN_EDGES, v)
+    _lib.set_option(_lib.PGX_OPT_SEG_MIN_EDGES, 512)
+
+
+# modes: pull / push (PageRank lowering, min programs with the shipped
+# segment policy: device graphs get the segmented scatter for supersteps
+# with >= m/4 sender edges), hubs (hub-cache arm), k1 (segments off: K1 in
+# every superstep), segall (the segmented scatter in every superstep)
+@pytest.mark.parametrize("mode", ["pull", "push", "hubs", "k1", "segall"])
 @pytest.mark.parametrize("r", RUNS, ids=lambda r: r.id)
-def test_golden_reference_runs(r, mode):
+def test_golden_reference_runs(r, mode, seg_threshold):
     if mode == "push" and r.app != "pagerank":
         pytest.skip("pagerank_mode only changes the PageRank lowering")
-    if mode == "hubs" and r.app == "pagerank":
-        pytest.skip("hub_cache only changes the min combiner")
+    if mode in ("hubs", "k1", "segall") and r.app == "pagerank":
+        pytest.skip("hub_cache / segments only change the min combiner")
     g = pgx.from_edges(r.src, r.dst, r.n, undirected=r.undirected, device="cuda")
     cap = r.kwargs.get("max_supersteps")
     cfg = pgx.EngineConfig(max_supersteps=cap if cap else pgx.DEFAULT_MAX_SUPERSTEPS,
                            pagerank_mode="push" if mode == "push" else "pull",
-                           hub_cache="on" if mode == "hubs" else "off")
+                           hub_cache="on" if mode == "hubs" else "off",
+                           segments="off" if mode == "k1" else
+                           "on" if mode == "segall" else "auto")
+    if mode == "segall":
+        seg_threshold(0)
     rep = pgx.run(g, program(r.app, r.kwargs), cfg)
     if r.app == "pagerank":
         assert rep.values.dtype == np.float64
