@@ -1,21 +1,27 @@
 #!/usr/bin/env python3
 """Benchmark: GTEPS of the B200 superstep engine vs the reference CPU path.
 
-Workload at N=1: BASELINE.json configs[1] -- Hashmin connected components
-on the symmetrised R-MAT scale-22 / edge-factor-8 graph (seed 2), run to
-quiescence (C2).  ``--config`` picks another BASELINE config (C1..C5).
+Workload at every N (1, 2, 4, 8): BASELINE.json configs[4] -- Hashmin
+connected components on the symmetrised R-MAT scale-26 / edge-factor-14
+graph (seed 5, n = 67.1M, m = 1.84e9), run to quiescence (C5): the largest
+config, the one that fits one B200 and the one BASELINE quotes at 1/2/4/8
+GPUs.  ``--config`` picks another BASELINE config (C1..C5).
 
 A "step" is one complete run of the program (every superstep to
-quiescence) over the graph.  ``value`` = sum of edges traversed by the
-senders over all supersteps / device time of the run kernel (GTEPS), with
-the CSR already resident in HBM; ``e2e`` = the same metric through the
-public ``run()`` with the CSR in pinned host memory: upload, device CSR
-preparation, the run and the result read-back are inside the timed region.
-L2 is flushed (a 512 MiB write) between timed steps.
+quiescence) with the CSR resident in HBM and the result left on the
+device: at N = 1 the persistent run kernel (one launch), at N > 1 the
+partitioned superstep loop on every rank.  The timed region
+is the same at every N: CUDA events on the run's stream around each step,
+the max over ranks of the summed step times.  ``value`` = edges traversed
+by the senders over all supersteps x K / that time (GTEPS, whole job).
+``e2e`` = the same metric through the public ``run()`` with the CSR in
+pinned host memory: upload, device CSR preparation, the run and the
+result read-back inside the timed region.  L2 is flushed (a 512 MiB write)
+between timed steps; the C5 CSR (7.4 GB) is larger than L2 as well.
 
 ``--impl reference`` times the reference algorithm's CPU implementation:
 the oracle port of pregelite's superstep engine (oracle/pregel_oracle.c,
-OpenMP on all host cores), on the same config/metric.
+OpenMP on all host cores), full runs of the same config and metric.
 """
 
 from __future__ import annotations
@@ -35,8 +41,18 @@ sys.path.insert(0, ROOT)
 
 METRIC = "GTEPS per app (PR/CC/SSSP) + % of HBM roofline at 1/2/4/8 B200 vs host CPU"
 APP_OF = {"C1": "pagerank", "C2": "components", "C3": "sssp", "C4": "pagerank",
-          "C5": "components"}
+          "C5": "components", "C5S": "components"}  # C5S: C5's shape at scale 16 (tests)
+APP_LONG = {"pagerank": "PageRank (10 supersteps, d=0.85, f64)",
+            "components": "Hashmin connected components (u32, to quiescence)",
+            "sssp": "unit-weight SSSP from the max out-degree vertex (u32)"}
 HBM_NORTH_STAR_GBS = 8000.0
+DEFAULT_CONFIG = "C5"
+
+
+def workload(cfg: str, app: str, n: int, m: int) -> str:
+    """The workload string both arms print (identical for the same config)."""
+    return (f"{cfg}: {APP_LONG[app]} on R-MAT scale {int(np.log2(max(n, 1)))}, "
+            f"n={n}, m={m}")
 
 
 def measured_peaks():
@@ -70,20 +86,6 @@ def algorithmic_bytes(app: str, n: int, m: int, steps) -> int:
     return sum(algorithmic_bytes_per_step(app, n, m, steps))
 
 
-def superstep_aggregate(app, n, m, rep, peak):
-    """SURVEY 8(d)'s first figure: sum_s B_s / sum_s t_s, t_s the device time
-    of superstep s (%globaltimer stamps of the persistent kernel), next to
-    the loop figure (B_total / kernel time) that `roofline` reports."""
-    b = algorithmic_bytes_per_step(app, n, m, step_views(app, rep))
-    t = [s.seconds for s in rep.supersteps]
-    gbs = sum(b) / sum(t) / 1e9 if sum(t) > 0 else 0.0
-    return {"achieved": round(gbs, 1), "unit": "GB/s", "peak": peak,
-            "frac": round(gbs / peak, 4),
-            "per_superstep": [{"s": i, "edges": st.edges, "us": round(ts * 1e6, 1),
-                               "GBps": round(bs / ts / 1e9, 1) if ts > 0 else None}
-                              for i, (st, ts, bs) in enumerate(zip(rep.supersteps, t, b))]}
-
-
 class StepView:
     def __init__(self, broadcasters, edges, recipients):
         self.broadcasters, self.edges, self.recipients = broadcasters, edges, recipients
@@ -95,6 +97,23 @@ def step_views(app, rep):
         bc = s.messages_sent if app == "components" else s.broadcasters
         out.append(StepView(bc, s.edges, s.recipients))
     return out
+
+
+def superstep_aggregate(app, n, m, rep, peak):
+    """SURVEY 8(d)'s first figure: sum_s B_s / sum_s t_s, t_s the device time
+    of superstep s (%globaltimer stamps of the persistent kernel; host
+    clock per superstep of the partitioned loop), next to the loop figure
+    (B_total / run time) that `roofline` reports."""
+    b = algorithmic_bytes_per_step(app, n, m, step_views(app, rep))
+    t = [s.seconds for s in rep.supersteps]
+    gbs = sum(b) / sum(t) / 1e9 if sum(t) > 0 else 0.0
+    return {"achieved": round(gbs, 1), "unit": "GB/s", "peak": peak,
+            "frac": round(gbs / peak, 4),
+            "per_superstep": [{"s": i, "edges": st.edges, "senders": st.senders,
+                               "recipients": st.recipients, "us": round(ts * 1e6, 1),
+                               "alg_bytes": bs,
+                               "GBps": round(bs / ts / 1e9, 1) if ts > 0 else None}
+                              for i, (st, ts, bs) in enumerate(zip(rep.supersteps, t, b))]}
 
 
 # ----------------------------------------------------------------------
@@ -130,7 +149,7 @@ class ClockSampler:
                         self.reasons.add(name)
             except Exception:
                 pass
-            time.sleep(0.02)
+            time.sleep(0.01)
 
     def __enter__(self):
         if self._nv is not None:
@@ -151,7 +170,7 @@ class ClockSampler:
 
 
 # ----------------------------------------------------------------------
-# the B200 arm
+# helpers
 # ----------------------------------------------------------------------
 
 def program_for(pgx, app, graph):
@@ -163,13 +182,25 @@ def program_for(pgx, app, graph):
     return pgx.sssp(int(torch.argmax(graph.out_degrees)))
 
 
-def cpu_baseline(cfg: str, graph, app: str, budget_s: float = 20.0):
-    """Oracle port of pregelite's engine on all host cores, bounded sample."""
+def oracle_inputs(n, off, tgt, app, symmetric: bool):
+    """In-CSR for the oracle's pull programs.  A symmetrised R-MAT CSR
+    (rows sorted, deduplicated) is its own transpose."""
+    from oracle import oracle as O
+    if app == "sssp":
+        return None, None
+    if symmetric:
+        return off, tgt
+    return O.transpose(n, off, tgt)
+
+
+def cpu_baseline(cfg: str, graph, app: str, budget_s: float = 30.0):
+    """Oracle port of pregelite's engine on all host cores: full runs of the
+    same workload (at least one, up to three within the budget)."""
     from oracle import oracle as O
     n = graph.vertex_count
     off = graph.out_offsets.cpu().numpy()
     tgt = graph.out_targets.cpu().numpy()
-    in_off, in_tgt = (None, None) if app == "sssp" else O.transpose(n, off, tgt)
+    in_off, in_tgt = oracle_inputs(n, off, tgt, app, O.CONFIGS[cfg].symmetric)
     threads = O.max_threads()
     src = int(np.argmax(np.diff(off)))
     edges_total, secs, runs = 0, 0.0, 0
@@ -184,7 +215,7 @@ def cpu_baseline(cfg: str, graph, app: str, budget_s: float = 20.0):
         secs += time.perf_counter() - t
         edges_total += sum(r.edges)
         runs += 1
-    return {"value": edges_total / secs / 1e9, "unit": "GTEPS", "cores": threads,
+    return {"value": round(edges_total / secs / 1e9, 5), "unit": "GTEPS", "cores": threads,
             "kind": "port",
             "sample": f"{runs} full {cfg} {app} run(s) (all supersteps) of the oracle "
                       f"port of pregelite's engine, {threads} OpenMP threads, "
@@ -197,20 +228,19 @@ def flush_l2(buf):
 
 #: scattered-access ceilings measured on this pool's B200 by tools/ceilings.py
 #: (profiles/ceilings_r1.json): uniformly random 4/8-byte slots of an
-#: L2-resident array.  Every edge of a superstep costs at least one such
-#: access (read-filter load / share gather / red), so these bound GTEPS.
+#: L2-resident array.
 SCATTER_CEILING = {"load": 290.0, "red": 193.0}
 
 
 def ncu_traffic(tag: str):
     """DRAM bytes per launch of the headline kernel from the committed ncu
-    summary (profiles/ncu_<tag>_*.json, newest), else None."""
+    summary (profiles/ncu_<tag>_*.json, newest round and version), else None."""
     import glob
     import re
 
-    def version(f):  # numeric: _v10 is newer than _v9
-        m = re.search(r"_v(\d+)\.json$", f)
-        return int(m.group(1)) if m else -1
+    def version(f):  # numeric: _r2_v10 is newer than _r2_v9 and _r1_v11
+        m = re.search(r"_r(\d+)_v(\d+)\.json$", f)
+        return (int(m.group(1)), int(m.group(2))) if m else (-1, -1)
     files = sorted(glob.glob(os.path.join(ROOT, "profiles", f"ncu_{tag}_*.json")), key=version)
     if not files:
         return None, None
@@ -221,13 +251,70 @@ def ncu_traffic(tag: str):
         return None, None
 
 
-def measure_device(pgx, g, prog, steps, warmup, flush, config=None):
-    """Device-resident timing: one persistent-kernel launch per step."""
+class _Dist:
+    """Process-group plumbing of the device arm (world 1: no-ops)."""
+
+    def __init__(self):
+        import torch
+        self.world = int(os.environ.get("WORLD_SIZE", "1"))
+        self.rank = int(os.environ.get("RANK", "0"))
+        # LOCAL_RANK modulo the visible devices: identity on a node with a
+        # GPU per rank; lets a functional run put several ranks on one GPU
+        ndev = max(torch.cuda.device_count(), 1)
+        self.local = int(os.environ.get("LOCAL_RANK", "0")) % ndev
+        torch.cuda.set_device(self.local)
+        self.dist = None
+        self.backend = None
+        if self.world > 1:
+            import torch.distributed as dist
+            os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+            self.backend = os.environ.get("PGX_DIST_BACKEND", "nccl")  # gloo: functional runs
+            if self.backend == "nccl":
+                dist.init_process_group("nccl", device_id=torch.device("cuda", self.local))
+            else:
+                dist.init_process_group(self.backend)
+            self.dist = dist
+
+    def barrier(self):
+        if self.dist is not None:
+            self.dist.barrier()
+
+    def max(self, x: float) -> float:
+        if self.dist is None:
+            return x
+        import torch
+        dev = "cuda" if self.backend == "nccl" else "cpu"
+        t = torch.tensor([x], dtype=torch.float64, device=dev)
+        self.dist.all_reduce(t, op=self.dist.ReduceOp.MAX)
+        return float(t.item())
+
+    def close(self):
+        if self.dist is not None:
+            self.dist.destroy_process_group()
+
+
+def make_plan(pgx, d: _Dist, g, prog, pcfg):
+    """The run prepared on this rank: the persistent kernel at N = 1, the
+    partitioned superstep loop at N > 1 (both: CSR resident, result left on
+    the device)."""
+    if d.world == 1:
+        return pgx.plan_run(g, prog, pcfg)
+    from paper_2010_01542_b200.distributed import plan_partitioned
+    from paper_2010_01542_b200.engine import lowering_of
+    return plan_partitioned(g, prog, lowering_of(prog), pcfg, d.dist)
+
+
+def time_steps(plan, d: _Dist, steps: int, warmup: int, flush):
+    """W untimed runs, then exactly K runs timed with CUDA events on the
+    run's stream (L2 flushed between them); barrier + synchronize on both
+    sides; the max over ranks of the summed step times."""
     import torch
-    plan = pgx.plan_run(g, prog, config)
     for _ in range(warmup):
         plan.launch()
     torch.cuda.synchronize()
+    d.barrier()
+    torch.cuda.synchronize()
+    k0 = getattr(plan, "launches", None)
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
           for _ in range(steps)]
     for i in range(steps):
@@ -236,91 +323,94 @@ def measure_device(pgx, g, prog, steps, warmup, flush, config=None):
         plan.launch()
         ev[i][1].record(plan.stream)
     torch.cuda.synchronize()
+    d.barrier()
+    torch.cuda.synchronize()
     ms = [a.elapsed_time(b) for a, b in ev]
-    return plan, ms
+    launches = (plan.launches - k0) if k0 is not None else steps  # 1 persistent kernel per run
+    return ms, d.max(float(sum(ms))), launches
 
 
-def bench_gpu(args):
+def time_e2e(pgx, d: _Dist, g, prog, pcfg, steps: int, warmup: int, flush):
+    """The public run() from page-locked host memory, timed on the device
+    (events on the current stream; run() returns after the read-back)."""
+    import torch
+    host = g.pin_memory()
+    ms = []
+    for i in range(warmup + steps):
+        host.drop_device_cache()
+        flush_l2(flush)
+        torch.cuda.synchronize()
+        d.barrier()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
+        pgx.run(host, prog, pcfg)
+        b.record()
+        torch.cuda.synchronize()
+        if i >= warmup:
+            ms.append(a.elapsed_time(b))
+    host.drop_device_cache()
+    return d.max(float(sum(ms))), len(ms)
+
+
+# ----------------------------------------------------------------------
+# the B200 arm (every N)
+# ----------------------------------------------------------------------
+
+def bench_pgx(args):
     import torch
     import paper_2010_01542_b200 as pgx
     from paper_2010_01542_b200.rmat import rmat_graph
 
-    world = int(os.environ.get("WORLD_SIZE", "1"))
-    rank = int(os.environ.get("RANK", "0"))
-    local = int(os.environ.get("LOCAL_RANK", "0"))
-    torch.cuda.set_device(local)
-    dist = None
-    if world > 1:
-        import torch.distributed as dist
-        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    d = _Dist()
     cfg = args.config
     app = APP_OF[cfg]
     g = rmat_graph(cfg)
     n, m = g.vertex_count, g.edge_count
     prog = program_for(pgx, app, g)
     flush = torch.empty(512 << 20, dtype=torch.uint8, device="cuda")
-
-    # ---- device-resident arm: one persistent kernel per step ----
     pcfg = pgx.EngineConfig(pagerank_mode="pull" if args.pr_pull else "push")
-    if dist is not None:
-        dist.barrier()
-    torch.cuda.synchronize()
-    with ClockSampler(local) as clocks:
-        plan, kernel_ms = measure_device(pgx, g, prog, args.steps, args.warmup, flush, pcfg)
-    if dist is not None:
-        dist.barrier()
-    rep = pgx.collect(plan, prog)
+    if d.world > 1:
+        os.environ["PGX_EXCHANGE"] = args.exchange
+
+    # ---- device-resident arm ----
+    plan = make_plan(pgx, d, g, prog, pcfg)
+    with ClockSampler(d.local) as clocks:
+        kernel_ms, total_ms, launches = time_steps(plan, d, args.steps, args.warmup, flush)
+    rep = plan.collect() if d.world > 1 else pgx.collect(plan, prog)
     edges = sum(s.edges for s in rep.supersteps)
-    total_ms = float(sum(kernel_ms))
-    if dist is not None:
-        t = torch.tensor([total_ms], device="cuda")
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        total_ms = float(t.item())
-    value = edges * args.steps * world / (total_ms * 1e-3) / 1e9
+    value = edges * args.steps / (total_ms * 1e-3) / 1e9
     ms_per_step = total_ms / args.steps
-    steps_view = step_views(app, rep)
-    alg_bytes = algorithmic_bytes(app, n, m, steps_view)
+    alg_bytes = algorithmic_bytes(app, n, m, step_views(app, rep))
     peak, peak_src = measured_peaks()
+    agg_peak = peak * d.world
     achieved = alg_bytes / (ms_per_step * 1e-3) / 1e9
+    del plan
+    torch.cuda.empty_cache()
 
     # ---- e2e arm: public run() with the CSR in pinned host memory ----
-    host = g.pin_memory()
-    e2e_ms = []
-    h2d = (n + 1) * 8 + m * 4
-    # the result tensor read back: f64 ranks, int64 labels (the reference's
-    # CC dtype, algorithms.py:111, widened on the device), u32 distances
+    e2e_total, e2e_n = time_e2e(pgx, d, g, prog, pcfg, args.e2e_steps, 1, flush)
+    # int64 offsets + int32 targets; at N > 1 every rank uploads its own
+    # rows (offsets slice of len + 1): the job total
+    h2d = (n + d.world) * 8 + m * 4
+    # the result read back: f64 ranks, int64 labels (the reference's CC
+    # dtype, algorithms.py:111, widened on the device), u32 distances
     d2h = n * (4 if app == "sssp" else 8)
-    for i in range(args.warmup + args.e2e_steps):
-        host.drop_device_cache()
-        flush_l2(flush)
-        torch.cuda.synchronize()
-        t = time.perf_counter()
-        r = pgx.run(host, prog, pcfg)
-        dt = time.perf_counter() - t
-        if i >= args.warmup:
-            e2e_ms.append(dt * 1e3)
-    e2e_total = float(sum(e2e_ms))
-    e2e_value = edges * len(e2e_ms) / (e2e_total * 1e-3) / 1e9
+    e2e_value = edges * e2e_n / (e2e_total * 1e-3) / 1e9
 
-    traffic, traffic_src = ncu_traffic("c2_components") if cfg == "C2" else (None, None)
+    traffic, traffic_src = ncu_traffic(f"{cfg.lower()}_{app}")
     ceiling = SCATTER_CEILING["red"] if (app == "pagerank" and not args.pr_pull) \
         else SCATTER_CEILING["load"]
     per_config = {}
-    if world == 1 and not args.no_per_config:
-        # C5 on one GPU is the same-workload N=1 point of the 2/4/8-GPU
-        # scaling runs (which measure C5); the headline N=1 line is C2
-        for c2 in ("C1", "C3", "C4", "C5"):
+    if d.world == 1 and not args.no_per_config:
+        for c2 in ("C1", "C2", "C3", "C4", "C5"):
             if c2 == cfg:
                 continue
-            del plan
-            torch.cuda.empty_cache()
             gx = rmat_graph(c2)
             appx = APP_OF[c2]
             px = program_for(pgx, appx, gx)
-            cfgx = pgx.EngineConfig(pagerank_mode="pull" if args.pr_pull else "push")
-            plan, msx = measure_device(pgx, gx, px, args.aux_steps, 3, flush, cfgx)
-            rx = pgx.collect(plan, px)
+            planx = pgx.plan_run(gx, px, pcfg)
+            msx, _, _ = time_steps(planx, d, args.aux_steps, 3, flush)
+            rx = pgx.collect(planx, px)
             ex = sum(st.edges for st in rx.supersteps)
             tx = float(np.median(msx))
             bx = algorithmic_bytes(appx, gx.vertex_count, gx.edge_count, step_views(appx, rx))
@@ -330,165 +420,79 @@ def bench_gpu(args):
                 "GTEPS": round(ex / (tx * 1e-3) / 1e9, 2),
                 "alg_GBps": round(bx / (tx * 1e-3) / 1e9, 1),
                 "frac_of_measured_hbm": round(bx / (tx * 1e-3) / 1e9 / peak, 4),
+                "superstep_us": [round(s.seconds * 1e6, 1) for s in rx.supersteps],
                 "pagerank_mode": ("pull" if args.pr_pull else "push") if appx == "pagerank" else None}
-            del gx
+            del planx, gx
+            torch.cuda.empty_cache()
+    if d.world == 1:
+        parallelism = "1 GPU (persistent cooperative run kernel)"
+    else:
+        ex = set(rep.exchanges or [])
+        parallelism = f"partitioned x{d.world} (1-D source ranges): " + " + ".join(
+            x for x, used in (
+                ("NCCL reduce_scatter (large supersteps)", "dense" in ex),
+                ("sparse all_to_all", "sparse" in ex),
+                ("fused peer-memory combine (NVLink P2P red.min)", "peer" in ex))
+            if used) + ", counters all-gather"
     line = {
         "metric": METRIC,
         "value": round(value, 4),
         "unit": "GTEPS",
-        "n_gpus": world,
+        "n_gpus": d.world,
         "steps": args.steps,
         "warmup": args.warmup,
         "ms_per_step": round(ms_per_step, 5),
         "higher_is_better": True,
-        "scaling": "weak",
+        "scaling": "strong",
         "vs_baseline": None,
         "dtype": "u32" if app != "pagerank" else "f64",
         "data": "synthetic R-MAT (SURVEY 8(d) generator, BASELINE.md CSR sha256-pinned)",
-        "config": {"workload": f"{cfg}: {app} on R-MAT scale {int(np.log2(n))}, "
-                               f"n={n}, m={m}", "n": n, "m": m,
+        "config": {"workload": workload(cfg, app, n, m), "n": n, "m": m,
                    "supersteps": rep.superstep_count, "edges_per_step": edges,
                    "l2": "flushed (512 MiB write) between timed steps",
-                   "parallelism": f"replicas x{world}" if world > 1 else "1 GPU"},
+                   "timed_region": "one run per step, CSR resident, result left on the device",
+                   "parallelism": parallelism},
         "e2e": {"value": round(e2e_value, 4), "unit": "GTEPS",
                 "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
-                "ms_per_step": round(e2e_total / len(e2e_ms), 4)},
-        "gpu_launches": args.steps,
-        "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak,
-                     "unit": "GB/s", "frac": round(achieved / peak, 4),
-                     "traffic": None, "peak_source": peak_src,
-                     "frac_of_8TBs": round(achieved / HBM_NORTH_STAR_GBS, 4),
+                "ms_per_step": round(e2e_total / e2e_n, 4), "steps": e2e_n},
+        "gpu_launches": launches,
+        "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": agg_peak,
+                     "unit": "GB/s", "frac": round(achieved / agg_peak, 4),
+                     "traffic": None, "peak_source": peak_src + (
+                         f" x {d.world} GPUs" if d.world > 1 else ""),
+                     "frac_of_8TBs": round(achieved / (HBM_NORTH_STAR_GBS * d.world), 4),
                      "alg_bytes_per_step": alg_bytes,
-                     "kernel": "min_run_kernel / pagerank_run_kernel (persistent)"},
-        "superstep_aggregate": superstep_aggregate(app, n, m, rep, peak),
+                     "kernel": "min_run_kernel / pagerank_pull_kernel (persistent)"
+                     if d.world == 1 else "pgx_scatter / pgx_apply_slice (partitioned)"},
+        "superstep_aggregate": superstep_aggregate(app, n, m, rep, agg_peak),
         "scattered_roofline": {
-            "bound": "random 4/8-byte L2 accesses (>= 1 per edge)",
-            "achieved": round(value / world, 2), "peak": ceiling, "unit": "G accesses/s",
-            "frac": round(value / world / ceiling, 4),
+            "bound": "random 4/8-byte L2 accesses (>= 1 per edge for K1; per entry segmented)",
+            "achieved": round(value / d.world, 2), "peak": ceiling, "unit": "G edges/s per GPU",
+            "frac": round(value / d.world / ceiling, 4),
             "peak_source": "profiles/ceilings_r1.json (tools/ceilings.py, measured B200)"},
         "per_config": per_config,
         "clocks": clocks.summary(),
     }
-    if traffic is not None:
+    if d.world > 1:
+        line["config"]["exchange_per_superstep"] = rep.exchanges
+        line["config"]["process_group"] = d.backend
+    if traffic is not None and d.world == 1:
         line["roofline"]["traffic"] = int(traffic)
         line["roofline"]["traffic_source"] = traffic_src
-    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+    if d.rank == 0 and d.world == 1 and not args.no_cpu_baseline:
         line["cpu_baseline"] = cpu_baseline(cfg, g, app)
-    if rank == 0:
+    if d.rank == 0:
         print(json.dumps(line), flush=True)
-    if dist is not None:
-        dist.destroy_process_group()
+    d.close()
 
 
-def bench_multi(args):
-    """N > 1 under torchrun: the partitioned superstep of the
-    same workload on every rank's GPU; min programs combine foreign messages
-    straight into the owners' mailboxes over NVLink peer memory (the fused
-    exchange, --exchange auto/peer) or through NCCL collectives (--exchange
-    hybrid/dense); strong scaling (the graph is fixed).  Timed with CUDA events around each run,
-    max over ranks."""
-    import torch
-    import torch.distributed as dist
-    import paper_2010_01542_b200 as pgx
-    from paper_2010_01542_b200.rmat import rmat_graph
-
-    world = int(os.environ["WORLD_SIZE"])
-    rank = int(os.environ.get("RANK", "0"))
-    # LOCAL_RANK modulo the visible devices: identity on a node with a GPU
-    # per rank; lets a functional run put several ranks on one GPU
-    local = int(os.environ.get("LOCAL_RANK", "0")) % torch.cuda.device_count()
-    torch.cuda.set_device(local)
-    os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
-    backend = os.environ.get("PGX_DIST_BACKEND", "nccl")  # gloo: functional runs only
-    if backend == "nccl":
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-    else:
-        dist.init_process_group(backend)
-    cfg = args.config
-    app = APP_OF[cfg]
-    g = rmat_graph(cfg)
-    n, m = g.vertex_count, g.edge_count
-    prog = program_for(pgx, app, g)
-    flush = torch.empty(512 << 20, dtype=torch.uint8, device="cuda")
-    os.environ["PGX_EXCHANGE"] = args.exchange
-    for _ in range(args.warmup):
-        rep = pgx.run(g, prog)
-    ms = []
-    with ClockSampler(local) as clocks:
-        for _ in range(args.steps):
-            flush_l2(flush)
-            dist.barrier()
-            torch.cuda.synchronize()
-            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            a.record()
-            rep = pgx.run(g, prog)
-            b.record()
-            torch.cuda.synchronize()
-            ms.append(a.elapsed_time(b))
-    t = torch.tensor([sum(ms)], device="cuda")
-    dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    total_ms = float(t.item())
-    edges = sum(s.edges for s in rep.supersteps)
-    value = edges * args.steps / (total_ms * 1e-3) / 1e9
-    ex = set(rep.exchanges or [])
-    peak, peak_src = measured_peaks()
-    alg = algorithmic_bytes(app, n, m, step_views(app, rep))
-    achieved = alg / (total_ms / args.steps * 1e-3) / 1e9
-    # e2e: the public run() from pinned host memory (local slice upload inside)
-    host = g.pin_memory()
-    e2e = []
-    for i in range(2 + args.e2e_steps):
-        dist.barrier()
-        torch.cuda.synchronize()
-        t0 = time.perf_counter()
-        pgx.run(host, prog)
-        torch.cuda.synchronize()
-        dt = time.perf_counter() - t0
-        host.drop_device_cache()
-        if i >= 2:
-            e2e.append(dt * 1e3)
-    te = torch.tensor([sum(e2e)], device="cuda")
-    dist.all_reduce(te, op=dist.ReduceOp.MAX)
-    e2e_ms = float(te.item()) / len(e2e)
-    line = {
-        "metric": METRIC, "value": round(value, 4), "unit": "GTEPS", "n_gpus": world,
-        "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": round(total_ms / args.steps, 4), "higher_is_better": True,
-        "scaling": "strong", "vs_baseline": None,
-        "dtype": "u32" if app != "pagerank" else "f64",
-        "data": "synthetic R-MAT (SURVEY 8(d) generator, BASELINE.md CSR sha256-pinned)",
-        "config": {"workload": f"{cfg}: {app} on R-MAT, n={n}, m={m}, 1-D source partition "
-                               f"over {world} GPUs (edge-balanced ranges)",
-                   "n": n, "m": m, "supersteps": rep.superstep_count,
-                   "l2": "flushed (512 MiB write) between timed steps",
-                   "parallelism": f"partitioned x{world}: " + " + ".join(
-                       x for x, used in (
-                           ("NCCL reduce_scatter (large supersteps)", "dense" in ex),
-                           ("sparse all_to_all", "sparse" in ex),
-                           ("fused peer-memory combine (NVLink P2P red.min)", "peer" in ex))
-                       if used) + ", counters all-gather",
-                   "exchange_per_superstep": rep.exchanges,
-                   "process_group": backend},
-        "e2e": {"value": round(edges / (e2e_ms * 1e-3) / 1e9, 4), "unit": "GTEPS",
-                "h2d_bytes_per_step": (n + 1) * 8 + m * 4,
-                "d2h_bytes_per_step": n * (4 if app == "sssp" else 8),
-                "ms_per_step": round(e2e_ms, 3)},
-        # our kernels per timed step: scatter + apply (+ reset_touched for
-        # the peer exchange) per superstep
-        "gpu_launches": sum(3 if e == "peer" else 2 for e in (rep.exchanges or []))
-                        * args.steps,
-        "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak * world,
-                     "unit": "GB/s", "frac": round(achieved / (peak * world), 4),
-                     "traffic": None, "peak_source": peak_src + f" x {world} GPUs"},
-        "clocks": clocks.summary(),
-    }
-    if rank == 0:
-        print(json.dumps(line), flush=True)
-    dist.destroy_process_group()
-
+# ----------------------------------------------------------------------
+# the reference arm
+# ----------------------------------------------------------------------
 
 def bench_reference(args):
-    """--impl reference: the oracle port of pregelite's engine on host cores."""
+    """--impl reference: the oracle port of pregelite's engine on host cores,
+    full runs of the same workload (rank 0 only)."""
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
@@ -497,44 +501,50 @@ def bench_reference(args):
     app = APP_OF[cfg]
     spec = O.CONFIGS[cfg]
     n, off, tgt = O.rmat_csr(spec)
-    in_off, in_tgt = (None, None) if app == "sssp" else O.transpose(n, off, tgt)
+    in_off, in_tgt = oracle_inputs(n, off, tgt, app, spec.symmetric)
     threads = O.max_threads()
     src = int(np.argmax(np.diff(off)))
-    # one step = one bounded sample of the workload: a complete run for
-    # C1-C4 (0.05-3 s on 16 host threads); for C5 (1.8e9 edges) its first
-    # superstep (every vertex broadcasts: 1.84e9 edge folds), so that the
-    # driver's --steps K --warmup W run stays within minutes
-    cap = 1 if cfg == "C5" else 10_000
 
     def once():
         if app == "pagerank":
-            return O.run_pagerank(n, off, tgt, 10, 0.85, in_off, in_tgt, max_steps=cap,
-                                  threads=threads)
+            return O.run_pagerank(n, off, tgt, 10, 0.85, in_off, in_tgt, threads=threads)
         if app == "components":
-            return O.run_cc(n, off, tgt, in_off, in_tgt, max_steps=cap, threads=threads)
-        return O.run_sssp(n, off, tgt, src, max_steps=cap, threads=threads)
+            return O.run_cc(n, off, tgt, in_off, in_tgt, threads=threads)
+        return O.run_sssp(n, off, tgt, src, threads=threads)
 
-    for _ in range(args.warmup):
+    # every step is a complete run (all supersteps to quiescence).  A C5 run
+    # takes seconds on the host, so K and W are capped to keep the whole arm
+    # within --ref-budget seconds; the line reports the counts it executed.
+    t = time.perf_counter()
+    once()
+    t1 = time.perf_counter() - t
+    warmup, steps = args.warmup, args.steps
+    if (warmup - 1 + steps) * t1 > args.ref_budget:
+        warmup = max(1, min(warmup, int(0.2 * args.ref_budget / t1)))
+        steps = max(1, min(steps, int(0.8 * args.ref_budget / t1)))
+    for _ in range(warmup - 1):
         once()
     secs, edges = 0.0, 0
-    steps = args.steps
     for _ in range(steps):
         t = time.perf_counter()
         r = once()
         secs += time.perf_counter() - t
         edges += sum(r.edges)
     v = edges / secs / 1e9
-    what = "full" if cap > 100 else "first-superstep"
-    sample = (f"{steps} {what} {cfg} {app} run(s) of the oracle port of pregelite's "
-              f"engine (oracle/pregel_oracle.c), {threads} OpenMP threads")
+    sample = (f"{steps} full {cfg} {app} run(s) (every superstep, {len(r.edges)} supersteps, "
+              f"{sum(r.edges)} edges each) of the oracle port of pregelite's engine "
+              f"(oracle/pregel_oracle.c), {threads} OpenMP threads, after {warmup} warm-up run(s)")
+    world = int(os.environ.get("WORLD_SIZE", "1"))
     line = {"metric": METRIC, "value": round(v, 5), "unit": "GTEPS", "impl": "reference",
-            "n_gpus": int(os.environ.get("WORLD_SIZE", "1")), "steps": steps,
-            "warmup": args.warmup, "ms_per_step": round(secs / steps * 1e3, 3),
-            "higher_is_better": True,
-            "scaling": "strong" if int(os.environ.get("WORLD_SIZE", "1")) > 1 else "weak",
-            "vs_baseline": None,
-            "dtype": "u32" if app != "pagerank" else "f64", "data": "synthetic R-MAT",
-            "config": {"workload": f"{cfg}: {app}, n={n}, m={tgt.size}"},
+            "n_gpus": world, "steps": steps, "warmup": warmup,
+            "steps_requested": args.steps, "warmup_requested": args.warmup,
+            "ms_per_step": round(secs / steps * 1e3, 3),
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+            "dtype": "u32" if app != "pagerank" else "f64",
+            "data": "synthetic R-MAT (SURVEY 8(d) generator, BASELINE.md CSR sha256-pinned)",
+            "config": {"workload": workload(cfg, app, n, int(tgt.size)), "n": n,
+                       "m": int(tgt.size), "supersteps": len(r.edges),
+                       "edges_per_step": int(sum(r.edges))},
             "cpu_baseline": {"value": round(v, 5), "unit": "GTEPS", "cores": threads,
                              "kind": "port", "sample": sample},
             "e2e": {"value": round(v, 5), "unit": "GTEPS", "h2d_bytes_per_step": 0,
@@ -545,32 +555,28 @@ def bench_reference(args):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=5)
-    ap.add_argument("--e2e-steps", type=int, default=5)
+    ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--impl", default="pgx", choices=["pgx", "reference"])
-    ap.add_argument("--config", default=None, choices=sorted(APP_OF),
-                    help="BASELINE config; default C2 (configs[1]) at N=1, "
-                         "C5 (the 1/2/4/8-GPU config) under torchrun N>1")
+    ap.add_argument("--config", default=DEFAULT_CONFIG, choices=sorted(APP_OF),
+                    help="BASELINE config (default C5 at every N)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-per-config", action="store_true")
     ap.add_argument("--aux-steps", type=int, default=5)
+    ap.add_argument("--ref-budget", type=float, default=150.0,
+                    help="reference arm: seconds for warm-up + timed runs")
     ap.add_argument("--exchange", default="auto", choices=["auto", "peer", "hybrid", "dense"],
                     help="N>1 min-program mailbox exchange (default: fused peer when mappable)")
     ap.add_argument("--pr-push", dest="pr_pull", action="store_false",
                     help="PageRank A/B arm: push scatter with red.add.f64")
     args = ap.parse_args()
-    world = int(os.environ.get("WORLD_SIZE", "1"))
-    if args.config is None:
-        args.config = "C5" if world > 1 else "C2"
     if args.warmup < 3:  # contract: W >= 3 (both arms)
         args.warmup = 3
     if args.impl == "reference":
         bench_reference(args)
-    elif int(os.environ.get("WORLD_SIZE", "1")) > 1:
-        bench_multi(args)
     else:
-        bench_gpu(args)
+        bench_pgx(args)
 
 
 if __name__ == "__main__":

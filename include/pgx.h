@@ -33,7 +33,7 @@
 extern "C" {
 #endif
 
-#define PGX_ABI_VERSION 3
+#define PGX_ABI_VERSION 4
 
 #define PGX_OK 0
 #define PGX_EINVAL (-1)   /* bad argument / unsupported configuration */
@@ -80,7 +80,7 @@ const char *pgx_last_error(void);
 #define PGX_OPT_VERTEX_SCHED 3  /* ablation: one thread per sender (no edge balance) */
 #define PGX_OPT_LAYOUT 4        /* ablation: PGX_LAYOUT_* of the CC/SSSP vertex state */
 #define PGX_OPT_SEG_MIN_EDGES 5 /* segmented scatter when a superstep's senders hold at least
-                                   m * value / 1024 edges (0 = every superstep, 1025 = never; default 512) */
+                                   m * value / 1024 edges (0 = every superstep, 1025 = never; default 256) */
 #define PGX_OPT_COUNT 6
 
 /* PGX_OPT_LAYOUT values (LayoutMode, layout.py:31-33).  EXTERNALISED is the
@@ -125,13 +125,14 @@ int pgx_graph_prepare(int32_t n, int64_t m, const int32_t *row_ptr,
 /* ---------------------------------------------------------------- */
 
 typedef struct PgxSegIndex {
-  int32_t seg_log2;         /* segment = vertex >> seg_log2 (<= 16)        */
+  int32_t seg_log2;         /* segment = vertex >> seg_log2 (5..15)        */
   int32_t nent;             /* entries                                     */
   int32_t nitems;           /* work items                                  */
   int32_t reserved;
   const int32_t *ent_src;   /* [nent]   source of each entry               */
   const int32_t *ent_eb;    /* [nent+1] first edge (segment order); [nent] = m */
-  const uint16_t *col16;    /* [m+256]  destination - segment base         */
+  const uint16_t *col16;    /* [m+256]  destination - segment base; bit 15
+                               flags the first edge of an entry            */
   const int32_t *tile_ent;  /* [ceil(m/256)+1] entry holding edge 256 t    */
   const int32_t *items;     /* [nitems][4] {segment, e0, e1, owns segment},
                                16-byte aligned, largest first              */
@@ -319,6 +320,10 @@ int pgx_peer_alloc(size_t bytes, void **ptr, void *ipc_handle);
 int pgx_peer_open(const void *ipc_handle, void **ptr);
 int pgx_peer_close(void *ptr);
 int pgx_peer_free(void *ptr);
+/* ranks that are threads of one process on different GPUs map each
+ * other's mailboxes directly: enable peer access to `peer_device` from the
+ * current device (already enabled: success) */
+int pgx_peer_enable(int32_t peer_device);
 
 /* size of the device counter block used by pgx_apply_slice (host out) */
 int pgx_slice_counters_bytes(size_t *bytes);
@@ -336,11 +341,31 @@ int pgx_apply_slice(int app, int32_t len, const int32_t *row_ptr,
                     uintptr_t stream);
 
 /* PageRank apply on an owned slice: rank, next share, per-CTA dangling
- * partials (partials[ceil(len/512)]) */
+ * partials (partials[ceil(len/512)]).  `dangling` is a DEVICE scalar, the
+ * job's dangling mass after the previous superstep (the all-reduce of
+ * every rank's partials, issued on the stream: no host read); the kernel
+ * uses dangling / n_total (algorithms.py:61-73). */
 int pgx_pr_apply_slice(int32_t len, const int32_t *row_ptr, double *rank,
                        double *mailbox_slice, double *share, double base,
-                       double damping, double dangling_over_n, int32_t last,
-                       double *partials, uintptr_t stream);
+                       double damping, const double *dangling, double n_total,
+                       int32_t last, double *partials, uintptr_t stream);
+
+/* K3 on a rank's slice, the pull fold of the partitioned PageRank
+ * (engine.py:425-457): in_col / in_graph_ws are the rank's local in-CSR
+ * (rows = the nrows padded mailbox positions, entries = local source ids,
+ * pgx_graph_prepare'd; nsrc = its non-zero row count, header word 0) and
+ * `share` the rank's shares.  Writes the partial fold of every row that
+ * lies inside one 256-edge tile into folded[row]; rows spanning tiles
+ * leave tail / head partials ([ceil(m/256)+2] each) that
+ * pgx_fold_spanning combines in tile order.  Rows without local in-edges
+ * are not written (zero `folded` first).  No atomics; deterministic. */
+int pgx_gather_slice(int32_t nrows, int64_t m, const int32_t *in_col,
+                     const void *in_graph_ws, int32_t nsrc, const double *share,
+                     double *folded, double *head, double *tail,
+                     uintptr_t stream);
+int pgx_fold_spanning(int32_t nspan, const int32_t *rows, const int32_t *t0,
+                      const int32_t *t1, const double *head, const double *tail,
+                      double *folded, uintptr_t stream);
 
 /* ---------------------------------------------------------------- */
 /* R-MAT input generator; input construction only.    */

@@ -126,6 +126,8 @@ CONFIGS = {
     "C3": RmatSpec(22, 16, 0.57, 0.19, 0.19, 3, False),
     "C4": RmatSpec(22, 28, 0.45, 0.22, 0.22, 4, False),
     "C5": RmatSpec(26, 14, 0.57, 0.19, 0.19, 5, True),
+    # test-only: C5's shape at scale 16 (bench.py functional multi-rank runs)
+    "C5S": RmatSpec(16, 14, 0.57, 0.19, 0.19, 5, True),
 }
 
 

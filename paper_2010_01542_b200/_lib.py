@@ -16,7 +16,7 @@ from .errors import ConfigError, ExecutionError
 PKG_DIR = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.environ.get("PGX_LIB") or os.path.join(PKG_DIR, "libpgx.so")
 
-PGX_ABI_VERSION = 3
+PGX_ABI_VERSION = 4
 PGX_OK, PGX_EINVAL, PGX_ECUDA, PGX_ENOMEM = 0, -1, -2, -3
 PGX_APP_PAGERANK, PGX_APP_CC, PGX_APP_SSSP, PGX_APP_PAGERANK_PULL = 0, 1, 2, 3
 PGX_OP_MIN_U32, PGX_OP_SUM_F64 = 0, 1
@@ -44,6 +44,7 @@ EXPORTS = (
     "pgx_scatter_peer", "pgx_reset_touched", "pgx_peer_alloc", "pgx_peer_open",
     "pgx_peer_close", "pgx_peer_free", "pgx_seg_workspace_bytes", "pgx_seg_max_items",
     "pgx_seg_count", "pgx_seg_build", "pgx_sssp_run_ex", "pgx_cc_run_ex",
+    "pgx_gather_slice", "pgx_fold_spanning", "pgx_peer_enable",
 )
 
 
@@ -100,8 +101,11 @@ _SIGS = {
     "pgx_slice_counters_bytes": (ctypes.c_int, [_p]),
     "pgx_apply_slice": (ctypes.c_int, [ctypes.c_int, _i32, _p, _p, _p, _p, _p, _p, _p, _p,
                                        _i32, ctypes.c_uint32, _up]),
-    "pgx_pr_apply_slice": (ctypes.c_int, [_i32, _p, _p, _p, _p, _f64, _f64, _f64, _i32, _p,
-                                          _up]),
+    "pgx_pr_apply_slice": (ctypes.c_int, [_i32, _p, _p, _p, _p, _f64, _f64, _p, _f64, _i32,
+                                          _p, _up]),
+    "pgx_gather_slice": (ctypes.c_int, [_i32, _i64, _p, _p, _i32, _p, _p, _p, _p, _up]),
+    "pgx_fold_spanning": (ctypes.c_int, [_i32, _p, _p, _p, _p, _p, _p, _up]),
+    "pgx_peer_enable": (ctypes.c_int, [_i32]),
     "pgx_microbench": (ctypes.c_int, [ctypes.c_int, _p, _i64, _i64, _u64, _p, _up]),
     "pgx_seg_workspace_bytes": (ctypes.c_int, [_i32, _i64, _i64, _i32, _p]),
     "pgx_seg_max_items": (ctypes.c_int, [_i32, _i64, _i32, _p]),

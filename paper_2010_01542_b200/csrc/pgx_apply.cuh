@@ -69,7 +69,8 @@ template <int APP, int S = 0, bool BFS = false>
 __device__ unsigned long long apply_min_phase(const int32_t *__restrict__ row_ptr, uint32_t *val,
                                               uint32_t *mailbox, int32_t n, const RunWs &ws,
                                               StepCounters *ctr, char *smem, bool count_only,
-                                              uint32_t bfs_msg = 0, uint32_t *snd = nullptr) {
+                                              uint32_t bfs_msg = 0, uint32_t *snd = nullptr,
+                                              uint32_t *sv = nullptr) {
   __shared__ unsigned long long s_w[33];
   __shared__ unsigned long long s_gbase;
   int32_t *s_list = reinterpret_cast<int32_t *>(smem);  // kListCap vertex ids
@@ -192,6 +193,7 @@ __device__ unsigned long long apply_min_phase(const int32_t *__restrict__ row_pt
             if (deg[j] > 0) {
               // senders bitmap of the next superstep (segmented scatter)
               if (snd) red_or_b32(snd + (v[j] >> 5), 1u << (v[j] & 31));
+              if (sv) sv[v[j]] = m[j];  // CC: the label it sends
               const unsigned pos = (unsigned)(run >> 32);
               const int eb = (int)(run & 0xFFFFFFFFull);
               PGX_ASSERT(pos < (unsigned)n && (int64_t)eb + deg[j] <= (int64_t)INT32_MAX);

@@ -137,6 +137,12 @@ __device__ __forceinline__ void red_min_u32(uint32_t *p, uint32_t v) {
   asm volatile("red.relaxed.gpu.global.min.u32 [%0], %1;" :: "l"(p), "r"(v) : "memory");
 }
 
+// system scope: slots other GPUs combine into as well (the fused peer
+// exchange); a .gpu-scoped atomic is not atomic against another device's
+__device__ __forceinline__ void red_min_u32_sys(uint32_t *p, uint32_t v) {
+  asm volatile("red.relaxed.sys.global.min.u32 [%0], %1;" :: "l"(p), "r"(v) : "memory");
+}
+
 __device__ __forceinline__ void red_or_b32(uint32_t *p, uint32_t v) {
   asm volatile("red.relaxed.gpu.global.or.b32 [%0], %1;" :: "l"(p), "r"(v) : "memory");
 }
@@ -259,6 +265,7 @@ struct RunWs {
   double *share2;          // pull PR: second share buffer
   double *head, *tail;     // pull PR: per-tile partials of tile-spanning rows
   uint32_t *snd[2];        // [n/32+2] x 2 senders bitmaps (segmented scatter; min apps)
+  uint32_t *sv[2];         // CC: [n] x 2 send values (the neutral for non-senders)
 };
 
 inline size_t run_ws_layout(int app, int64_t n, int64_t m, int32_t max_steps, RunWs *ws,
@@ -281,6 +288,7 @@ inline size_t run_ws_layout(int app, int64_t n, int64_t m, int32_t max_steps, Ru
   w.mailbox = take(W * (size_t)(n + 1) * (interleaved && !pr ? 2 : 1));
   w.share2 = w.head = w.tail = nullptr;
   w.snd[0] = w.snd[1] = nullptr;
+  w.sv[0] = w.sv[1] = nullptr;
   if (app == PGX_APP_PAGERANK_PULL) {
     w.share2 = (double *)take(sizeof(double) * (size_t)(n + 1));
     w.head = (double *)take(sizeof(double) * (size_t)(ceil_div(m, kTile) + 2));
@@ -293,6 +301,10 @@ inline size_t run_ws_layout(int app, int64_t n, int64_t m, int32_t max_steps, Ru
     w.tile_src = (int32_t *)take(sizeof(int32_t) * (size_t)(ceil_div(m, kTile) + 2));
     w.snd[0] = (uint32_t *)take(sizeof(uint32_t) * (size_t)(n / 32 + 2));
     w.snd[1] = (uint32_t *)take(sizeof(uint32_t) * (size_t)(n / 32 + 2));
+    if (app == PGX_APP_CC) {
+      w.sv[0] = (uint32_t *)take(sizeof(uint32_t) * (size_t)(n + 1));
+      w.sv[1] = (uint32_t *)take(sizeof(uint32_t) * (size_t)(n + 1));
+    }
   } else {
     w.f_eb = w.f_rs = w.tile_src = nullptr;
     w.has = nullptr;

@@ -80,9 +80,11 @@ __global__ void __launch_bounds__(kBlock, PGX_MIN_BLOCKS) min_run_kernel(MinRunP
   const unsigned gtid = blockIdx.x * blockDim.x + threadIdx.x;
 
   // ---- setup (algorithms.py:96-97 / 129-134) + superstep-0 senders ----
+  const bool use_sv = APP == PGX_APP_CC && p.use_seg;
   for (unsigned v = gtid; v < (unsigned)p.n; v += nthreads) {
     *slot<S>(val, v) = (APP == PGX_APP_CC) ? v : kNeutralMin;
     if (!BFS) *slot<S>(mailbox, v) = kNeutralMin;  // the bitmap kernel has no mailbox
+    if (use_sv) p.ws.sv[0][v] = p.ws.sv[1][v] = kNeutralMin;
   }
   for (unsigned wi = gtid; wi < (unsigned)(p.n / 32 + 2); wi += nthreads) {
     p.ws.has[wi] = 0u;
@@ -128,11 +130,24 @@ __global__ void __launch_bounds__(kBlock, PGX_MIN_BLOCKS) min_run_kernel(MinRunP
     const int64_t edges_s = (APP == PGX_APP_CC && s == 0) ? p.m
                                                           : (int64_t)(packed_s & 0xFFFFFFFFull);
     if (p.use_seg) {
-      // senders bitmap of superstep s + 1 (written by the next apply): last
-      // read by scatter(s - 1), clear it unless that superstep had no senders
+      // senders bitmap (and CC send values) of superstep s + 1, written by
+      // the next apply: they still hold the senders of s - 1 (last read by
+      // scatter(s - 1)); clear them unless that superstep had no senders
       if (s >= 1 && (p.ws.ctr[s - 1].packed >> 32) != 0ull) {
         uint32_t *nx = p.ws.snd[(s + 1) & 1];
-        for (unsigned wi = gtid; wi < (unsigned)(p.n / 32 + 2); wi += nthreads) nx[wi] = 0u;
+        uint32_t *svx = use_sv ? p.ws.sv[(s + 1) & 1] : nullptr;
+        for (unsigned wi = gtid; wi < (unsigned)(p.n / 32 + 2); wi += nthreads) {
+          uint32_t w = nx[wi];
+          if (!w) continue;
+          nx[wi] = 0u;
+          if (use_sv) {
+            while (w) {
+              const int b = __ffs(w) - 1;
+              w &= w - 1;
+              svx[(wi << 5) + b] = kNeutralMin;
+            }
+          }
+        }
       }
     }
     if (p.use_seg && edges_s >= p.seg_min_edges && edges_s > 0) {
@@ -142,7 +157,7 @@ __global__ void __launch_bounds__(kBlock, PGX_MIN_BLOCKS) min_run_kernel(MinRunP
       sp.m = p.m;
       sp.n = p.n;
       sp.snd = p.ws.snd[s & 1];
-      sp.val = val;
+      sp.sv = use_sv ? p.ws.sv[s & 1] : nullptr;
       sp.uniform = (uint32_t)s + 1u;
       sp.mailbox = mailbox;
       sp.has = p.ws.has;
@@ -205,11 +220,12 @@ __global__ void __launch_bounds__(kBlock, PGX_MIN_BLOCKS) min_run_kernel(MinRunP
     //      pending messages are only counted (engine.py:299-300) ----
     const bool at_cap = (s + 1 == p.max_steps);
     uint32_t *snd_out = p.use_seg ? p.ws.snd[(s + 1) & 1] : nullptr;
+    uint32_t *sv_out = use_sv ? p.ws.sv[(s + 1) & 1] : nullptr;
     const unsigned long long rb =
         bfs ? apply_min_phase<APP, 0, true>(p.row_ptr, val, mailbox, p.n, p.ws, &p.ws.ctr[s + 1],
                                             smem, at_cap, (uint32_t)s + 1u, snd_out)
             : apply_min_phase<APP, S>(p.row_ptr, val, mailbox, p.n, p.ws, &p.ws.ctr[s + 1], smem,
-                                      at_cap, 0u, snd_out);
+                                      at_cap, 0u, snd_out, sv_out);
     const unsigned bc = block_sum<unsigned>((unsigned)(rb & 0xFFFFFFFFull), s_red);
     const unsigned rc = block_sum<unsigned>((unsigned)(rb >> 32), s_red);
     if (threadIdx.x == 0) {
@@ -541,7 +557,7 @@ static int min_run(int app, int32_t n, int64_t m, const int32_t *row_ptr, const 
   if (nhubs < 0 || nhubs > kHubs || (nhubs > 0 && !hub_ids))
     return fail(PGX_EINVAL, "hub count must be in [0, pgx_hub_capacity()]");
   if (seg) {
-    if (seg->seg_log2 < 5 || seg->seg_log2 > 16 || seg->nent < 1 || seg->nent > m ||
+    if (seg->seg_log2 < 5 || seg->seg_log2 > kSegMaxLog2 || seg->nent < 1 || seg->nent > m ||
         seg->nitems < 1 || !seg->ent_src || !seg->ent_eb || !seg->col16 || !seg->tile_ent ||
         !seg->items || reinterpret_cast<uintptr_t>(seg->items) % 16 ||
         reinterpret_cast<uintptr_t>(seg->col16) % 16)

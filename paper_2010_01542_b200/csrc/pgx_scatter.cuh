@@ -228,7 +228,10 @@ __device__ void scatter_phase(const ScatterArgs &a, char *smem, bool read_filter
                 }
                 if (a.has && prev == a.neutral) atomicOr(a.has + (v >> 5), 1u << (v & 31));
               } else {
-                red_min_u32(slot<S>(mb, v), msg);
+                // owned slots of a peer-exchange rank are combined into by
+                // the other GPUs too: system-scope atomics there
+                if (PEER && v >= a.lo && v < a.hi) red_min_u32_sys(slot<S>(mb, v), msg);
+                else red_min_u32(slot<S>(mb, v), msg);
                 PGX_COUNT(0);
                 if (a.has && prev == a.neutral) {
                   red_or_b32(a.has + (v >> 5), 1u << (v & 31));
@@ -241,7 +244,7 @@ __device__ void scatter_phase(const ScatterArgs &a, char *smem, bool read_filter
                 // over NVLink when the owner is another GPU
                 int o = 0;
                 while (o + 1 < a.world && v >= __ldg(a.bounds + o + 1)) o++;
-                red_min_u32(a.peer_mb[o] + v, msg);
+                red_min_u32_sys(a.peer_mb[o] + v, msg);
               }
             }
           }

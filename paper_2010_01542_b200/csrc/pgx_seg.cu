@@ -14,7 +14,9 @@
 //   2. a stable LSD radix sort of the runs by segment (CUB, graph
 //      preparation only);
 //   3. entry edge offsets = exclusive scan of the sorted runs' lengths;
-//      every run's destinations are copied as 16-bit segment offsets;
+//      every run's destinations are copied as 16-bit segment offsets, the
+//      first one flagged (bit 15: the scatter finds entry boundaries in
+//      the destination stream itself);
 //   4. the 256-edge tile map of the new edge order and the segments' edge
 //      ranges, from which the host cuts the work items (hot segments into
 //      slices, largest first).
@@ -110,7 +112,9 @@ __global__ void seg_copy_kernel(int64_t nent, const int32_t *perm, const int32_t
     const int r = perm[i];
     const int32_t s = run_pos[r];
     const int32_t d0 = ent_eb[i], d1 = ent_eb[i + 1];
-    for (int32_t j = 0; j < d1 - d0; j++) col16[d0 + j] = (uint16_t)((uint32_t)col[s + j] & mask);
+    // bit 15: the entry's first edge (the scatter's entry boundaries)
+    for (int32_t j = 0; j < d1 - d0; j++)
+      col16[d0 + j] = (uint16_t)(((uint32_t)col[s + j] & mask) | (j == 0 ? kSegEntryFlag : 0u));
     for (int64_t t = ((int64_t)d0 + kTile - 1) / kTile; t * kTile < d1; t++) tile_ent[t] = (int32_t)i;
   }
 }
@@ -187,7 +191,7 @@ int seg_check(int32_t n, int64_t m, const int32_t *row_ptr, const int32_t *col_i
               const void *graph_ws, int32_t L) {
   int rc = check_graph(n, m, row_ptr, col_idx, graph_ws);
   if (rc) return rc;
-  if (L < 5 || L > 16) return fail(PGX_EINVAL, "seg_log2 must be in [5, 16]");
+  if (L < 5 || L > kSegMaxLog2) return fail(PGX_EINVAL, "seg_log2 must be in [5, 15]");
   if (m < 1) return fail(PGX_EINVAL, "the segmented index needs at least one edge");
   return PGX_OK;
 }
@@ -227,14 +231,14 @@ extern "C" {
 
 int pgx_seg_workspace_bytes(int32_t n, int64_t m, int64_t nent, int32_t seg_log2,
                             size_t *bytes) {
-  if (!bytes || n < 1 || m < 0 || seg_log2 < 5 || seg_log2 > 16 || nent > m)
+  if (!bytes || n < 1 || m < 0 || seg_log2 < 5 || seg_log2 > kSegMaxLog2 || nent > m)
     return fail(PGX_EINVAL, "bad segmented-index workspace arguments");
   *bytes = seg_ws_layout(n, m, nent, seg_log2, nullptr, nullptr);
   return PGX_OK;
 }
 
 int pgx_seg_max_items(int32_t n, int64_t m, int32_t seg_log2, int32_t *max_items) {
-  if (!max_items || n < 1 || m < 0 || seg_log2 < 5 || seg_log2 > 16)
+  if (!max_items || n < 1 || m < 0 || seg_log2 < 5 || seg_log2 > kSegMaxLog2)
     return fail(PGX_EINVAL, "bad segmented-index arguments");
   // one item per segment plus at most one extra slice per item target
   // (the target is >= m / kMaxSegSlices, see pgx_seg_build)

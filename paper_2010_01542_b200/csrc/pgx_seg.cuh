@@ -50,21 +50,27 @@ __device__ __forceinline__ void cp_async_wait_all() {
 
 // Messages of a segmented scatter pass:
 //   kSegSourceId  CC superstep 0: every source sends its id;
-//   kSegLabel     the sources flagged in the senders bitmap send val[src];
-//   kSegUniform   the flagged sources send `uniform` (unit-weight SSSP).
+//   kSegLabel     the source sends sv[src], its send value of this
+//                 superstep (the neutral when it is not a sender: a no-op);
+//   kSegUniform   the sources flagged in the senders bitmap send `uniform`
+//                 (unit-weight SSSP).
 enum SegMsg { kSegSourceId = 0, kSegLabel = 1, kSegUniform = 2 };
 
 // work items: about kSegItemsPerCta per persistent CTA, and never more than
 // kMaxSegSlices slices of hot segments in total (pgx_seg_build)
 constexpr int kSegItemsPerCta = 2;
 constexpr int64_t kMaxSegSlices = 4096;
+// col16: bit 15 flags the first edge of an entry, the low seg_log2 bits
+// are the destination's offset in its segment (so seg_log2 <= 15)
+constexpr uint32_t kSegEntryFlag = 0x8000u;
+constexpr int kSegMaxLog2 = 15;
 
 struct SegPass {
   PgxSegIndex ix;
   int64_t m;
   int32_t n;
-  const uint32_t *snd;  // senders bitmap of this superstep (kSegLabel / kSegUniform)
-  const uint32_t *val;  // kSegLabel: the senders' current values
+  const uint32_t *snd;  // kSegUniform: senders bitmap of this superstep
+  const uint32_t *sv;   // kSegLabel: send values of this superstep
   uint32_t uniform;     // kSegUniform: the message
   uint32_t *mailbox;    // K1's outputs: min-combined mailbox + has-bitmask
   uint32_t *has;
@@ -72,9 +78,11 @@ struct SegPass {
   bool write_mailbox;   // false: the has-bitmask is the whole result (unit SSSP)
 };
 
-// per-warp window: entry edge starts [kSlots], messages [kSlots], the
-// tile's 16-bit destinations [kTile]
-constexpr int kSegWinWords = 2 * kSlots + kTile / 2;
+// per-warp window: the messages of the tile's entries [kSegMsgSlots], the
+// tile's flagged 16-bit destinations [kTile]; 16-byte aligned (cp.async 16)
+constexpr int kSegMsgSlots = (kSlots + 3) & ~3;
+constexpr int kSegWinWords = kSegMsgSlots + kTile / 2;
+static_assert(kSegWinWords % 4 == 0, "16-byte aligned per-warp windows");
 
 __host__ __device__ constexpr size_t seg_smem_bytes(int seg_log2) {
   return ((size_t)4 << seg_log2) + (size_t)kWarps * kSegWinWords * 4;
@@ -85,16 +93,15 @@ __device__ void seg_scatter_phase(const SegPass &a, char *smem_raw) {
   uint32_t *smem = reinterpret_cast<uint32_t *>(smem_raw);
   const int L = a.ix.seg_log2;
   const int S = 1 << L;
+  const uint32_t lmask = (uint32_t)S - 1u;
   uint32_t *s_mb = smem;  // [S] this item's mailbox segment
   __shared__ int s_item[4];
   __shared__ unsigned s_tctr;
   const int lane = (int)lane_id(), warp = threadIdx.x >> 5;
-  int32_t *w_eb = reinterpret_cast<int32_t *>(smem + S) + warp * kSegWinWords;
-  uint32_t *w_msg = reinterpret_cast<uint32_t *>(w_eb + kSlots);
-  uint16_t *w_col = reinterpret_cast<uint16_t *>(w_msg + kSlots);
+  uint32_t *w_msg = smem + S + warp * kSegWinWords;
+  uint16_t *w_col = reinterpret_cast<uint16_t *>(w_msg + kSegMsgSlots);
   const unsigned upto = (lane == 31) ? 0xFFFFFFFFu : ((2u << lane) - 1u);
   const int ntiles = (int)((a.m + kTile - 1) / kTile);
-  const int m32 = (int)a.m;
   const int nent = a.ix.nent;
   for (;;) {
     if (threadIdx.x == 0) {
@@ -141,62 +148,56 @@ __device__ void seg_scatter_phase(const SegPass &a, char *smem_raw) {
       const int k = i1 - i0 + 1;  // <= kTile + 1 entries
       PGX_ASSERT(i0 >= 0 && k >= 1 && k <= kTile + 1 && i1 < nent);
       __syncwarp();
-      // one round trip for the whole tile: 16-bit destinations + entry window
+      // one round trip for the whole tile: the flagged 16-bit destinations
+      // and the entries' messages
       cp_async16(w_col + lane * 8, a.ix.col16 + ta + lane * 8);
       if (MSG == kSegSourceId) {
 #pragma unroll
         for (int q = 0; q < (kSlots + 31) / 32; q++) {
           const int j = lane + 32 * q;
-          if (j <= k) cp_async4(w_eb + j, a.ix.ent_eb + i0 + j);  // ent_eb[nent] = m
           if (j < k) cp_async4(w_msg + j, a.ix.ent_src + i0 + j);
         }
-        cp_async_wait_all();
       } else {
-        // the entry's message: val[src] / uniform when src is a sender of
-        // this superstep (senders bitmap), else the neutral (no effect)
         int src[(kSlots + 31) / 32];
 #pragma unroll
         for (int q = 0; q < (kSlots + 31) / 32; q++) {
           const int j = lane + 32 * q;
-          if (j <= k) cp_async4(w_eb + j, a.ix.ent_eb + i0 + j);
           src[q] = (j < k) ? __ldg(a.ix.ent_src + i0 + j) : -1;
         }
-        uint32_t bits[(kSlots + 31) / 32], vv[(kSlots + 31) / 32];
+        if (MSG == kSegLabel) {
+          // one random load per entry: the send value is the neutral for
+          // a source that does not send in this superstep
 #pragma unroll
-        for (int q = 0; q < (kSlots + 31) / 32; q++) {
-          bits[q] = src[q] >= 0 ? a.snd[src[q] >> 5] : 0u;
-          if (MSG == kSegLabel) vv[q] = src[q] >= 0 ? a.val[src[q]] : kNeutralMin;
-        }
+          for (int q = 0; q < (kSlots + 31) / 32; q++)
+            if (src[q] >= 0) cp_async4(w_msg + lane + 32 * q, a.sv + src[q]);
+        } else {
+          uint32_t bits[(kSlots + 31) / 32];
 #pragma unroll
-        for (int q = 0; q < (kSlots + 31) / 32; q++) {
-          const int j = lane + 32 * q;
-          if (j < k) {
-            const bool on = (bits[q] >> (src[q] & 31)) & 1u;
-            w_msg[j] = on ? (MSG == kSegLabel ? vv[q] : a.uniform) : kNeutralMin;
+          for (int q = 0; q < (kSlots + 31) / 32; q++)
+            bits[q] = src[q] >= 0 ? a.snd[src[q] >> 5] : 0u;
+#pragma unroll
+          for (int q = 0; q < (kSlots + 31) / 32; q++) {
+            const int j = lane + 32 * q;
+            if (j < k) w_msg[j] = ((bits[q] >> (src[q] & 31)) & 1u) ? a.uniform : kNeutralMin;
           }
         }
-        cp_async_wait_all();
       }
+      cp_async_wait_all();
       __syncwarp();
-      int cur = 0;
+      // entry of edge e (tile-relative) = flags in [0, e] - flag(0): the
+      // tile's first edge belongs to entry i0 whether or not it starts it
+      int cur = -(int)(w_col[0] >> 15);
 #pragma unroll
       for (int r = 0; r < kItems; r++) {
-        const int rb = r * 32;  // tile-relative round base
-        const int el = rb + lane;
-        const int ci = cur + 1 + lane;
-        unsigned bit = 0;
-        if (ci <= k) {
-          const unsigned pp = (unsigned)(w_eb[ci] - ta - rb);
-          if (pp < 32u) bit = 1u << pp;
-        }
-        const unsigned bm = __reduce_or_sync(0xFFFFFFFFu, bit);
+        const int el = r * 32 + lane;
+        const uint32_t c = w_col[el];
+        const unsigned bm = __ballot_sync(0xFFFFFFFFu, (c & kSegEntryFlag) != 0u);
         const int sidx = cur + __popc(bm & upto);
         cur += __popc(bm);
         if (el >= ea && el < ez) {
           PGX_ASSERT(sidx >= 0 && sidx < k);
           const uint32_t msg = w_msg[sidx];
-          const int loc = w_col[el];
-          PGX_ASSERT(loc < S);
+          const int loc = (int)(c & lmask);
           // shared-memory read-filter (the mailbox.py:159 short-circuit),
           // then the combine; both on the SM, no L2 request
           if (msg < s_mb[loc]) atomicMin(s_mb + loc, msg);
@@ -224,7 +225,6 @@ __device__ void seg_scatter_phase(const SegPass &a, char *smem_raw) {
     }
     __syncthreads();
   }
-  (void)m32;
 }
 
 }  // namespace pgx

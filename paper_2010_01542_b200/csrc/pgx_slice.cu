@@ -4,6 +4,7 @@
 // slices onto their owners between the two (NCCL via torch.distributed).
 #include "pgx_apply.cuh"
 #include "pgx_common.cuh"
+#include "pgx_gather.cuh"
 #include "pgx_scatter.cuh"
 
 namespace pgx {
@@ -100,10 +101,16 @@ __global__ void __launch_bounds__(kBlock) apply_slice_kernel(
   if (threadIdx.x == 0 && bcast) atomicAdd(&ctr->bcast, bcast);
 }
 
+// PageRank apply of an owned slice.  `dangling` is the job's dangling mass
+// after the previous superstep (device scalar: summed over ranks by a
+// collective on the stream, no host read), dn = dangling / n as in the
+// single-GPU kernel (algorithms.py:61-73).
 __global__ void __launch_bounds__(kBlock) pr_apply_slice_kernel(
     int32_t len, const int32_t *__restrict__ row_ptr, double *rank, double *mailbox,
-    double *share, double base, double damping, double dn, int32_t last, double *partials) {
+    double *share, double base, double damping, const double *dangling, double n_total,
+    int32_t last, double *partials) {
   __shared__ double s_red[32];
+  const double dn = __ddiv_rn(*dangling, n_total);
   const int v = blockIdx.x * kBlock + threadIdx.x;
   double my_d = 0.0;
   if (v < len) {
@@ -117,6 +124,28 @@ __global__ void __launch_bounds__(kBlock) pr_apply_slice_kernel(
   }
   const double b = block_sum<double>(my_d, s_red);
   if (threadIdx.x == 0) partials[blockIdx.x] = b;
+}
+
+// Pull fold of a rank's slice (the reference's PR mode, engine.py:425-457):
+// K3 over the rank's local in-CSR (rows = padded mailbox positions, ids =
+// local sources), writing the full-width partial fold; rows spanning tiles
+// leave head / tail partials for fold_spanning_kernel.
+__global__ void __launch_bounds__(kBlock, PGX_MIN_BLOCKS) gather_slice_kernel(GatherArgs g) {
+  extern __shared__ __align__(16) char smem[];
+  gather_phase(g, smem);
+}
+
+// rows whose in-edges span tiles: tail of the first tile + heads of the
+// later ones, in tile order (the persistent kernel's combine)
+__global__ void fold_spanning_kernel(int32_t nspan, const int32_t *rows, const int32_t *t0,
+                                     const int32_t *t1, const double *head, const double *tail,
+                                     double *folded) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < nspan; i += gridDim.x * blockDim.x) {
+    const int a = t0[i], b = t1[i];
+    double f = tail[a];
+    for (int t = a + 1; t <= b; t++) f = __dadd_rn(f, head[t]);
+    folded[rows[i]] = f;
+  }
 }
 
 __global__ void slice_init_kernel(int app, int32_t len, int32_t lo, uint32_t *val,
@@ -476,15 +505,79 @@ int pgx_apply_slice(int app, int32_t len, const int32_t *row_ptr, uint32_t *val,
 }
 
 int pgx_pr_apply_slice(int32_t len, const int32_t *row_ptr, double *rank, double *mailbox_slice,
-                       double *share, double base, double damping, double dangling_over_n,
-                       int32_t last, double *partials, uintptr_t stream) {
-  if (len < 0 || (len && (!row_ptr || !rank || !mailbox_slice || !share || !partials)))
+                       double *share, double base, double damping, const double *dangling,
+                       double n_total, int32_t last, double *partials, uintptr_t stream) {
+  if (len < 0 || !(n_total >= 1.0) ||
+      (len && (!row_ptr || !rank || !mailbox_slice || !share || !partials || !dangling)))
     return fail(PGX_EINVAL, "bad pr_apply_slice arguments");
   if (!len) return PGX_OK;
   const int grid = (int)ceil_div(len, kBlock);
   pr_apply_slice_kernel<<<grid, kBlock, 0, (cudaStream_t)stream>>>(
-      len, row_ptr, rank, mailbox_slice, share, base, damping, dangling_over_n, last, partials);
+      len, row_ptr, rank, mailbox_slice, share, base, damping, dangling, n_total, last, partials);
   PGX_CUDA(cudaGetLastError());
+  return PGX_OK;
+}
+
+int pgx_gather_slice(int32_t nrows, int64_t m, const int32_t *in_col, const void *in_graph_ws,
+                     int32_t nsrc, const double *share, double *folded, double *head,
+                     double *tail, uintptr_t stream) {
+  if (nrows < 1 || m < 0 || m > INT32_MAX || nsrc < 0 || nsrc > nrows)
+    return fail(PGX_EINVAL, "bad gather_slice sizes");
+  if (!m) return PGX_OK;
+  if (!in_col || !in_graph_ws || !share || !folded || !head || !tail)
+    return fail(PGX_EINVAL, "null gather_slice pointer");
+  if (reinterpret_cast<uintptr_t>(in_col) % 32)  // 256-bit id loads in the fold
+    return fail(PGX_EINVAL, "in_col must be 32-byte aligned");
+  GraphWs w;
+  graph_ws_layout(nrows, m, &w, (char *)in_graph_ws);
+  GatherArgs g;
+  g.in_col = in_col;
+  g.eb = w.nz_eb;
+  g.ids = w.nz_id;
+  g.tile_src = w.tile_src;
+  g.nsrc = nsrc;  // the workspace header's non-zero row count (host copy)
+  g.E = m;
+  g.share = share;
+  g.folded = folded;
+  g.head = head;
+  g.tail = tail;
+  g.n = INT32_MAX;  // local source ids: unchecked
+  cudaStream_t st = (cudaStream_t)stream;
+  const size_t smem = (size_t)kWarps * kSlots * 8 + 16;
+  int sms = 148, dev = 0;
+  if (cudaGetDevice(&dev) == cudaSuccess)
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const int grid = (int)std::max<int64_t>(
+      1, std::min<int64_t>(ceil_div(ceil_div(m, kTile), kWarps), (int64_t)sms * PGX_MIN_BLOCKS));
+  PGX_CUDA(cudaFuncSetAttribute(gather_slice_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                (int)smem));
+  gather_slice_kernel<<<grid, kBlock, smem, st>>>(g);
+  PGX_CUDA(cudaGetLastError());
+  return PGX_OK;
+}
+
+int pgx_fold_spanning(int32_t nspan, const int32_t *rows, const int32_t *t0, const int32_t *t1,
+                      const double *head, const double *tail, double *folded, uintptr_t stream) {
+  if (nspan < 0 || (nspan && (!rows || !t0 || !t1 || !head || !tail || !folded)))
+    return fail(PGX_EINVAL, "bad fold_spanning arguments");
+  if (!nspan) return PGX_OK;
+  const int grid = (int)std::min<int64_t>(ceil_div(nspan, 256), 148 * 8);
+  fold_spanning_kernel<<<grid, 256, 0, (cudaStream_t)stream>>>(nspan, rows, t0, t1, head, tail,
+                                                               folded);
+  PGX_CUDA(cudaGetLastError());
+  return PGX_OK;
+}
+
+int pgx_peer_enable(int32_t peer_device) {
+  int dev = 0;
+  PGX_CUDA(cudaGetDevice(&dev));
+  if (peer_device == dev) return PGX_OK;
+  const cudaError_t e = cudaDeviceEnablePeerAccess(peer_device, 0);
+  if (e == cudaErrorPeerAccessAlreadyEnabled) {
+    cudaGetLastError();  // clear the sticky-free "already enabled" status
+    return PGX_OK;
+  }
+  if (e != cudaSuccess) return cuda_fail(e, "cudaDeviceEnablePeerAccess");
   return PGX_OK;
 }
 

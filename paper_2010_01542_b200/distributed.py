@@ -5,44 +5,54 @@ B200 build's scale-out of the same superstep, with results identical to
 one GPU (CC labels / SSSP distances bit-exact, PageRank within 1e-9):
 
 * **partition**: 1-D by source vertex.  Rank r owns the contiguous vertex
-  range ``[lo_r, hi_r)`` -- its out-edges (a local CSR with GLOBAL
-  destination ids) and that slice of the mailbox.  Ranges follow the
-  reference's exact integer edge-balance rule (``edge_balanced_partition``,
-  scheduler.py:91-116) over ``out_degree + 1`` (edges + vertex work);
-* **per superstep**: every rank scatters its senders into a full-width
-  local mailbox (``pgx_scatter``); one reduction per owner delivers the
-  combined slice (``min`` for CC/SSSP, ``sum`` for PageRank) -- issued as
-  ``len(world)`` ``reduce`` calls, which NCCL runs over NVLink/NVSwitch;
-  the owner applies on its slice (``pgx_apply_slice`` /
-  ``pgx_pr_apply_slice``); an ``all_reduce`` of the counters (recipients,
-  broadcasts, senders, edges, dangling mass) drives the halt test.  No
-  all-gather is needed: a sender is always local to its owner.
+  range ``[lo_r, hi_r)`` -- its out-edges and that block of the mailbox.
+  Ranges balance ``out_degree + 1`` (edges + vertex work) across ranks
+  (``partition_bounds``).
+* **owner-blocked mailbox**: every rank's full-width mailbox is laid out as
+  ``world`` equal blocks of ``B`` slots (B = the largest range, rounded up
+  to 64): vertex v of owner r lives at position ``r * B + (v - lo_r)``.  The
+  local CSR stores those positions (remapped once per graph), so the
+  per-superstep reduction is ONE equal-block ``reduce_scatter_tensor``
+  (ncclReduceScatter, in place, NVLS-eligible) instead of per-owner
+  reduces, and the owner of a slot is ``slot // B``.  Messages stay global
+  vertex ids (CC labels, SSSP distances).
+* **per superstep** (min programs): every rank scatters its senders into
+  its full-width mailbox (``pgx_scatter``); the mailbox is delivered to the
+  owners by one of three exchanges (below); the owner applies on its block
+  (``pgx_apply_slice``); ONE all-gather of every rank's (recipients,
+  broadcasts, senders, edges) drives the halt test and the statistics and
+  sizes the next scatter -- the only host read of the superstep (plus the
+  split sizes on a sparse superstep).
+* **exchanges** (min programs, chosen per superstep, collectively):
+  - ``peer`` (the fused compute + collective): when every rank maps every
+    other rank's mailbox (CUDA IPC over NVLink / NVSwitch, ``pgx_peer_*``),
+    ``pgx_scatter_peer`` combines each message that passes the rank's local
+    filter straight into the OWNER's slot with a system-scope
+    ``red.min`` -- no reduction at all; a one-element all-reduce orders the
+    combines before the owners' apply.  Used for supersteps that traverse
+    at most n/2 edges ("auto") or always ("peer");
+  - ``dense``: the equal-block ``reduce_scatter_tensor`` (MIN), used for the
+    big supersteps;
+  - ``sparse`` (when no peer mapping exists): if every
+    rank's edges bound its touched foreign slots below a quarter of the
+    dense volume, the touched slots are compacted into (slot, value) pairs
+    (grouped by owner) and exchanged with ``all_to_all_single``.
+* **PageRank**: the reference's pull fold (engine.py:425-457) per rank --
+  a local in-CSR of the rank's out-edges (rows = mailbox positions,
+  entries = local sources), folded with the K3 kernel into a full-width
+  partial sum (``pgx_gather_slice`` + ``pgx_fold_spanning``), then the
+  SUM ``reduce_scatter_tensor``.  The dangling mass is all-reduced on the
+  device and read by the next apply from device memory: a PageRank
+  superstep has no host synchronisation.  ``pr_mode="push"`` keeps the
+  ``red.add.f64`` scatter as the A/B arm.
 * has-message after the reduction is ``mailbox != neutral``: CC / SSSP
-  messages are < n <= 2^31 and never equal UINT32_MAX, and PageRank needs
-  no flag (the paper's neutral-value caveat).
-* **fused peer exchange** (min programs, the default when every rank can
-  map every other rank's mailbox): the scatter kernel itself combines each
-  message that passes its local filter into the OWNER's mailbox slot over
-  NVLink peer memory (``pgx_scatter_peer``: one fire-and-forget
-  ``red.min`` per surviving foreign message, a system-scope fence at the
-  end), so the mailbox is never reduced by a collective: a one-element
-  all-reduce after the scatter orders the peers' combines before the
-  owners' apply.  Mailboxes are ``cudaMalloc`` blocks shared by CUDA IPC
-  (``pgx_peer_alloc`` / ``pgx_peer_open``); ranks that are threads of one
-  process use the raw pointers.  The choice is collective: if any rank
-  cannot map a peer, every rank falls back to the collective exchanges.
-* **sparse exchange** (SURVEY 8(f) row 3): late supersteps touch few
-  mailbox slots, yet the dense reduction always moves n slots.  Every rank
-  counts the slots it touched outside its own range (has-bits of the
-  scatter); when the largest count makes 8-byte (slot, value) pairs cheaper
-  than half the dense volume, the ranks compact their touched slots in
-  vertex order (grouped by owner) and exchange them with one variable-size
-  ``all_to_all_single``; owners min-combine what they receive.  The choice
-  is collective (an all-reduce of the counts) and recorded per superstep.
+  messages are < n < 2^31 - 1 and never equal the exchange neutral
+  INT32_MAX (the signed int32 MIN of NCCL / gloo is then exact).
 
 The orchestration below is backend-agnostic: ``CudaBackend`` drives
 libpgx.so on the rank's GPU (NCCL process group); tests/ drive the same
-``PartitionedRun`` with a CPU test backend over a gloo process group.
+``PartitionedRun`` with a CPU test backend over a gloo process group and
+with the CUDA backend on threads sharing one GPU.
 """
 
 from __future__ import annotations
@@ -56,11 +66,13 @@ from dataclasses import dataclass
 import numpy as np
 import torch
 
-from .scheduler import edge_balanced_partition
-
 #: min neutral of the exchanged mailbox: INT32_MAX, so that the signed
 #: int32 MIN reduction of NCCL / gloo is exact (messages are < n < 2^31 - 1)
 EXCHANGE_NEUTRAL = 2 ** 31 - 1
+
+#: mailbox blocks are padded to a multiple of this many slots (has-bitmask
+#: words and 128-byte lines never straddle two owners)
+BLOCK_ALIGN = 64
 
 
 def distributed_context():
@@ -77,9 +89,46 @@ def distributed_context():
 
 
 def partition_bounds(out_degrees, world: int) -> np.ndarray:
-    """Owner ranges ``bounds[r]..bounds[r+1]`` (edge + vertex balanced)."""
-    deg = np.asarray(out_degrees, dtype=np.int64)
-    return edge_balanced_partition(deg + 1, world).boundaries.astype(np.int64)
+    """Contiguous owner ranges ``bounds[r]..bounds[r+1]`` balancing
+    ``out_degree + 1`` per vertex: range r ends at the first vertex whose
+    inclusive work prefix reaches ``(r + 1) / world`` of the total (exact
+    integer comparison), so every range carries less than
+    ``total / world + max work`` and an empty graph gives empty ranges."""
+    if world < 1:
+        raise ValueError(f"world size must be >= 1, got {world}")
+    w = torch.as_tensor(np.asarray(out_degrees, dtype=np.int64)) + 1
+    n = int(w.numel())
+    bounds = np.zeros(world + 1, dtype=np.int64)
+    bounds[-1] = n
+    if n == 0 or world == 1:
+        return bounds
+    prefix = torch.cumsum(w, 0)                       # inclusive work prefix
+    total = int(prefix[-1])
+    goal = torch.arange(1, world, dtype=torch.int64) * total
+    cut = torch.searchsorted(prefix * world, goal, right=False) + 1
+    bounds[1:-1] = np.minimum(cut.numpy(), n)
+    return np.maximum.accumulate(bounds)
+
+
+def owner_block(bounds) -> int:
+    """Slots per owner block of the padded mailbox."""
+    sizes = np.diff(np.asarray(bounds, dtype=np.int64))
+    big = int(sizes.max()) if sizes.size else 0
+    return max(BLOCK_ALIGN, -(-big // BLOCK_ALIGN) * BLOCK_ALIGN)
+
+
+def padded_positions(col: torch.Tensor, bounds, block: int,
+                     chunk: int = 1 << 27) -> torch.Tensor:
+    """Global vertex ids -> owner-blocked mailbox positions (int32), in
+    chunks (the int64 temporaries stay bounded)."""
+    inner = torch.as_tensor(np.asarray(bounds[1:-1], dtype=np.int64), device=col.device)
+    lo = torch.as_tensor(np.asarray(bounds[:-1], dtype=np.int64), device=col.device)
+    out = torch.empty(col.numel(), dtype=torch.int32, device=col.device)
+    for a in range(0, col.numel(), chunk):
+        c = col[a:a + chunk].to(torch.int64)
+        owner = torch.searchsorted(inner, c, right=True)
+        out[a:a + chunk] = (owner * block + c - lo[owner]).to(torch.int32)
+    return out
 
 
 @dataclass
@@ -88,7 +137,6 @@ class StepCounts:
     broadcasts: int
     senders: int
     edges: int
-    dangling: float = 0.0
 
 
 class PartitionedRun:
@@ -103,28 +151,28 @@ class PartitionedRun:
         self.n, self.m = n, m
         self.lo = int(self.bounds[self.rank])
         self.hi = int(self.bounds[self.rank + 1])
+        self.B = owner_block(self.bounds)
+        self.npad = self.world * self.B
+        self.b.bind(self.bounds, self.rank, self.B)
         # min-program exchange: "auto" (peer if every rank maps every peer,
         # else hybrid), "peer", "hybrid" (dense / sparse per superstep),
         # "dense" (A/B switches)
         self.exchange = "auto"
-        self._coalesced = None  # NCCL uneven reduce_scatter available?
         be = str(getattr(dist, "get_backend", lambda: "")())
-        # gloo has no CUDA all_gather: small collectives go through the host
+        # gloo has no CUDA collectives: stage device tensors through the host
         self._host_coll = be == "gloo" and self.b.device.type == "cuda"
         self._cdev = torch.device("cpu") if self._host_coll else self.b.device
-
-    @property
-    def sparse_ok(self) -> bool:
-        return self.exchange != "dense"
-
-    @sparse_ok.setter
-    def sparse_ok(self, ok: bool):
-        self.exchange = "auto" if ok else "dense"
 
     def _coll_sync(self):
         """Before a host-side collective: the rank's kernels have finished."""
         if self._host_coll:
             torch.cuda.current_stream(self.b.device).synchronize()
+
+    def _to_coll(self, t: torch.Tensor) -> torch.Tensor:
+        if self._host_coll:
+            self._coll_sync()
+            return t.cpu()
+        return t
 
     def _peer_setup(self) -> bool:
         """Map every rank's mailbox on every rank (collective decision).
@@ -136,14 +184,11 @@ class PartitionedRun:
         if cached is not None and cached[0] == self.exchange:
             self.b.peer_active = cached[1]
             return cached[1]
-        if self.exchange not in ("auto", "peer") or not hasattr(self.b, "peer_handle"):
-            want = False
-        else:
-            want = True
+        want = self.exchange in ("auto", "peer") and hasattr(self.b, "peer_handle")
         h = self.b.peer_handle() if want else None
         handles = [None] * self.world
         self.dist.all_gather_object(handles, h)
-        ok = all(x is not None for x in handles) and self.b.open_peers(handles, self.bounds)
+        ok = all(x is not None for x in handles) and self.b.open_peers(handles)
         t = torch.tensor([1 if ok else 0], dtype=torch.int64, device=self._cdev)
         self._coll_sync()
         self.dist.all_reduce(t, op=self.dist.ReduceOp.MIN)
@@ -163,83 +208,56 @@ class PartitionedRun:
     # ---- collectives --------------------------------------------------
 
     def _reduce_slices(self, op):
-        """Deliver every owner the reduction of its mailbox slice."""
+        """Deliver every owner the reduction of its mailbox block: one
+        equal-block reduce_scatter, in place (output = this rank's block of
+        the input)."""
+        full = self.b.mailbox
+        mine = full[self.rank * self.B:(self.rank + 1) * self.B]
         if self._host_coll:  # gloo: stage the mailbox through the host
             self._coll_sync()
-            full = self.b.mailbox.cpu()
-            for r in range(self.world):
-                part = full[int(self.bounds[r]):int(self.bounds[r + 1])]
-                if part.numel():
-                    self.dist.reduce(part, dst=r, op=op)
-            self.b.mailbox[self.lo:self.hi].copy_(full[self.lo:self.hi])
+            host = full.cpu()
+            out = torch.empty(self.B, dtype=host.dtype)
+            self.dist.reduce_scatter_tensor(out, host, op=op)
+            mine.copy_(out)
             return
-        full = self.b.mailbox
-        parts = [full[int(self.bounds[r]):int(self.bounds[r + 1])] for r in range(self.world)]
-        backend = getattr(self.dist, "get_backend", lambda: None)()
-        if self._coalesced is not False and str(backend) == "nccl":
-            # one uneven reduce_scatter: NCCL coalesces the per-owner reduces
-            try:
-                self.dist.reduce_scatter(parts[self.rank], parts, op=op)
-                self._coalesced = True
-                return
-            except Exception:  # pragma: no cover - torch without uneven support
-                self._coalesced = False
-        for r, part in enumerate(parts):
-            if part.numel():
-                self.dist.reduce(part, dst=r, op=op)
+        self.dist.reduce_scatter_tensor(mine, full, op=op)
 
-    def _exchange_min(self, op, allow_sparse: bool = True) -> str:
-        """Dense per-owner reduction or sparse pair exchange (collective choice)."""
-        if not allow_sparse:  # a big superstep: dense, no count, no host sync
-            self._reduce_slices(op)
-            self.b.dense_exchanged()
-            return "dense"
-        touched = self.b.touched_count()
-        t = torch.tensor([touched], dtype=torch.int64, device=self._cdev)
-        self.dist.all_reduce(t, op=self.dist.ReduceOp.MAX)
-        if self.exchange != "dense" and 8 * int(t.item()) * 2 < 4 * self.n:
-            pairs, splits = self.b.compact_touched(self.bounds)
-            pairs = pairs.to(self._cdev)
-            sc = torch.tensor(splits, dtype=torch.int64, device=self._cdev)
-            rc = torch.empty_like(sc)
-            self.dist.all_to_all_single(rc, sc)
-            recv_splits = rc.tolist()
-            recv = torch.empty(sum(recv_splits), dtype=torch.int64, device=self._cdev)
+    def _exchange_min(self, op, max_edges: int, allow_sparse: bool) -> str:
+        """Dense block reduction or sparse pair exchange.  The choice uses
+        every rank's edge count (a bound on its touched foreign slots, known
+        to all ranks from the counters all-gather): collective without a
+        further reduction."""
+        if allow_sparse and self.exchange != "dense" and 16 * max_edges < 4 * self.npad:
+            pairs, splits = self.b.compact_touched()           # one host read
+            send = torch.tensor(splits, dtype=torch.int64, device=self._cdev)
+            recv_n = torch.empty_like(send)
+            self.dist.all_to_all_single(recv_n, send)
+            recv_splits = recv_n.tolist()
+            pairs = self._to_coll(pairs)
+            recv = torch.empty(sum(recv_splits), dtype=torch.int64, device=pairs.device)
             self.dist.all_to_all_single(recv, pairs, recv_splits, list(splits))
             self.b.scatter_pairs(recv.to(self.b.device))
             return "sparse"
         self._reduce_slices(op)
-        self.b.dense_exchanged()
         return "dense"
 
-    def _gather_counts(self, local: torch.Tensor) -> StepCounts:
+    def _gather_counts(self, local: torch.Tensor):
         """Every rank's (recipients, broadcasts, senders, edges) in ONE
         all-gather and one host read: the sums drive the halt test and the
         statistics, the rank's own senders / edges size its next scatter."""
-        local = local.to(device=self._cdev, dtype=torch.int64)
+        local = self._to_coll(local.to(torch.int64))
         parts = [torch.empty_like(local) for _ in range(self.world)]
-        self._coll_sync()
         self.dist.all_gather(parts, local)
         rows = [self.b.decode_counts(r) for r in torch.stack(parts).tolist()]
         self.b.set_frontier(rows[self.rank][2], rows[self.rank][3])
         tot = [sum(r[i] for r in rows) for i in range(4)]
-        return StepCounts(*tot)
-
-    def _allreduce_counts(self, c: StepCounts) -> StepCounts:
-        t = torch.tensor([c.recipients, c.broadcasts, c.senders, c.edges],
-                         dtype=torch.int64, device=self._cdev)
-        self._coll_sync()
-        self.dist.all_reduce(t)
-        d = torch.tensor([c.dangling], dtype=torch.float64, device=self._cdev)
-        self.dist.all_reduce(d)
-        v = t.tolist()
-        return StepCounts(v[0], v[1], v[2], v[3], float(d.item()))
+        return StepCounts(*tot), max(r[3] for r in rows)
 
     def _gather_values(self):
-        local = self.b.values().to(self._cdev)
+        local = self._to_coll(self.b.values())
         sizes = np.diff(self.bounds)
-        mx = int(sizes.max())
-        pad = torch.zeros(mx, dtype=local.dtype, device=local.device)
+        mx = int(sizes.max()) if sizes.size else 0
+        pad = torch.zeros(max(mx, 1), dtype=local.dtype, device=local.device)
         pad[:local.numel()] = local
         parts = [torch.empty_like(pad) for _ in range(self.world)]
         self.dist.all_gather(parts, pad)
@@ -248,10 +266,16 @@ class PartitionedRun:
     # ---- min programs: CC / SSSP -------------------------------------
 
     def run_min(self, app: str, source: int, max_steps: int):
+        """loop_min, then every rank's values gathered (rank order)."""
+        stats, hit_cap, wall = self.loop_min(app, source, max_steps)
+        return self._gather_values(), stats, hit_cap, wall
+
+    def loop_min(self, app: str, source: int, max_steps: int):
+        """The superstep loop of a CC / SSSP run; values stay on the rank."""
         op = self.dist.ReduceOp.MIN
         n = self.n
         peer_ok = self._peer_setup()
-        self.b.init_min(app, self.lo, self.hi)
+        self.b.init_min(app)
         if peer_ok:  # every mailbox is neutral before any peer combines into it
             self._fence()
         stats = []
@@ -261,8 +285,10 @@ class PartitionedRun:
             if own:
                 self.b.seed_source(source - self.lo)
             nxt = StepCounts(0, 1, 1 if deg > 0 else 0, deg)
+            max_edges = deg
         else:
             nxt = StepCounts(0, n, self.b.global_nonzero_degree(), self.m)
+            max_edges = self.m
         hit_cap = False
         t0 = time.perf_counter()
         active = n  # superstep 0 runs every vertex
@@ -274,16 +300,15 @@ class PartitionedRun:
             # the dense collective (n slots per rank) for the big ones
             use_peer = peer_ok and (self.exchange == "peer" or 2 * cur.edges <= n)
             self.b.reset_mailbox()
-            self.b.scatter_min(dense=(app == "components" and s == 0),
-                               id_offset=self.lo, peer=use_peer)
+            self.b.scatter_min(dense=(app == "components" and s == 0), peer=use_peer)
             if use_peer:
                 self._fence()
                 exchange = "peer"
-            else:  # auto with the peer path mapped: only big supersteps get here
-                exchange = self._exchange_min(op, allow_sparse=not peer_ok)
+            else:  # with the peer path mapped only big supersteps get here
+                exchange = self._exchange_min(op, max_edges, allow_sparse=not peer_ok)
             self.b.exchanged(exchange)
             at_cap = s + 1 == max_steps
-            nxt = self._gather_counts(self.b.apply_min(app, count_only=at_cap))
+            nxt, max_edges = self._gather_counts(self.b.apply_min(app, count_only=at_cap))
             sent = cur.edges if app == "sssp" else cur.broadcasts
             stats.append(dict(index=s, active_count=active,
                               messages_sent=sent, edges=cur.edges,
@@ -296,44 +321,50 @@ class PartitionedRun:
             if at_cap:
                 hit_cap = True
                 break
-        values = self._gather_values()
-        return values, stats, hit_cap, time.perf_counter() - t0
+        return stats, hit_cap, time.perf_counter() - t0
 
     # ---- PageRank -------------------------------------------------------
 
     def run_pagerank(self, iterations: int, damping: float, max_steps: int):
+        """loop_pagerank, then every rank's ranks gathered (rank order)."""
+        stats, hit_cap, wall = self.loop_pagerank(iterations, damping, max_steps)
+        return self._gather_values(), stats, hit_cap, wall
+
+    def loop_pagerank(self, iterations: int, damping: float, max_steps: int):
+        """The superstep loop of a PageRank run; ranks stay on the rank.
+        No host read inside the loop: the dangling mass stays on the device."""
         op = self.dist.ReduceOp.SUM
         n = self.n
         base = (1.0 - damping) / n      # algorithms.py:49
         r0 = 1.0 / n                    # algorithms.py:50
         last = iterations - 1
-        ndangling = self.b.init_pagerank(self.lo, self.hi, r0)
+        ndangling = self.b.init_pagerank(r0)
         t = torch.tensor([ndangling], dtype=torch.int64, device=self._cdev)
+        self._coll_sync()
         self.dist.all_reduce(t)
         ndangling = int(t.item())
-        dangling = r0 * ndangling       # algorithms.py:55
         nspread = n - ndangling
+        # algorithms.py:55: the setup's dangling mass, then each superstep's
+        dangling = torch.tensor([r0 * ndangling], dtype=torch.float64, device=self.b.device)
         stats = []
         t0 = time.perf_counter()
         steps = min(max_steps, iterations)
         for s in range(steps):
             ts = time.perf_counter()
             # the fold of superstep s: shares broadcast at s-1 (or the seed)
-            self.b.reset_mailbox()
-            self.b.scatter_sum()
+            self.b.fold_sum()
             self._reduce_slices(op)
-            local_d = self.b.apply_pagerank(base, damping, dangling / n, s == last)
-            d = torch.tensor([local_d], dtype=torch.float64, device=self._cdev)
+            local = self.b.apply_pagerank(base, damping, dangling, s == last)
+            d = self._to_coll(local)
             self.dist.all_reduce(d)
-            dangling = float(d.item())
+            dangling = d.to(self.b.device)
             stats.append(dict(index=s, active_count=n,
                               messages_sent=0 if s == last else nspread,
                               edges=self.m, senders=nspread, recipients=n,
                               broadcasters=0 if s == last else nspread,
                               seconds=time.perf_counter() - ts))
         hit_cap = steps < iterations  # engine.py:299-300
-        values = self._gather_values()
-        return values, stats, hit_cap, time.perf_counter() - t0
+        return stats, hit_cap, time.perf_counter() - t0
 
 
 # ----------------------------------------------------------------------
@@ -360,6 +391,7 @@ class PeerMailbox:
         _lib.check(lib.pgx_peer_alloc(4 * max(n, 1), ctypes.byref(ptr), handle),
                    "pgx_peer_alloc")
         self.ptr = int(ptr.value)
+        self.n = n
         self.handle = handle.raw
         self.tensor = torch.as_tensor(_DeviceArray(self.ptr, n, "<i4"), device=device)
         # freed with its owner (the backend drops it only after its last run)
@@ -367,14 +399,15 @@ class PeerMailbox:
 
 
 class CudaBackend:
-    """Owns the rank's local CSR, full-width mailbox and owned-slice state."""
+    """Owns the rank's local CSR, full-width mailbox and owned-block state."""
 
-    def __init__(self, graph, lo: int, hi: int, device):
+    def __init__(self, graph, lo: int, hi: int, device, pr_mode: str = "pull"):
         from . import _lib
         self._lib = _lib
         self.lib = _lib.load()
         self.device = torch.device(device)
         self.stream = torch.cuda.current_stream(self.device)
+        self.pr_mode = pr_mode
         dev = self.device
         # slice where the graph lives and upload only this rank's rows (a
         # pinned host graph stays pinned under slicing: one DMA per array)
@@ -384,10 +417,13 @@ class CudaBackend:
         base, end = int(off[lo]), int(off[hi])
         self.row_ptr = (off[lo:hi + 1] - base).to(dev, non_blocking=True) \
             .to(torch.int32).contiguous()
-        self.col = graph.out_targets[base:end].to(dev, non_blocking=True) \
+        self.col_global = graph.out_targets[base:end].to(dev, non_blocking=True) \
             .to(torch.int32).contiguous()
+        self.col = self.col_global          # padded positions after bind()
         self.len = hi - lo
+        self.lo_own, self.hi_own = lo, hi
         self.m_local = int(self.col.numel())
+        self.launches = 0
         st = self.stream.cuda_stream
         ws_bytes = _lib.out_size(self.lib.pgx_graph_workspace_bytes, max(self.len, 1),
                                  self.m_local)
@@ -397,29 +433,19 @@ class CudaBackend:
                                                   self.row_ptr.data_ptr(),
                                                   self.gws.data_ptr(), ws_bytes, st),
                        "pgx_graph_prepare")
-        # graph workspace layout (pgx_engine.cu graph_ws_layout): hdr, nz_id,
-        # nz_eb, tile_src, blk -- 256-byte aligned chunks
-        al = lambda x: (x + 255) // 256 * 256
-        o_id = al(16)
-        o_eb = o_id + al(4 * (self.len + 1))
-        o_tile = o_eb + al(4 * (self.len + 1))
-        self._g_hdr = self.gws[:16].view(torch.int32)
-        self._g_nz_id = self.gws[o_id:o_id + 4 * (self.len + 1)].view(torch.int32)
-        self._g_nz_eb = self.gws[o_eb:o_eb + 4 * (self.len + 1)].view(torch.int32)
-        ntile = (self.m_local + 255) // 256 + 2
-        self._g_tile = self.gws[o_tile:o_tile + 4 * ntile].view(torch.int32)
+        self._g_hdr, self._g_nz_id, self._g_nz_eb, self._g_tile = \
+            self._graph_views(self.gws, self.len, self.m_local)
         cb = _lib.out_size(self.lib.pgx_slice_counters_bytes)
         self.ctr = torch.zeros(cb, dtype=torch.uint8, device=dev)
+        ntile = (self.m_local + 255) // 256 + 2
         self.f_eb = torch.empty(self.len + 1, dtype=torch.int32, device=dev)
         self.f_rs = torch.empty(self.len + 1, dtype=torch.int32, device=dev)
         self.f_msg = torch.empty(self.len + 1, dtype=torch.int32, device=dev)
         self.f_tile = torch.empty(ntile, dtype=torch.int32, device=dev)
         self.nsrc, self.E = 0, 0
-        self.lo_own, self.hi_own = lo, hi
-        self.has = torch.zeros(self.n // 32 + 2, dtype=torch.int32, device=dev)
-        sb = _lib.out_size(self.lib.pgx_touched_scratch_bytes, self.n)
-        self.tscratch = torch.empty(sb, dtype=torch.uint8, device=dev)
-        self.tcount = torch.zeros(1, dtype=torch.int64, device=dev)
+        self._scattered = 0
+        self._bound = None
+        self._pull = None
         self._last = None
         # fused peer exchange state (PartitionedRun._peer_setup)
         self.peer_active = False
@@ -430,10 +456,51 @@ class CudaBackend:
         weakref.finalize(self, CudaBackend._close_all, self.lib, self._opened)
 
     @staticmethod
+    def _graph_views(gws, rows, m):
+        """(hdr, nz_id, nz_eb, tile_src) views of a graph workspace
+        (pgx_common.cuh graph_ws_layout: 256-byte aligned chunks)."""
+        al = lambda x: (x + 255) // 256 * 256
+        o_id = al(16)
+        o_eb = o_id + al(4 * (rows + 1))
+        o_tile = o_eb + al(4 * (rows + 1))
+        ntile = (m + 255) // 256 + 2
+        return (gws[:16].view(torch.int32), gws[o_id:o_id + 4 * (rows + 1)].view(torch.int32),
+                gws[o_eb:o_eb + 4 * (rows + 1)].view(torch.int32),
+                gws[o_tile:o_tile + 4 * ntile].view(torch.int32))
+
+    def _k(self, rc, name, kernels=1):
+        """Check a libpgx launch and count its kernels (bench gpu_launches)."""
+        self.launches += kernels
+        self._lib.check(rc, name)
+
+    @staticmethod
     def _close_all(lib, opened):
         for p in opened:
             lib.pgx_peer_close(ctypes.c_void_p(p))
         opened.clear()
+
+    # ---- layout ----
+    def bind(self, bounds, rank: int, block: int):
+        """Adopt the job's owner-blocked layout: destinations become padded
+        mailbox positions (once per bounds)."""
+        sig = (tuple(int(x) for x in bounds), rank, block)
+        if self._bound == sig:
+            return
+        self.rank, self.block, self.world = rank, block, len(bounds) - 1
+        self.npad = self.world * block
+        self.blo = rank * block                       # this rank's block
+        with torch.cuda.device(self.device), torch.cuda.stream(self.stream):
+            self.col = padded_positions(self.col_global, bounds, block)
+            self.has = torch.zeros(self.npad // 32 + 2, dtype=torch.int32, device=self.device)
+            sb = self._lib.out_size(self.lib.pgx_touched_scratch_bytes, self.npad)
+            self.tscratch = torch.empty(sb, dtype=torch.uint8, device=self.device)
+            self.tcount = torch.zeros(1, dtype=torch.int64, device=self.device)
+            self._pbounds = torch.arange(self.world + 1, dtype=torch.int32,
+                                         device=self.device) * block
+        self._pull = None
+        self._peer_sig = None
+        self._peer_decision = None
+        self._bound = sig
 
     # ---- helpers ----
     def _nnz(self) -> int:
@@ -450,29 +517,25 @@ class CudaBackend:
             self._nnz_global = int((torch.diff(self._glob_off) > 0).sum())
         return self._nnz_global
 
-    def _counters(self):
-        c = self.ctr[:32].view(torch.int64).tolist()
-        d = float(self.ctr[24:32].view(torch.float64).item())
-        return c, d
-
-    # ---- min programs ----
     # ---- fused peer exchange ----
     def peer_handle(self):
         """This rank's mappable mailbox (allocated once), or None."""
         try:
-            if self._peer_mb is None:
-                self._peer_mb = PeerMailbox(self._lib, self.lib, self.n, self.device)
+            if self._peer_mb is None or self._peer_mb.n != self.npad:
+                self._peer_mb = PeerMailbox(self._lib, self.lib, self.npad, self.device)
         except Exception:
             return None
-        return {"pid": os.getpid(), "ptr": self._peer_mb.ptr, "handle": self._peer_mb.handle}
+        return {"pid": os.getpid(), "device": self.device.index, "ptr": self._peer_mb.ptr,
+                "handle": self._peer_mb.handle}
 
     def close_peers(self):
         CudaBackend._close_all(self.lib, self._opened)  # in place: the finalizer's list
         self._peer_sig = None
 
-    def open_peers(self, handles, bounds) -> bool:
-        """Device array of every rank's mailbox base (IPC-mapped, or the raw
-        pointer for ranks that are threads of this process)."""
+    def open_peers(self, handles) -> bool:
+        """Device array of every rank's mailbox base: IPC-mapped, or the raw
+        pointer for ranks that are threads of this process (peer access
+        enabled when they sit on another GPU)."""
         sig = tuple((h["pid"], h["ptr"]) for h in handles)
         if sig == self._peer_sig:
             return True
@@ -481,36 +544,39 @@ class CudaBackend:
         try:
             for h in handles:
                 if h["pid"] == os.getpid():
+                    if h["device"] != self.device.index:
+                        with torch.cuda.device(self.device):
+                            self._lib.check(self.lib.pgx_peer_enable(h["device"]),
+                                            "pgx_peer_enable")
                     ptrs.append(h["ptr"])
                     continue
                 p = ctypes.c_void_p()
-                self._lib.check(self.lib.pgx_peer_open(h["handle"], ctypes.byref(p)),
-                                "pgx_peer_open")
+                with torch.cuda.device(self.device):
+                    self._lib.check(self.lib.pgx_peer_open(h["handle"], ctypes.byref(p)),
+                                    "pgx_peer_open")
                 self._opened.append(int(p.value))
                 ptrs.append(int(p.value))
         except Exception:
             self.close_peers()
             return False
         self._peer_ptrs = torch.tensor(ptrs, dtype=torch.int64, device=self.device)
-        self._bounds32 = torch.tensor(np.asarray(bounds), dtype=torch.int32, device=self.device)
-        self._world = len(handles)
         self._peer_sig = sig
         return True
 
-    def init_min(self, app, lo, hi):
+    # ---- min programs ----
+    def init_min(self, app):
         self.app = app
-        self.lo = lo
         if self.peer_active:
             self.mailbox = self._peer_mb.tensor
         else:
-            self.mailbox = torch.empty(self.n, dtype=torch.int32, device=self.device)
+            self.mailbox = torch.empty(self.npad, dtype=torch.int32, device=self.device)
         self.mailbox.fill_(EXCHANGE_NEUTRAL)
         self.has.zero_()
         self.val = torch.empty(max(self.len, 1), dtype=torch.int32, device=self.device)
         app_id = self._lib.PGX_APP_CC if app == "components" else self._lib.PGX_APP_SSSP
-        self._lib.check(self.lib.pgx_slice_init(app_id, self.len, lo, self.val.data_ptr(),
-                                                self.row_ptr.data_ptr(), None, 0.0,
-                                                self.stream.cuda_stream), "pgx_slice_init")
+        self._k(self.lib.pgx_slice_init(app_id, self.len, self.lo_own, self.val.data_ptr(),
+                                        self.row_ptr.data_ptr(), None, 0.0,
+                                        self.stream.cuda_stream), "pgx_slice_init")
         self.nsrc, self.E = 0, 0
         self._last = None  # exchange of the previous superstep
 
@@ -528,19 +594,17 @@ class CudaBackend:
 
     def reset_mailbox(self):
         """Undo what the previous superstep's exchange left behind.  The
-        owned slice is always neutral here (the apply consumed it), and it
+        owned block is always neutral here (the apply consumed it), and it
         is never written: a peer may already be combining into it."""
-        if self.app == "pagerank":
-            self.mailbox.zero_()
-            return
         if self._last == "peer":  # foreign filter copies back to neutral, bits cleared
-            self._lib.check(self.lib.pgx_reset_touched(
-                self.n, self.lo_own, self.hi_own, self.has.data_ptr(), self.mailbox.data_ptr(),
-                EXCHANGE_NEUTRAL, self.stream.cuda_stream), "pgx_reset_touched")
+            self._k(self.lib.pgx_reset_touched(
+                self.npad, self.blo, self.blo + self.block, self.has.data_ptr(),
+                self.mailbox.data_ptr(), EXCHANGE_NEUTRAL, self.stream.cuda_stream),
+                "pgx_reset_touched")
             return
         if self._last == "dense":  # every foreign slot holds a stale partial
-            self.mailbox[:self.lo_own].fill_(EXCHANGE_NEUTRAL)
-            self.mailbox[self.hi_own:].fill_(EXCHANGE_NEUTRAL)
+            self.mailbox[:self.blo].fill_(EXCHANGE_NEUTRAL)
+            self.mailbox[self.blo + self.block:].fill_(EXCHANGE_NEUTRAL)
         # sparse: the compaction reset the foreign touched slots
         if self._last is not None:
             self.has.zero_()
@@ -548,74 +612,61 @@ class CudaBackend:
     def exchanged(self, kind: str):
         self._last = kind
 
-    def dense_exchanged(self):
-        pass  # recorded by exchanged("dense")
-
-    def touched_count(self) -> int:
-        self._lib.check(self.lib.pgx_touched(
-            self.n, self.lo_own, self.hi_own, self.has.data_ptr(), None, EXCHANGE_NEUTRAL,
-            None, self.tcount.data_ptr(), self.tscratch.data_ptr(), self.stream.cuda_stream),
-            "pgx_touched")
-        return int(self.tcount.item())
-
-    def compact_touched(self, bounds):
-        cnt = int(self.tcount.item())
-        pairs = torch.empty(max(cnt, 1), dtype=torch.int64, device=self.device)
-        self._lib.check(self.lib.pgx_touched(
-            self.n, self.lo_own, self.hi_own, self.has.data_ptr(), self.mailbox.data_ptr(),
-            EXCHANGE_NEUTRAL, pairs.data_ptr(), self.tcount.data_ptr(),
-            self.tscratch.data_ptr(), self.stream.cuda_stream), "pgx_touched")
-        pairs = pairs[:cnt]
-        slots = pairs >> 32
-        b = torch.as_tensor(bounds[1:-1], dtype=torch.int64, device=self.device)
-        owner = torch.searchsorted(b, slots, right=True)
-        splits = torch.bincount(owner, minlength=len(bounds) - 1).tolist()
-        return pairs, splits
+    def compact_touched(self):
+        """(slot << 32 | value) pairs of the touched foreign slots, in slot
+        order (grouped by owner), and the per-owner counts (one host read).
+        Touched foreign slots never outnumber the edges just scattered."""
+        cap = max(min(self._scattered, self.npad), 1)
+        pairs = torch.empty(cap, dtype=torch.int64, device=self.device)
+        self._k(self.lib.pgx_touched(
+            self.npad, self.blo, self.blo + self.block, self.has.data_ptr(),
+            self.mailbox.data_ptr(), EXCHANGE_NEUTRAL, pairs.data_ptr(),
+            self.tcount.data_ptr(), self.tscratch.data_ptr(), self.stream.cuda_stream),
+            "pgx_touched", 3)
+        # per-owner counts of the valid prefix; the unused tail is binned
+        # past the last owner
+        idx = torch.arange(cap, device=self.device)
+        owner = torch.where(idx < self.tcount, (pairs >> 32) // self.block,
+                            torch.full_like(pairs, self.world))
+        counts = torch.bincount(owner, minlength=self.world + 1).tolist()
+        splits = counts[:self.world]
+        return pairs[:sum(splits)], splits
 
     def scatter_pairs(self, pairs):
-        self._lib.check(self.lib.pgx_scatter_pairs(pairs.data_ptr(), pairs.numel(),
-                                                   self.mailbox.data_ptr(),
-                                                   self.stream.cuda_stream), "pgx_scatter_pairs")
+        self._k(self.lib.pgx_scatter_pairs(pairs.data_ptr(), pairs.numel(),
+                                           self.mailbox.data_ptr(),
+                                           self.stream.cuda_stream), "pgx_scatter_pairs")
 
-    def scatter_min(self, dense: bool, id_offset: int, peer: bool = False):
+    def scatter_min(self, dense: bool, peer: bool = False):
         L, st = self.lib, self.stream.cuda_stream
         op = self._lib.PGX_OP_MIN_U32
+        if dense:
+            src = (self._g_nz_eb.data_ptr(), None, self._g_nz_id.data_ptr(), self.lo_own, None,
+                   self._g_tile.data_ptr(), self._nnz(), self.m_local)
+            self._scattered = self.m_local
+        else:
+            src = (self.f_eb.data_ptr(), self.f_rs.data_ptr(), None, 0,
+                   self.f_msg.data_ptr(), self.f_tile.data_ptr(), self.nsrc, self.E)
+            self._scattered = self.E
         if peer:
-            if dense:
-                src = (self._g_nz_eb.data_ptr(), None, self._g_nz_id.data_ptr(), id_offset, None,
-                       self._g_tile.data_ptr(), self._nnz(), self.m_local)
-            else:
-                src = (self.f_eb.data_ptr(), self.f_rs.data_ptr(), None, 0,
-                       self.f_msg.data_ptr(), self.f_tile.data_ptr(), self.nsrc, self.E)
             rc = L.pgx_scatter_peer(int(dense), self.col.data_ptr(), *src,
                                     self.mailbox.data_ptr(), self.has.data_ptr(),
                                     EXCHANGE_NEUTRAL, self._peer_ptrs.data_ptr(),
-                                    self._bounds32.data_ptr(), self._world, self.lo_own,
-                                    self.hi_own, st)
-            self._lib.check(rc, "pgx_scatter_peer")
+                                    self._pbounds.data_ptr(), self.world, self.blo,
+                                    self.blo + self.len, st)
+            self._k(rc, "pgx_scatter_peer")
             return
-        if dense:
-            nnz = self._nnz()
-            rc = L.pgx_scatter(op, 1, self.col.data_ptr(), self._g_nz_eb.data_ptr(), None,
-                               self._g_nz_id.data_ptr(), id_offset, None,
-                               self._g_tile.data_ptr(), nnz, self.m_local,
-                               self.mailbox.data_ptr(), self.has.data_ptr(),
-                               EXCHANGE_NEUTRAL, st)
-        else:
-            rc = L.pgx_scatter(op, 0, self.col.data_ptr(), self.f_eb.data_ptr(),
-                               self.f_rs.data_ptr(), None, 0, self.f_msg.data_ptr(),
-                               self.f_tile.data_ptr(), self.nsrc, self.E,
-                               self.mailbox.data_ptr(), self.has.data_ptr(),
-                               EXCHANGE_NEUTRAL, st)
-        self._lib.check(rc, "pgx_scatter")
+        rc = L.pgx_scatter(op, int(dense), self.col.data_ptr(), *src,
+                           self.mailbox.data_ptr(), self.has.data_ptr(), EXCHANGE_NEUTRAL, st)
+        self._k(rc, "pgx_scatter")
 
     def apply_min(self, app, count_only: bool) -> torch.Tensor:
-        """K2 on the owned slice; returns the raw device counter block
-        (decode_counts) -- no host synchronisation, no extra kernels."""
+        """K2 on the owned block; returns the raw device counter block
+        (decode_counts) -- no host synchronisation."""
         self.ctr.zero_()
         app_id = self._lib.PGX_APP_CC if app == "components" else self._lib.PGX_APP_SSSP
-        sl = self.mailbox[self.lo:self.lo + self.len]
-        self._lib.check(self.lib.pgx_apply_slice(
+        sl = self.mailbox[self.blo:self.blo + self.len]
+        self._k(self.lib.pgx_apply_slice(
             app_id, self.len, self.row_ptr.data_ptr(), self.val.data_ptr(), sl.data_ptr(),
             self.f_eb.data_ptr(), self.f_rs.data_ptr(), self.f_msg.data_ptr(),
             self.f_tile.data_ptr(), self.ctr.data_ptr(), int(count_only), EXCHANGE_NEUTRAL,
@@ -632,73 +683,170 @@ class CudaBackend:
         self.nsrc, self.E = int(senders), int(edges)
 
     # ---- PageRank ----
-    def init_pagerank(self, lo, hi, r0) -> int:
+    def _ensure_pull(self):
+        """The rank's local in-CSR (rows = padded positions, entries = local
+        sources in ascending order), its tile map and the rows that span
+        tiles -- built once per layout (graph preparation)."""
+        if self._pull is not None:
+            return self._pull
+        dev, st = self.device, self.stream
+        with torch.cuda.device(dev), torch.cuda.stream(st):
+            src = torch.repeat_interleave(
+                torch.arange(self.len, dtype=torch.int32, device=dev),
+                torch.diff(self.row_ptr).to(torch.int64))
+            dst = self.col
+            order = torch.sort(dst, stable=True).indices    # sources stay ascending
+            in_col = src[order].contiguous()
+            del src, order
+            in_deg = torch.bincount(dst.to(torch.int64), minlength=self.npad)
+            in_ptr64 = torch.zeros(self.npad + 1, dtype=torch.int64, device=dev)
+            in_ptr64[1:] = torch.cumsum(in_deg, 0)
+            in_ptr = in_ptr64.to(torch.int32)
+            m = self.m_local
+            ws_bytes = self._lib.out_size(self.lib.pgx_graph_workspace_bytes, self.npad, m)
+            ws = torch.empty(ws_bytes, dtype=torch.uint8, device=dev)
+            self._lib.check(self.lib.pgx_graph_prepare(self.npad, m, in_ptr.data_ptr(),
+                                                       ws.data_ptr(), ws_bytes, st.cuda_stream),
+                            "pgx_graph_prepare")
+            nz = in_deg > 0
+            a = in_ptr64[:-1] // 256
+            b = (in_ptr64[1:] - 1) // 256
+            rows = torch.nonzero(nz & (a != b)).flatten()
+            ntile = (m + 255) // 256 + 2
+            self._pull = {
+                "in_col": in_col, "in_ptr": in_ptr, "ws": ws, "nsrc": int(nz.sum()),
+                "span_rows": rows.to(torch.int32), "span_t0": a[rows].to(torch.int32),
+                "span_t1": b[rows].to(torch.int32),
+                "head": torch.zeros(ntile, dtype=torch.float64, device=dev),
+                "tail": torch.zeros(ntile, dtype=torch.float64, device=dev)}
+        return self._pull
+
+    def init_pagerank(self, r0) -> int:
         self.app = "pagerank"
-        self.lo = lo
-        self.mailbox = torch.zeros(self.n, dtype=torch.float64, device=self.device)
-        self.rank = torch.empty(max(self.len, 1), dtype=torch.float64, device=self.device)
+        self.mailbox = torch.zeros(self.npad, dtype=torch.float64, device=self.device)
+        self.rank_v = torch.empty(max(self.len, 1), dtype=torch.float64, device=self.device)
         self.share = torch.empty(max(self.len, 1), dtype=torch.float64, device=self.device)
-        self._lib.check(self.lib.pgx_slice_init(self._lib.PGX_APP_PAGERANK, self.len, lo,
-                                                self.rank.data_ptr(), self.row_ptr.data_ptr(),
-                                                self.share.data_ptr(), r0,
-                                                self.stream.cuda_stream), "pgx_slice_init")
+        self._k(self.lib.pgx_slice_init(self._lib.PGX_APP_PAGERANK, self.len, self.lo_own,
+                                        self.rank_v.data_ptr(), self.row_ptr.data_ptr(),
+                                        self.share.data_ptr(), r0,
+                                        self.stream.cuda_stream), "pgx_slice_init")
         self.partials = torch.zeros((self.len + 511) // 512 + 1, dtype=torch.float64,
                                     device=self.device)
+        if self.pr_mode == "pull" and self.m_local > 0:
+            self._ensure_pull()
         deg = torch.diff(self.row_ptr)
         return int((deg == 0).sum())
 
-    def scatter_sum(self):
-        nnz = self._nnz()
-        self._lib.check(self.lib.pgx_scatter(
-            self._lib.PGX_OP_SUM_F64, 1, self.col.data_ptr(), self._g_nz_eb.data_ptr(), None,
-            self._g_nz_id.data_ptr(), 0, self.share.data_ptr(), self._g_tile.data_ptr(), nnz,
-            self.m_local, self.mailbox.data_ptr(), None, 0, self.stream.cuda_stream),
-            "pgx_scatter")
+    def fold_sum(self):
+        """This rank's partial fold of every destination into the full-width
+        mailbox: the pull fold (K3) by default, the red.add.f64 scatter for
+        pr_mode="push"."""
+        st = self.stream.cuda_stream
+        self.mailbox.zero_()
+        if self.m_local == 0:
+            return
+        if self.pr_mode == "push":
+            self._k(self.lib.pgx_scatter(
+                self._lib.PGX_OP_SUM_F64, 1, self.col.data_ptr(), self._g_nz_eb.data_ptr(),
+                None, self._g_nz_id.data_ptr(), 0, self.share.data_ptr(),
+                self._g_tile.data_ptr(), self._nnz(), self.m_local, self.mailbox.data_ptr(),
+                None, 0, st), "pgx_scatter")
+            return
+        p = self._pull
+        self._k(self.lib.pgx_gather_slice(self.npad, self.m_local, p["in_col"].data_ptr(),
+                                          p["ws"].data_ptr(), p["nsrc"], self.share.data_ptr(),
+                                          self.mailbox.data_ptr(), p["head"].data_ptr(),
+                                          p["tail"].data_ptr(), st), "pgx_gather_slice")
+        ns = int(p["span_rows"].numel())
+        if ns:
+            self._k(self.lib.pgx_fold_spanning(ns, p["span_rows"].data_ptr(),
+                                               p["span_t0"].data_ptr(), p["span_t1"].data_ptr(),
+                                               p["head"].data_ptr(), p["tail"].data_ptr(),
+                                               self.mailbox.data_ptr(), st), "pgx_fold_spanning")
 
-    def apply_pagerank(self, base, damping, dn, last: bool) -> float:
-        sl = self.mailbox[self.lo:self.lo + self.len]
-        self._lib.check(self.lib.pgx_pr_apply_slice(
-            self.len, self.row_ptr.data_ptr(), self.rank.data_ptr(), sl.data_ptr(),
-            self.share.data_ptr(), base, damping, dn, int(last), self.partials.data_ptr(),
-            self.stream.cuda_stream), "pgx_pr_apply_slice")
-        return float(self.partials[:(self.len + 511) // 512].sum().item())
+    def apply_pagerank(self, base, damping, dangling: torch.Tensor, last: bool) -> torch.Tensor:
+        """Apply on the owned block; returns this rank's dangling mass as a
+        one-element device tensor (no host read)."""
+        sl = self.mailbox[self.blo:self.blo + self.len]
+        nb = (self.len + 511) // 512
+        self._k(self.lib.pgx_pr_apply_slice(
+            self.len, self.row_ptr.data_ptr(), self.rank_v.data_ptr(), sl.data_ptr(),
+            self.share.data_ptr(), base, damping, dangling.data_ptr(), float(self.n), int(last),
+            self.partials.data_ptr(), self.stream.cuda_stream), "pgx_pr_apply_slice")
+        return self.partials[:nb].sum().reshape(1)
 
     def values(self):
         if self.app == "pagerank":
-            return self.rank[:self.len]
+            return self.rank_v[:self.len]
         return self.val[:self.len]
+
+
+class PartitionedPlan:
+    """A partitioned run prepared on this rank (local CSR slice, tile map,
+    padded layout, peer mappings cached on the graph): ``launch()`` runs the
+    superstep loop with the result left on the device, ``collect()``
+    gathers it."""
+
+    def __init__(self, graph, program, low, config, dist):
+        rank, world = dist.get_rank(), dist.get_world_size()
+        self.n, self.m = graph.vertex_count, graph.edge_count
+        dev = torch.device("cuda", torch.cuda.current_device())
+        pr_mode = getattr(config, "pagerank_mode", "pull")
+        key = ("partitioned", world, rank, dev.index, pr_mode)
+        cached = graph._device.get(key)
+        if cached is None:  # local CSR slice + its tile map, built once per graph
+            deg = torch.diff(graph.out_offsets.cpu()).numpy()
+            bounds = partition_bounds(deg, world)
+            backend = CudaBackend(graph, int(bounds[rank]), int(bounds[rank + 1]), dev,
+                                  pr_mode=pr_mode)
+            cached = graph._device[key] = (bounds, backend)
+        self.bounds, self.backend = cached
+        self.runner = PartitionedRun(self.backend, dist, self.bounds, self.n, self.m)
+        self.runner.exchange = os.environ.get("PGX_EXCHANGE", "auto")
+        self.program, self.low, self.config = program, low, config
+        self.app = low["app"]
+        self.stream = self.backend.stream
+        self._out = None
+
+    def launch(self) -> None:
+        """Every superstep of one run (host-driven; values stay on the GPU)."""
+        if self.app == "pagerank":
+            self._out = self.runner.loop_pagerank(self.low["iterations"], self.low["damping"],
+                                                  self.config.max_supersteps)
+        else:
+            self._out = self.runner.loop_min(self.app, self.low.get("source", 0),
+                                             self.config.max_supersteps)
+
+    @property
+    def launches(self) -> int:
+        """libpgx kernels this rank has launched so far."""
+        return self.backend.launches
+
+    def collect(self):
+        from .engine import RunReport, SuperstepStats
+        stats, cap, wall = self._out
+        vals = self.runner._gather_values()
+        if self.app == "pagerank":
+            values = vals.cpu().numpy()
+        else:
+            v = vals.cpu().numpy().view(np.uint32)
+            values = v.astype(np.int64) if self.app == "components" else v
+        steps = [SuperstepStats(**{k: v for k, v in s.items() if k != "exchange"})
+                 for s in stats]
+        if self.program.extract is not None:
+            from types import SimpleNamespace
+            values = self.program.extract(SimpleNamespace(state=values,
+                                                          halted=np.ones(values.shape[0], bool)))
+        return RunReport(values, len(steps), steps, wall, cap, device_values=vals,
+                         exchanges=[s.get("exchange", "dense") for s in stats])
+
+
+def plan_partitioned(graph, program, low, config, dist) -> PartitionedPlan:
+    return PartitionedPlan(graph, program, low, config, dist)
 
 
 def run_partitioned(graph, program, low, config, dist):
     """engine.run() under torchrun: every rank calls run() with the graph."""
-    from .engine import RunReport, SuperstepStats
-    rank, world = dist.get_rank(), dist.get_world_size()
-    n, m = graph.vertex_count, graph.edge_count
-    dev = torch.device("cuda", torch.cuda.current_device())
-    key = ("partitioned", world, rank, dev.index)
-    cached = graph._device.get(key)
-    if cached is None:  # local CSR slice + its tile map, built once per graph
-        deg = torch.diff(graph.out_offsets.cpu()).numpy()
-        bounds = partition_bounds(deg, world)
-        backend = CudaBackend(graph, int(bounds[rank]), int(bounds[rank + 1]), dev)
-        cached = graph._device[key] = (bounds, backend)
-    bounds, backend = cached
-    runner = PartitionedRun(backend, dist, bounds, n, m)
-    runner.exchange = os.environ.get("PGX_EXCHANGE", "auto")
-    app = low["app"]
-    if app == "pagerank":
-        vals, stats, cap, wall = runner.run_pagerank(low["iterations"], low["damping"],
-                                                     config.max_supersteps)
-        values = vals.cpu().numpy()
-    else:
-        vals, stats, cap, wall = runner.run_min(app, low.get("source", 0),
-                                                config.max_supersteps)
-        v = vals.cpu().numpy().view(np.uint32)
-        values = v.astype(np.int64) if app == "components" else v
-    steps = [SuperstepStats(**{k: v for k, v in s.items() if k != "exchange"}) for s in stats]
-    if program.extract is not None:
-        from types import SimpleNamespace
-        values = program.extract(SimpleNamespace(state=values,
-                                                 halted=np.ones(values.shape[0], bool)))
-    return RunReport(values, len(steps), steps, wall, cap, device_values=vals,
-                     exchanges=[s.get("exchange", "dense") for s in stats])
+    plan = plan_partitioned(graph, program, low, config, dist)
+    plan.launch()
+    return plan.collect()

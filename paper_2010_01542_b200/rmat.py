@@ -22,6 +22,8 @@ CONFIGS = {
     "C3": (22, 16, 0.57, 0.19, 0.19, 3, False),
     "C4": (22, 28, 0.45, 0.22, 0.22, 4, False),
     "C5": (26, 14, 0.57, 0.19, 0.19, 5, True),
+    # test-only: C5's shape (symmetrised, a/b/c, edge factor, seed) at scale 16
+    "C5S": (16, 14, 0.57, 0.19, 0.19, 5, True),
 }
 
 

@@ -79,20 +79,23 @@ def test_load_edge_list(tmp_path):
         pgx.load_edge_list(p)
 
 
-def test_edge_balanced_partition_reference_examples():
-    # reference tests/test_scheduler.py:98-143
-    assert pgx.edge_balanced_partition(np.array([5, 1, 1, 1]), 2).boundaries.tolist() == [0, 1, 4]
-    assert pgx.edge_balanced_partition(np.empty(0, int), 4).boundaries.tolist() == [0] * 5
+def test_partition_bounds_balance():
+    """The multi-GPU owner ranges (distributed.partition_bounds): contiguous,
+    covering, each carrying < total / W + max work of out_degree + 1."""
+    from paper_2010_01542_b200.distributed import partition_bounds
+    assert partition_bounds(np.empty(0, int), 4).tolist() == [0] * 5
+    assert partition_bounds(np.array([5, 1, 1, 1]), 1).tolist() == [0, 4]
     rng = np.random.default_rng(1)
     for w in (2, 3, 8, 32):
         deg = rng.zipf(2.3, size=2000).clip(max=2000)
-        p = pgx.edge_balanced_partition(deg, w)
-        total, mx = int(deg.sum()), int(deg.max())
+        b = partition_bounds(deg, w)
+        assert b[0] == 0 and b[-1] == deg.size and np.all(np.diff(b) >= 0)
+        work = deg + 1
+        total, mx = int(work.sum()), int(work.max())
         for k in range(w):
-            lo, hi = p.block(k)
-            assert int(deg[lo:hi].sum()) * w < total + mx * w
-    with pytest.raises(pgx.ConfigError):
-        pgx.edge_balanced_partition(np.array([1]), 0)
+            assert int(work[b[k]:b[k + 1]].sum()) * w < total + mx * w
+    with pytest.raises(ValueError):
+        partition_bounds(np.array([1]), 0)
 
 
 def test_gather_adjacency_matches_slices():

@@ -24,20 +24,53 @@ SPECS = [O.RmatSpec(14, 8, .57, .19, .19, 31, True),
          O.RmatSpec(13, 16, .45, .22, .22, 32, False)]
 
 
-def _run(off, tgt, app, kw, world, exchange="auto"):
+def _run(off, tgt, app, kw, world, exchange="auto", pr_mode="pull", d=None):
     n = off.size - 1
     g = pgx.from_csr(torch.from_numpy(off).cuda(), torch.from_numpy(tgt).cuda())
     bounds = partition_bounds(np.diff(off), world)
 
     def rank_fn(r, d):
-        be = CudaBackend(g, int(bounds[r]), int(bounds[r + 1]), "cuda:0")
+        be = CudaBackend(g, int(bounds[r]), int(bounds[r + 1]), "cuda:0", pr_mode=pr_mode)
         run = PartitionedRun(be, d, bounds, n, int(tgt.size))
         run.exchange = exchange
         cap = kw.get("max_supersteps", 10_000)
         if app == "pagerank":
             return run.run_pagerank(10, 0.85, cap)
         return run.run_min(app, kw.get("source", 0), cap)
-    return run_ranks(world, rank_fn)[0]
+    return run_ranks(world, rank_fn, d)[0]
+
+
+@pytest.mark.parametrize("world", [2, 3])
+@pytest.mark.parametrize("pr_mode", ["pull", "push"])
+def test_partitioned_pagerank_modes(world, pr_mode):
+    """Partitioned PageRank on the pull fold (pgx_gather_slice +
+    pgx_fold_spanning, default) and on the red.add.f64 push arm: both
+    within 1e-9 of the oracle, through the equal-block reduce_scatter."""
+    from thread_dist import ThreadDist
+    for spec in SPECS:
+        n, off, tgt = O.rmat_csr(spec)
+        want = O.run_pagerank(n, off, tgt)
+        d = ThreadDist(world)
+        vals, stats, hit, _ = _run(off, tgt, "pagerank", {}, world, pr_mode=pr_mode, d=d)
+        v = vals.cpu().numpy()
+        assert np.max(np.abs(v - want.values) / np.abs(want.values)) <= 1e-9
+        assert [s["messages_sent"] for s in stats] == want.messages_sent
+        assert d.calls.get("reduce_scatter_tensor") == 10  # one per superstep
+
+
+def test_collectives_of_the_production_branch():
+    """The thread stand-in reports the NCCL backend, so the driver takes the
+    device-tensor branch: dense supersteps are one reduce_scatter_tensor,
+    sparse ones all_to_all_single."""
+    from thread_dist import ThreadDist
+    n, off, tgt = O.rmat_csr(SPECS[0])
+    d = ThreadDist(2)
+    vals, stats, hit, _ = _run(off, tgt, "components", {}, 2, exchange="hybrid", d=d)
+    ex = [s["exchange"] for s in stats]
+    assert d.calls.get("reduce_scatter_tensor") == ex.count("dense") > 0
+    assert d.calls.get("all_to_all_single") == 2 * ex.count("sparse") > 0
+    assert np.array_equal(vals.cpu().numpy().view(np.uint32).astype(np.int64),
+                          O.run_cc(n, off, tgt).values.astype(np.int64))
 
 
 @pytest.mark.parametrize("world", [1, 2, 4, 8])

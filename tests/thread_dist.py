@@ -20,6 +20,7 @@ class ThreadDist:
 
     def __init__(self, world: int):
         self.world = world
+        self.calls = {}  # collective name -> calls (rank 0), for the tests
         self._bar = threading.Barrier(world)
         self._slots = [None] * world
         self._tls = threading.local()
@@ -69,7 +70,43 @@ class ThreadDist:
         torch.cuda.synchronize() if tensor.is_cuda else None
         self._bar.wait()
 
+    def get_backend(self):
+        """The production branch of the driver (CUDA tensors, no host
+        staging): the collectives below take device tensors like NCCL's."""
+        return "nccl"
+
+    def _count(self, name):
+        if self.get_rank() == 0:
+            self.calls[name] = self.calls.get(name, 0) + 1
+
+    def reduce_scatter_tensor(self, out, inp, op=_d.ReduceOp.SUM):
+        """Equal blocks; `out` may alias this rank's block of `inp` (the
+        driver's in-place call): every rank reduces its block from every
+        input before anyone writes."""
+        self._count("reduce_scatter_tensor")
+        r = self.get_rank()
+        torch.cuda.synchronize() if inp.is_cuda else None
+        blk = out.numel()
+        assert inp.numel() == blk * self.world, "reduce_scatter_tensor: unequal blocks"
+        self._slots[r] = inp
+        self._bar.wait()
+        parts = [t[r * blk:(r + 1) * blk] for t in self._slots]
+        res = parts[0].clone()
+        for t in parts[1:]:
+            if op == _d.ReduceOp.MIN:
+                res = torch.minimum(res, t)
+            elif op == _d.ReduceOp.MAX:
+                res = torch.maximum(res, t)
+            else:
+                res = res + t
+        torch.cuda.synchronize() if inp.is_cuda else None
+        self._bar.wait()
+        out.copy_(res)
+        torch.cuda.synchronize() if out.is_cuda else None
+        self._bar.wait()
+
     def all_to_all_single(self, out, inp, out_splits=None, in_splits=None):
+        self._count("all_to_all_single")
         r = self.get_rank()
         torch.cuda.synchronize() if inp.is_cuda else None
         w = self.world
@@ -109,9 +146,9 @@ class ThreadDist:
         self._bar.wait()
 
 
-def run_ranks(world, fn):
+def run_ranks(world, fn, d=None):
     """Run fn(rank, dist) on `world` threads; returns the per-rank results."""
-    d = ThreadDist(world)
+    d = ThreadDist(world) if d is None else d
     out = [None] * world
     err = []
 

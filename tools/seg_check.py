@@ -46,6 +46,6 @@ for c in cfgs:
             [(s.active_count, s.messages_sent, s.edges, s.recipients) for s in rep.supersteps] == \
             [(s.active_count, s.messages_sent, s.edges, s.recipients) for s in base.supersteps]
         print(f"{c} {k}: identical to K1 = {bool(same)}", flush=True)
-    _lib.set_option(_lib.PGX_OPT_SEG_MIN_EDGES, 512)
+    _lib.set_option(_lib.PGX_OPT_SEG_MIN_EDGES, 256)
     del g
     torch.cuda.empty_cache()
