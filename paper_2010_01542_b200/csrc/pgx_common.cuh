@@ -181,7 +181,9 @@ __device__ __forceinline__ void grid_sync(GridBarrier *bar, unsigned &gen) {
       const unsigned target = (gen + 1) * gridDim.x;
       asm volatile("red.release.gpu.global.add.u32 [%0], %1;" ::"l"(&bar->count), "r"(1u)
                    : "memory");
-      while (ld_acquire(&bar->count) < target) {
+      // wrap-safe: the counter is monotonic within a launch and may pass
+      // 2^32 on very long runs; compare the signed distance
+      while ((int)(ld_acquire(&bar->count) - target) < 0) {
       }
     } else {
       const unsigned arrived = atomicAdd(&bar->count, 1u);

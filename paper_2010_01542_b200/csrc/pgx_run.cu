@@ -123,24 +123,35 @@ __global__ void __launch_bounds__(kBlock, PGX_MIN_BLOCKS) min_run_kernel(MinRunP
   // the host launches the BFS instantiation only for the default options
   constexpr bool bfs = BFS && APP == PGX_APP_SSSP && S == 0;
   if (gtid == 0) p.stats[PGX_STAT_HDR + 7] = (int64_t)globaltimer();
+  unsigned sv_stale = 0u;  // bit b: sv[b] may hold stale senders (grid-uniform)
 
   for (int s = 0;; s++) {
     // ---- scatter(s): senders push along out-edges into the mailbox ----
     const unsigned long long packed_s = p.ws.ctr[s].packed;
     const int64_t edges_s = (APP == PGX_APP_CC && s == 0) ? p.m
                                                           : (int64_t)(packed_s & 0xFFFFFFFFull);
+    // a segmented superstep needs exact send values: after a K1 superstep
+    // left them stale (below), K1 runs instead (never on C2 / C5, whose
+    // dense supersteps come first)
+    const bool seg_s = p.use_seg && edges_s >= p.seg_min_edges && edges_s > 0 &&
+                       !((sv_stale >> (s & 1)) & 1u);
     if (p.use_seg) {
       // senders bitmap (and CC send values) of superstep s + 1, written by
       // the next apply: they still hold the senders of s - 1 (last read by
-      // scatter(s - 1)); clear them unless that superstep had no senders
+      // scatter(s - 1)); clear them unless that superstep had no senders.
+      // The send values are cleared only under a segmented superstep (the
+      // stores hide behind its streaming); otherwise the buffer is marked
+      // stale and the superstep that would read it runs K1
       if (s >= 1 && (p.ws.ctr[s - 1].packed >> 32) != 0ull) {
         uint32_t *nx = p.ws.snd[(s + 1) & 1];
+        const bool clear_sv = use_sv && seg_s;
         uint32_t *svx = use_sv ? p.ws.sv[(s + 1) & 1] : nullptr;
+        if (use_sv && !clear_sv) sv_stale |= 1u << ((s + 1) & 1);
         for (unsigned wi = gtid; wi < (unsigned)(p.n / 32 + 2); wi += nthreads) {
           uint32_t w = nx[wi];
           if (!w) continue;
           nx[wi] = 0u;
-          if (use_sv) {
+          if (clear_sv) {
             while (w) {
               const int b = __ffs(w) - 1;
               w &= w - 1;
@@ -150,7 +161,7 @@ __global__ void __launch_bounds__(kBlock, PGX_MIN_BLOCKS) min_run_kernel(MinRunP
         }
       }
     }
-    if (p.use_seg && edges_s >= p.seg_min_edges && edges_s > 0) {
+    if (seg_s) {
       // dense superstep: the segmented shared-memory scatter (pgx_seg.cuh)
       SegPass sp;
       sp.ix = p.seg;

@@ -316,6 +316,10 @@ def plan_run(graph: Graph, program: VertexProgram,
     pull = app == "pagerank" and config.pagerank_mode == "pull"
     if app == "pagerank":
         max_steps = min(max_steps, int(low["iterations"]))
+    else:
+        # CC / SSSP quiesce within n + 1 supersteps, so a larger cap is never
+        # reached: size the per-superstep buffers for n + 2 at most
+        max_steps = min(max_steps, n + 2)
     if pull:
         csr.ensure_transpose(stream)
     hubs = app != "pagerank" and (config.hub_cache == "on" or

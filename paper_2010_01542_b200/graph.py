@@ -391,9 +391,17 @@ def from_csr(offsets, targets, vertex_count: int | None = None) -> Graph:
     tgt = targets if isinstance(targets, torch.Tensor) else \
         torch.as_tensor(np.asarray(targets))
     n = off.numel() - 1 if vertex_count is None else int(vertex_count)
-    if off.numel() != n + 1:
+    if off.numel() != n + 1 or n < 0:
         raise GraphLoadError("offsets must have vertex_count + 1 entries")
-    return Graph(n, off, tgt.reshape(-1).contiguous())
+    tgt = tgt.reshape(-1).contiguous()
+    m = tgt.numel()
+    # the checks load_cache runs (graph.py:325-373): the kernels index the
+    # mailbox with these values unchecked
+    if int(off[0]) != 0 or int(off[-1]) != m or bool((torch.diff(off) < 0).any()):
+        raise GraphLoadError("offsets must start at 0, end at len(targets) and never decrease")
+    if m and (int(tgt.min()) < 0 or int(tgt.max()) >= n):
+        raise GraphLoadError(f"target id out of range [0, {n})")
+    return Graph(n, off, tgt)
 
 
 def gather_adjacency(offsets, targets, ids):

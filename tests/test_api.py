@@ -207,3 +207,16 @@ def test_load_cache_rejects_short_and_odd_files(tmp_path):
         p.write_bytes(data)
         with pytest.raises(pgx.GraphLoadError, match=msg):
             pgx.load_cache(p)
+
+
+@pytest.mark.parametrize("off,tgt", [([1, 2], [0, 0]), ([0, 3], [0, 0]), ([0, 2, 1], [0, 1]),
+                                     ([0, 1], [5]), ([0, 1], [-1])])
+def test_from_csr_rejects_malformed_input(off, tgt):
+    with pytest.raises(pgx.GraphLoadError):
+        pgx.from_csr(np.array(off), np.array(tgt, dtype=np.int32))
+
+
+def test_huge_superstep_cap_is_cheap():
+    """A cap used to mean 'unbounded' must not size device buffers by it."""
+    from paper_2010_01542_b200.engine import _validate
+    _validate(pgx.connected_components(), pgx.EngineConfig(max_supersteps=2 ** 31 - 2))

@@ -21,6 +21,7 @@ import pytest
 import torch
 
 import paper_2010_01542_b200 as pgx
+from paper_2010_01542_b200 import _lib
 from golden_cases import DANGLING_RANKS, PATH3_RANKS, load_runs
 from oracle import oracle as O
 from paper_2010_01542_b200.rmat import rmat_graph
@@ -51,16 +52,19 @@ def rel_err(got, want):
 
 @pytest.fixture
 def seg_threshold():
-    """Set PGX_OPT_SEG_MIN_EDGES for one test, restore the shipped value."""
-    from paper_2010_01542_b200 import _lib
-    yield lambda v: _lib.set_option(_lib.PGX_OPT_SEG_MIN_EDGES, v)
-    _lib.set_option(_lib.PGX_OPT_SEG_MIN_EDGES, 512)
+    """Set PGX_OPT_SEG_MIN_EDGES (and optionally the gate / fused-apply
+    knobs) for one test, restore the shipped values."""
+    def set_(v):
+        _lib.set_option(_lib.PGX_OPT_SEG_MIN_EDGES, v)
+    yield set_
+    set_(256)
 
 
 # modes: pull / push (PageRank lowering, min programs with the shipped
 # segment policy: device graphs get the segmented scatter for supersteps
 # with >= m/4 sender edges), hubs (hub-cache arm), k1 (segments off: K1 in
-# every superstep), segall (the segmented scatter in every superstep)
+# every superstep), segall (the segmented scatter whenever its send values
+# are exact: every superstep until the first K1 one)
 @pytest.mark.parametrize("mode", ["pull", "push", "hubs", "k1", "segall"])
 @pytest.mark.parametrize("r", RUNS, ids=lambda r: r.id)
 def test_golden_reference_runs(r, mode, seg_threshold):
@@ -74,8 +78,8 @@ def test_golden_reference_runs(r, mode, seg_threshold):
                            pagerank_mode="push" if mode == "push" else "pull",
                            hub_cache="on" if mode == "hubs" else "off",
                            segments="off" if mode == "k1" else
-                           "on" if mode == "segall" else "auto")
-    if mode == "segall":
+                           "on" if mode.startswith("seg") else "auto")
+    if mode.startswith("seg"):
         seg_threshold(0)
     rep = pgx.run(g, program(r.app, r.kwargs), cfg)
     if r.app == "pagerank":
@@ -278,3 +282,16 @@ def test_load_cache_pinned_and_on_device(tmp_path):
                           "reference_cache_edgelist_idmap_u.pglcsr")
     d = pgx.load_cache(golden, device="cuda")
     assert d.id_map is not None and d.out_targets.is_cuda
+
+
+@pytest.mark.gpu
+def test_unbounded_cap_sizes_buffers_by_n():
+    """a cap of 2^31 - 2 ('unbounded') must not allocate per-cap
+    statistics; CC / SSSP quiesce within n + 1 supersteps."""
+    g = pgx.from_edges(np.arange(63), np.arange(1, 64), 64, undirected=True, device="cuda")
+    cfg = pgx.EngineConfig(max_supersteps=2 ** 31 - 2)
+    plan = pgx.plan_run(g, pgx.sssp(0), cfg)
+    assert plan.stats.numel() <= _lib.PGX_STAT_HDR + _lib.PGX_STAT_FIELDS * (64 + 2)
+    r = pgx.run(g, pgx.sssp(0), cfg)
+    assert r.superstep_count == 65 and not r.hit_superstep_cap
+    assert r.values.tolist() == list(range(64))
