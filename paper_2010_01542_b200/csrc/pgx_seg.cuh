@@ -78,6 +78,16 @@ struct SegPass {
   bool write_mailbox;   // false: the has-bitmask is the whole result (unit SSSP)
 };
 
+// Shared-memory slot of segment offset `loc`: the bank bits (low 5) are
+// XORed with a hash of the rest.  R-MAT offsets are skewed towards zero
+// bits (P(bit = 0) = a + c = 0.76), so a quarter of a round's lanes would
+// share bank 0 -- 7.5-way conflicts measured on C5 (ncu, superstep 0).  A
+// bijection within each 32-slot row: a warp's flush of 32 consecutive
+// slots still reads one row, conflict-free.
+__device__ __forceinline__ int seg_swz(int loc) {
+  return loc ^ (int)(((uint32_t)(loc >> 5) * 0x9E3779B1u) >> 27);
+}
+
 // per-warp window: the messages of the tile's entries [kSegMsgSlots], the
 // tile's flagged 16-bit destinations [kTile]; 16-byte aligned (cp.async 16)
 constexpr int kSegMsgSlots = (kSlots + 3) & ~3;
@@ -197,7 +207,7 @@ __device__ void seg_scatter_phase(const SegPass &a, char *smem_raw) {
         if (el >= ea && el < ez) {
           PGX_ASSERT(sidx >= 0 && sidx < k);
           const uint32_t msg = w_msg[sidx];
-          const int loc = (int)(c & lmask);
+          const int loc = seg_swz((int)(c & lmask));
           // shared-memory read-filter (the mailbox.py:159 short-circuit),
           // then the combine; both on the SM, no L2 request
           if (msg < s_mb[loc]) atomicMin(s_mb + loc, msg);
@@ -210,7 +220,7 @@ __device__ void seg_scatter_phase(const SegPass &a, char *smem_raw) {
     const int base = seg << L;
 #pragma unroll 4
     for (int i = threadIdx.x; i < S; i += blockDim.x) {
-      const uint32_t v = s_mb[i];
+      const uint32_t v = s_mb[seg_swz(i)];
       const int g = base + i;
       const bool in = g < a.n;
       const bool touched = v != kNeutralMin && in;
