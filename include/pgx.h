@@ -131,15 +131,16 @@ typedef struct PgxSegIndex {
   int32_t reserved;
   const int32_t *ent_src;   /* [nent]   source of each entry               */
   const int32_t *ent_eb;    /* [nent+1] first edge (segment order); [nent] = m */
-  const uint16_t *col16;    /* [m+256]  destination - segment base; bit 15
-                               flags the first edge of an entry            */
+  const uint16_t *col16;    /* [m+256]  shared-memory slot of (destination -
+                               segment base), bank-swizzled; bit 15 flags
+                               the first edge of an entry                  */
   const int32_t *tile_ent;  /* [ceil(m/256)+1] entry holding edge 256 t    */
   const int32_t *items;     /* [nitems][4] {segment, e0, e1, owns segment},
                                16-byte aligned, largest first              */
 } PgxSegIndex;
 
-/* default segment size (8192 vertices: a 32 KB shared-memory mailbox) */
-#define PGX_SEG_LOG2_DEFAULT 13
+/* default segment size (16384 vertices: a 64 KB shared-memory mailbox) */
+#define PGX_SEG_LOG2_DEFAULT 14
 
 /* workspace bytes of pgx_seg_count / pgx_seg_build (nent < 0: the count
  * step only) and the capacity the items array needs (host outs) */

@@ -112,9 +112,11 @@ __global__ void seg_copy_kernel(int64_t nent, const int32_t *perm, const int32_t
     const int r = perm[i];
     const int32_t s = run_pos[r];
     const int32_t d0 = ent_eb[i], d1 = ent_eb[i + 1];
-    // bit 15: the entry's first edge (the scatter's entry boundaries)
+    // bit 15: the entry's first edge (the scatter's entry boundaries); the
+    // offset is stored as its swizzled shared-memory slot (seg_swz)
     for (int32_t j = 0; j < d1 - d0; j++)
-      col16[d0 + j] = (uint16_t)(((uint32_t)col[s + j] & mask) | (j == 0 ? kSegEntryFlag : 0u));
+      col16[d0 + j] = (uint16_t)((uint32_t)seg_swz((int)((uint32_t)col[s + j] & mask)) |
+                                 (j == 0 ? kSegEntryFlag : 0u));
     for (int64_t t = ((int64_t)d0 + kTile - 1) / kTile; t * kTile < d1; t++) tile_ent[t] = (int32_t)i;
   }
 }

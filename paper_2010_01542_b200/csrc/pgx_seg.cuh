@@ -32,6 +32,8 @@
 // mailbox + has-bitmask, so K2 (apply) runs unchanged.
 #pragma once
 
+#include <type_traits>
+
 #include "pgx_common.cuh"
 
 namespace pgx {
@@ -197,22 +199,27 @@ __device__ void seg_scatter_phase(const SegPass &a, char *smem_raw) {
       // entry of edge e (tile-relative) = flags in [0, e] - flag(0): the
       // tile's first edge belongs to entry i0 whether or not it starts it
       int cur = -(int)(w_col[0] >> 15);
+      // the destinations are stored pre-swizzled (seg_swz, pgx_seg_build)
+      auto rounds = [&](auto checked) {
 #pragma unroll
-      for (int r = 0; r < kItems; r++) {
-        const int el = r * 32 + lane;
-        const uint32_t c = w_col[el];
-        const unsigned bm = __ballot_sync(0xFFFFFFFFu, (c & kSegEntryFlag) != 0u);
-        const int sidx = cur + __popc(bm & upto);
-        cur += __popc(bm);
-        if (el >= ea && el < ez) {
-          PGX_ASSERT(sidx >= 0 && sidx < k);
-          const uint32_t msg = w_msg[sidx];
-          const int loc = seg_swz((int)(c & lmask));
-          // shared-memory read-filter (the mailbox.py:159 short-circuit),
-          // then the combine; both on the SM, no L2 request
-          if (msg < s_mb[loc]) atomicMin(s_mb + loc, msg);
+        for (int r = 0; r < kItems; r++) {
+          const int el = r * 32 + lane;
+          const uint32_t c = w_col[el];
+          const unsigned bm = __ballot_sync(0xFFFFFFFFu, (c & kSegEntryFlag) != 0u);
+          const int sidx = cur + __popc(bm & upto);
+          cur += __popc(bm);
+          if (!decltype(checked)::value || (el >= ea && el < ez)) {
+            PGX_ASSERT(sidx >= 0 && sidx < k);
+            const uint32_t msg = w_msg[sidx];
+            const int loc = (int)(c & lmask);
+            // shared-memory read-filter (the mailbox.py:159 short-circuit),
+            // then the combine; both on the SM, no L2 request
+            if (msg < s_mb[loc]) atomicMin(s_mb + loc, msg);
+          }
         }
-      }
+      };
+      if (ea == 0 && ez == kTile) rounds(std::false_type{});  // interior tile
+      else rounds(std::true_type{});
       t = tn;
     }
     __syncthreads();
