@@ -129,7 +129,8 @@ typedef struct PgxSegIndex {
   int32_t nent;             /* entries                                     */
   int32_t nitems;           /* work items                                  */
   int32_t reserved;
-  const int32_t *ent_src;   /* [nent]   source of each entry               */
+  const int32_t *ent_src;   /* [nent+4] source of each entry (16-byte
+                               aligned; 4 slots of padding)                */
   const int32_t *ent_eb;    /* [nent+1] first edge (segment order); [nent] = m */
   const uint16_t *col16;    /* [m+256]  shared-memory slot of (destination -
                                segment base), bank-swizzled; bit 15 flags

@@ -270,8 +270,9 @@ int pgx_seg_build(int32_t n, int64_t m, const int32_t *row_ptr, const int32_t *c
   if (!ws || !ent_src || !ent_eb || !col16 || !tile_ent || !items || !nitems)
     return fail(PGX_EINVAL, "null segmented-index output");
   if (nent < 1 || nent > m) return fail(PGX_EINVAL, "entry count out of range");
-  if (reinterpret_cast<uintptr_t>(items) % 16 || reinterpret_cast<uintptr_t>(col16) % 16)
-    return fail(PGX_EINVAL, "items and col16 must be 16-byte aligned");
+  if (reinterpret_cast<uintptr_t>(items) % 16 || reinterpret_cast<uintptr_t>(col16) % 16 ||
+      reinterpret_cast<uintptr_t>(ent_src) % 16)
+    return fail(PGX_EINVAL, "items, col16 and ent_src must be 16-byte aligned");
   const int L = seg_log2;
   cudaStream_t st = (cudaStream_t)stream;
   SegWs w;

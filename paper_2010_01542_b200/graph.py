@@ -93,7 +93,8 @@ class DeviceCSR:
                              dtype=torch.uint8, device=dev)
             cap = ctypes.c_int32(0)
             _lib.check(lib.pgx_seg_max_items(n, m, L, ctypes.byref(cap)), "pgx_seg_max_items")
-            ent_src = torch.empty(ne, dtype=torch.int32, device=dev)
+            # + 4: the scatter stages entries in 16-byte chunks
+            ent_src = torch.zeros(ne + 4, dtype=torch.int32, device=dev)
             ent_eb = torch.empty(ne + 1, dtype=torch.int32, device=dev)
             col16 = torch.empty(m + 256, dtype=torch.int16, device=dev)
             tile_ent = torch.empty((m + 255) // 256 + 1, dtype=torch.int32, device=dev)

@@ -1,0 +1,5 @@
+set -x
+timeout 900 python tools/seg_check.py C2,C5 off shipped > gpurun_out/r2n_seg.log 2>&1; echo "seg rc=$?"
+timeout 900 python tools/seg_check.py C3 off shipped min=128 > gpurun_out/r2n_seg3.log 2>&1; echo "seg3 rc=$?"
+timeout 1500 python -m pytest tests/test_gpu.py -x -q -p no:cacheprovider > gpurun_out/r2n_pytest.log 2>&1; echo "pytest rc=$?"
+tail -2 gpurun_out/r2n_pytest.log
