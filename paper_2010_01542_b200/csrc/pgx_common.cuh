@@ -310,8 +310,8 @@ inline size_t run_ws_layout(int app, int64_t n, int64_t m, int32_t max_steps, Ru
     w.snd[0] = (uint32_t *)take(sizeof(uint32_t) * (size_t)(n / 32 + 2));
     w.snd[1] = (uint32_t *)take(sizeof(uint32_t) * (size_t)(n / 32 + 2));
     if (app == PGX_APP_CC) {
-      w.sv[0] = (uint32_t *)take(sizeof(uint32_t) * (size_t)(n + 1));
-      w.sv[1] = (uint32_t *)take(sizeof(uint32_t) * (size_t)(n + 1));
+      w.sv[0] = (uint32_t *)take(sizeof(uint32_t) * (size_t)(n + 4));  // whole uint4 stores
+      w.sv[1] = (uint32_t *)take(sizeof(uint32_t) * (size_t)(n + 4));
     }
   } else {
     w.f_eb = w.f_rs = w.tile_src = nullptr;

@@ -135,30 +135,27 @@ __global__ void __launch_bounds__(kBlock, PGX_MIN_BLOCKS) min_run_kernel(MinRunP
     // dense supersteps come first)
     const bool seg_s = p.use_seg && edges_s >= p.seg_min_edges && edges_s > 0 &&
                        !((sv_stale >> (s & 1)) & 1u);
-    if (p.use_seg) {
-      // senders bitmap (and CC send values) of superstep s + 1, written by
-      // the next apply: they still hold the senders of s - 1 (last read by
-      // scatter(s - 1)); clear them unless that superstep had no senders.
-      // The send values are cleared only under a segmented superstep (the
-      // stores hide behind its streaming); otherwise the buffer is marked
-      // stale and the superstep that would read it runs K1
-      if (s >= 1 && (p.ws.ctr[s - 1].packed >> 32) != 0ull) {
-        uint32_t *nx = p.ws.snd[(s + 1) & 1];
-        const bool clear_sv = use_sv && seg_s;
-        uint32_t *svx = use_sv ? p.ws.sv[(s + 1) & 1] : nullptr;
-        if (use_sv && !clear_sv) sv_stale |= 1u << ((s + 1) & 1);
-        for (unsigned wi = gtid; wi < (unsigned)(p.n / 32 + 2); wi += nthreads) {
-          uint32_t w = nx[wi];
-          if (!w) continue;
-          nx[wi] = 0u;
-          if (clear_sv) {
-            while (w) {
-              const int b = __ffs(w) - 1;
-              w &= w - 1;
-              svx[(wi << 5) + b] = kNeutralMin;
-            }
-          }
+    if (p.use_seg && s >= 1 && (p.ws.ctr[s - 1].packed >> 32) != 0ull) {
+      // the send buffers of superstep s + 1, written by the next apply,
+      // still hold the senders of s - 1 (last read by scatter(s - 1))
+      if (use_sv) {
+        // CC send values: cleared whole (a streaming store of n words)
+        // under a segmented superstep, which hides it; otherwise the
+        // buffer is marked stale and the superstep that would read it runs
+        // K1 (never on C2 / C5, whose dense supersteps come first)
+        if (seg_s) {
+          uint4 *svx = reinterpret_cast<uint4 *>(p.ws.sv[(s + 1) & 1]);
+          const uint4 nn = make_uint4(kNeutralMin, kNeutralMin, kNeutralMin, kNeutralMin);
+          for (unsigned i = gtid; i < (unsigned)((p.n + 4) / 4); i += nthreads) svx[i] = nn;
+          sv_stale &= ~(1u << ((s + 1) & 1));
+        } else {
+          sv_stale |= 1u << ((s + 1) & 1);
         }
+      } else {
+        // unit-weight SSSP senders bitmap: clear the set words
+        uint32_t *nx = p.ws.snd[(s + 1) & 1];
+        for (unsigned wi = gtid; wi < (unsigned)(p.n / 32 + 2); wi += nthreads)
+          if (nx[wi]) nx[wi] = 0u;
       }
     }
     if (seg_s) {
@@ -230,7 +227,9 @@ __global__ void __launch_bounds__(kBlock, PGX_MIN_BLOCKS) min_run_kernel(MinRunP
     // ---- apply(s+1): consume + compute + frontier build; at the cap the
     //      pending messages are only counted (engine.py:299-300) ----
     const bool at_cap = (s + 1 == p.max_steps);
-    uint32_t *snd_out = p.use_seg ? p.ws.snd[(s + 1) & 1] : nullptr;
+    // senders bitmap for the unit-weight SSSP segmented pass; CC sends from
+    // its send values alone
+    uint32_t *snd_out = (p.use_seg && !use_sv) ? p.ws.snd[(s + 1) & 1] : nullptr;
     uint32_t *sv_out = use_sv ? p.ws.sv[(s + 1) & 1] : nullptr;
     const unsigned long long rb =
         bfs ? apply_min_phase<APP, 0, true>(p.row_ptr, val, mailbox, p.n, p.ws, &p.ws.ctr[s + 1],
