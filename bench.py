@@ -99,7 +99,19 @@ def step_views(app, rep):
     return out
 
 
-def superstep_aggregate(app, n, m, rep, peak):
+def scatter_split(plan, rep):
+    """Per-superstep scatter time (us) of the persistent kernel: the
+    %globaltimer stamps at the scatter's start (field 7) and at the barrier
+    ending it (field 5); the rest of the superstep is the apply."""
+    import paper_2010_01542_b200 as pgx  # noqa: F401
+    from paper_2010_01542_b200 import _lib
+    k = rep.superstep_count
+    st = plan.stats[_lib.PGX_STAT_HDR:_lib.PGX_STAT_HDR + k * _lib.PGX_STAT_FIELDS]
+    st = st.view(k, _lib.PGX_STAT_FIELDS).cpu().numpy()
+    return [round(max(int(r[5]) - int(r[7]), 0) * 1e-3, 1) for r in st]
+
+
+def superstep_aggregate(app, n, m, rep, peak, scatter_us=None):
     """SURVEY 8(d)'s first figure: sum_s B_s / sum_s t_s, t_s the device time
     of superstep s (%globaltimer stamps of the persistent kernel; host
     clock per superstep of the partitioned loop), next to the loop figure
@@ -109,10 +121,13 @@ def superstep_aggregate(app, n, m, rep, peak):
     gbs = sum(b) / sum(t) / 1e9 if sum(t) > 0 else 0.0
     return {"achieved": round(gbs, 1), "unit": "GB/s", "peak": peak,
             "frac": round(gbs / peak, 4),
-            "per_superstep": [{"s": i, "edges": st.edges, "senders": st.senders,
-                               "recipients": st.recipients, "us": round(ts * 1e6, 1),
-                               "alg_bytes": bs,
-                               "GBps": round(bs / ts / 1e9, 1) if ts > 0 else None}
+            "per_superstep": [dict({"s": i, "edges": st.edges, "senders": st.senders,
+                                    "recipients": st.recipients, "us": round(ts * 1e6, 1),
+                                    "alg_bytes": bs,
+                                    "GBps": round(bs / ts / 1e9, 1) if ts > 0 else None},
+                                   **({"scatter_us": scatter_us[i],
+                                       "apply_us": round(ts * 1e6 - scatter_us[i], 1)}
+                                      if scatter_us else {}))
                               for i, (st, ts, bs) in enumerate(zip(rep.supersteps, t, b))]}
 
 
@@ -377,6 +392,7 @@ def bench_pgx(args):
     with ClockSampler(d.local) as clocks:
         kernel_ms, total_ms, launches = time_steps(plan, d, args.steps, args.warmup, flush)
     rep = plan.collect() if d.world > 1 else pgx.collect(plan, prog)
+    split = scatter_split(plan, rep) if d.world == 1 else None
     edges = sum(s.edges for s in rep.supersteps)
     value = edges * args.steps / (total_ms * 1e-3) / 1e9
     ms_per_step = total_ms / args.steps
@@ -464,7 +480,7 @@ def bench_pgx(args):
                      "alg_bytes_per_step": alg_bytes,
                      "kernel": "min_run_kernel / pagerank_pull_kernel (persistent)"
                      if d.world == 1 else "pgx_scatter / pgx_apply_slice (partitioned)"},
-        "superstep_aggregate": superstep_aggregate(app, n, m, rep, agg_peak),
+        "superstep_aggregate": superstep_aggregate(app, n, m, rep, agg_peak, split),
         "scattered_roofline": {
             "bound": "random 4/8-byte L2 accesses (>= 1 per edge for K1; per entry segmented)",
             "achieved": round(value / d.world, 2), "peak": ceiling, "unit": "G edges/s per GPU",

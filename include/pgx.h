@@ -81,7 +81,10 @@ const char *pgx_last_error(void);
 #define PGX_OPT_LAYOUT 4        /* ablation: PGX_LAYOUT_* of the CC/SSSP vertex state */
 #define PGX_OPT_SEG_MIN_EDGES 5 /* segmented scatter when a superstep's senders hold at least
                                    m * value / 1024 edges (0 = every superstep, 1025 = never; default 256) */
-#define PGX_OPT_COUNT 6
+#define PGX_OPT_SEG_PREDICT 6   /* CC: the apply builds no frontier when the next superstep is
+                                   predicted segmented, which then runs segmented (0 never,
+                                   1 predicted -- default, 2 after every segmented superstep) */
+#define PGX_OPT_COUNT 7
 
 /* PGX_OPT_LAYOUT values (LayoutMode, layout.py:31-33).  EXTERNALISED is the
  * default SoA (value[], mailbox[] apart).  INTERLEAVED keeps one {mailbox,

@@ -24,6 +24,7 @@ PGX_STAT_HDR, PGX_STAT_FIELDS = 4, 8
 PGX_OPT_READ_FILTER, PGX_OPT_CTAS_PER_SM, PGX_OPT_CAS_LOOP, PGX_OPT_VERTEX_SCHED = 0, 1, 2, 3
 PGX_OPT_LAYOUT = 4
 PGX_OPT_SEG_MIN_EDGES = 5
+PGX_OPT_SEG_PREDICT = 6
 PGX_SEG_LOG2_DEFAULT = 14
 PGX_IPC_HANDLE_BYTES = 64
 PGX_LAYOUT_EXTERNALISED, PGX_LAYOUT_INTERLEAVED = 0, 1

@@ -70,7 +70,8 @@ __device__ unsigned long long apply_min_phase(const int32_t *__restrict__ row_pt
                                               uint32_t *mailbox, int32_t n, const RunWs &ws,
                                               StepCounters *ctr, char *smem, bool count_only,
                                               uint32_t bfs_msg = 0, uint32_t *snd = nullptr,
-                                              uint32_t *sv = nullptr) {
+                                              uint32_t *sv = nullptr,
+                                              bool no_frontier = false) {
   __shared__ unsigned long long s_w[33];
   __shared__ unsigned long long s_gbase;
   int32_t *s_list = reinterpret_cast<int32_t *>(smem);  // kListCap vertex ids
@@ -184,6 +185,16 @@ __device__ unsigned long long apply_min_phase(const int32_t *__restrict__ row_pt
 #endif
         unsigned long long total;
         unsigned long long run = block_excl_scan_u64(mine, s_w, &total);
+        if (no_frontier) {
+          // CC, next superstep predicted segmented: it reads the send
+          // values, not a frontier -- only count (senders << 32 | edges),
+          // no frontier SoA / tile map stores
+          if (threadIdx.x == 0 && total) atomicAdd(&ctr->packed, total);
+#pragma unroll
+          for (int j = 0; j < kApplyItems; j++)
+            if (deg[j] > 0) sv[v[j]] = m[j];
+          continue;
+        }
         if (total != 0) {  // block-uniform
           if (threadIdx.x == 0) s_gbase = atomicAdd(&ctr->packed, total);
           __syncthreads();

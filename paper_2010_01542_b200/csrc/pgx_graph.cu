@@ -15,6 +15,7 @@ int g_opt[PGX_OPT_COUNT] = {
     /* PGX_OPT_VERTEX_SCHED */ 0,  // ablation: one thread per sender
     /* PGX_OPT_LAYOUT */ PGX_LAYOUT_EXTERNALISED,
     /* PGX_OPT_SEG_MIN_EDGES */ 256,  // segmented scatter from m/4 sender edges
+    /* PGX_OPT_SEG_PREDICT */ 1,      // skip the frontier before predicted segmented supersteps
 };
 
 namespace {

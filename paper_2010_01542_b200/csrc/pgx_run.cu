@@ -63,6 +63,7 @@ struct MinRunParams {
   PgxSegIndex seg;
   int32_t use_seg;
   int64_t seg_min_edges;
+  int32_t seg_predict;  // PGX_OPT_SEG_PREDICT
 };
 
 // S = 0: externalised SoA (value = the caller's output array); S = 1:
@@ -124,6 +125,8 @@ __global__ void __launch_bounds__(kBlock, PGX_MIN_BLOCKS) min_run_kernel(MinRunP
   constexpr bool bfs = BFS && APP == PGX_APP_SSSP && S == 0;
   if (gtid == 0) p.stats[PGX_STAT_HDR + 7] = (int64_t)globaltimer();
   unsigned sv_stale = 0u;  // bit b: sv[b] may hold stale senders (grid-uniform)
+  bool front_skipped = false;  // the last apply built no frontier (grid-uniform)
+  int e_prev = (int)p.m;       // edges of the previous superstep (prediction)
 
   for (int s = 0;; s++) {
     // ---- scatter(s): senders push along out-edges into the mailbox ----
@@ -133,7 +136,11 @@ __global__ void __launch_bounds__(kBlock, PGX_MIN_BLOCKS) min_run_kernel(MinRunP
     // a segmented superstep needs exact send values: after a K1 superstep
     // left them stale (below), K1 runs instead (never on C2 / C5, whose
     // dense supersteps come first)
-    const bool seg_s = p.use_seg && edges_s >= p.seg_min_edges && edges_s > 0 &&
+    // (after an apply that predicted a segmented superstep and built no
+    // frontier, the segmented pass runs whatever the edge count: a wrong
+    // guess costs at most one dense pass; the send values are exact)
+    const bool seg_s = p.use_seg && edges_s > 0 &&
+                       (edges_s >= p.seg_min_edges || front_skipped) &&
                        !((sv_stale >> (s & 1)) & 1u);
     if (p.use_seg && s >= 1 && (p.ws.ctr[s - 1].packed >> 32) != 0ull) {
       // the send buffers of superstep s + 1, written by the next apply,
@@ -231,17 +238,27 @@ __global__ void __launch_bounds__(kBlock, PGX_MIN_BLOCKS) min_run_kernel(MinRunP
     // its send values alone
     uint32_t *snd_out = (p.use_seg && !use_sv) ? p.ws.snd[(s + 1) & 1] : nullptr;
     uint32_t *sv_out = use_sv ? p.ws.sv[(s + 1) & 1] : nullptr;
+    // CC: predict whether superstep s+1 is segmented (it reads the send
+    // values, not a frontier): this one is and the geometric edge trend
+    // E_s * E_s / E_{s-1} stays above twice the threshold.  A wrong guess
+    // runs the next superstep segmented anyway (at most one dense pass)
+    const float e_s = (float)edges_s;
+    const bool trend = e_s * (e_s / (float)max(e_prev, 1)) >= 2.0f * (float)p.seg_min_edges;
+    const bool skip = use_sv && seg_s && !at_cap &&
+                      (p.seg_predict == 2 || (p.seg_predict == 1 && trend));
     const unsigned long long rb =
         bfs ? apply_min_phase<APP, 0, true>(p.row_ptr, val, mailbox, p.n, p.ws, &p.ws.ctr[s + 1],
                                             smem, at_cap, (uint32_t)s + 1u, snd_out)
             : apply_min_phase<APP, S>(p.row_ptr, val, mailbox, p.n, p.ws, &p.ws.ctr[s + 1], smem,
-                                      at_cap, 0u, snd_out, sv_out);
+                                      at_cap, 0u, snd_out, sv_out, skip);
     const unsigned bc = block_sum<unsigned>((unsigned)(rb & 0xFFFFFFFFull), s_red);
     const unsigned rc = block_sum<unsigned>((unsigned)(rb >> 32), s_red);
     if (threadIdx.x == 0) {
       if (bc) atomicAdd(&p.ws.ctr[s + 1].bcast, bc);
       if (rc) atomicAdd(&p.ws.ctr[s].recip, rc);
     }
+    front_skipped = skip;
+    e_prev = (int)edges_s;
     grid_sync<kArriveRed>(p.ws.bar, gen);
 
     // ---- stats + halt test (engine.py:284-300) ----
@@ -612,6 +629,7 @@ static int min_run(int app, int32_t n, int64_t m, const int32_t *row_ptr, const 
   if (p.use_seg) p.seg = *seg;
   else memset(&p.seg, 0, sizeof p.seg);
   p.seg_min_edges = (m * (int64_t)g_opt[PGX_OPT_SEG_MIN_EDGES]) / 1024;
+  p.seg_predict = g_opt[PGX_OPT_SEG_PREDICT];
   size_t smem = scatter_smem(PGX_OP_MIN_U32, nhubs);
   if (p.use_seg) smem = std::max(smem, seg_smem_bytes(p.seg.seg_log2) + 16);
   int grid = 0;

@@ -54,8 +54,9 @@ def rel_err(got, want):
 def seg_threshold():
     """Set PGX_OPT_SEG_MIN_EDGES (and optionally the gate / fused-apply
     knobs) for one test, restore the shipped values."""
-    def set_(v):
+    def set_(v, pred=1):
         _lib.set_option(_lib.PGX_OPT_SEG_MIN_EDGES, v)
+        _lib.set_option(_lib.PGX_OPT_SEG_PREDICT, pred)
     yield set_
     set_(256)
 
@@ -64,13 +65,15 @@ def seg_threshold():
 # segment policy: device graphs get the segmented scatter for supersteps
 # with >= m/4 sender edges), hubs (hub-cache arm), k1 (segments off: K1 in
 # every superstep), segall (the segmented scatter whenever its send values
-# are exact: every superstep until the first K1 one)
-@pytest.mark.parametrize("mode", ["pull", "push", "hubs", "k1", "segall"])
+# are exact: every superstep until the first K1 one), segskip (default
+# threshold, the apply never builds a frontier after a segmented superstep,
+# so every superstep after one runs segmented too)
+@pytest.mark.parametrize("mode", ["pull", "push", "hubs", "k1", "segall", "segskip"])
 @pytest.mark.parametrize("r", RUNS, ids=lambda r: r.id)
 def test_golden_reference_runs(r, mode, seg_threshold):
     if mode == "push" and r.app != "pagerank":
         pytest.skip("pagerank_mode only changes the PageRank lowering")
-    if mode in ("hubs", "k1", "segall") and r.app == "pagerank":
+    if mode in ("hubs", "k1", "segall", "segskip") and r.app == "pagerank":
         pytest.skip("hub_cache / segments only change the min combiner")
     g = pgx.from_edges(r.src, r.dst, r.n, undirected=r.undirected, device="cuda")
     cap = r.kwargs.get("max_supersteps")
@@ -79,8 +82,10 @@ def test_golden_reference_runs(r, mode, seg_threshold):
                            hub_cache="on" if mode == "hubs" else "off",
                            segments="off" if mode == "k1" else
                            "on" if mode.startswith("seg") else "auto")
-    if mode.startswith("seg"):
+    if mode == "segall":
         seg_threshold(0)
+    elif mode == "segskip":
+        seg_threshold(256, pred=2)
     rep = pgx.run(g, program(r.app, r.kwargs), cfg)
     if r.app == "pagerank":
         assert rep.values.dtype == np.float64

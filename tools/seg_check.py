@@ -15,8 +15,8 @@ from paper_2010_01542_b200.rmat import rmat_graph
 
 cfgs = sys.argv[1].split(",") if len(sys.argv) > 1 else ["C2", "C3"]
 variants = sys.argv[2:] or ["off", "shipped"]
-OPTS = {"min": _lib.PGX_OPT_SEG_MIN_EDGES}
-DEFAULTS = {"min": 256}
+OPTS = {"min": _lib.PGX_OPT_SEG_MIN_EDGES, "pred": _lib.PGX_OPT_SEG_PREDICT}
+DEFAULTS = {"min": 256, "pred": 1}
 for c in cfgs:
     g = rmat_graph(c)
     app = {"C2": "components", "C3": "sssp", "C5": "components", "C5S": "components"}[c]
