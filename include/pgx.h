@@ -153,6 +153,20 @@ int pgx_seg_workspace_bytes(int32_t n, int64_t m, int64_t nent,
 int pgx_seg_max_items(int32_t n, int64_t m, int32_t seg_log2,
                       int32_t *max_items);
 
+/* Rectangular form (the partitioned path): nrows source rows, destinations
+ * < ndst (pgx_seg_workspace_bytes / pgx_seg_max_items then take ndst). */
+int pgx_seg_count_ex(int32_t nrows, int32_t ndst, int64_t m,
+                     const int32_t *row_ptr, const int32_t *col_idx,
+                     const void *graph_ws, int32_t seg_log2, void *ws,
+                     size_t ws_bytes, int64_t *nent, uintptr_t stream);
+int pgx_seg_build_ex(int32_t nrows, int32_t ndst, int64_t m,
+                     const int32_t *row_ptr, const int32_t *col_idx,
+                     const void *graph_ws, int32_t seg_log2, int64_t nent,
+                     void *ws, size_t ws_bytes, int32_t *ent_src,
+                     int32_t *ent_eb, uint16_t *col16, int32_t *tile_ent,
+                     int32_t *items, int32_t *nitems, int32_t ctas,
+                     uintptr_t stream);
+
 /* step 1 (syncs): the number of entries into *nent (host out).  graph_ws
  * is the pgx_graph_prepare workspace of (row_ptr, col_idx). */
 int pgx_seg_count(int32_t n, int64_t m, const int32_t *row_ptr,
@@ -343,7 +357,24 @@ int pgx_apply_slice(int app, int32_t len, const int32_t *row_ptr,
                     uint32_t *val, uint32_t *mailbox_slice, int32_t *f_eb,
                     int32_t *f_rs, uint32_t *f_msg, int32_t *tile_src,
                     void *counters, int32_t count_only, uint32_t neutral,
-                    uintptr_t stream);
+                    uint32_t *send_values, uintptr_t stream);
+/* send_values (CC, may be NULL): the label every new sender sends is also
+ * stored at send_values[local v] -- the input of pgx_seg_scatter; the
+ * caller fills it with UINT32_MAX (no message) before the apply. */
+
+/* K1s on a rank's slice (the dense supersteps of the partitioned CC): the
+ * destination-segmented scatter (pgx_seg.cuh) of the rank's local CSR,
+ * whose destinations are padded mailbox positions < ndst, built with
+ * pgx_seg_count_ex / pgx_seg_build_ex (nrows = the rank's rows).  msg 0:
+ * every entry's source sends its global id (local id + id_offset, CC
+ * superstep 0); msg 1: it sends send_values[local source] (UINT32_MAX =
+ * no message).  Writes exactly what pgx_scatter(PGX_OP_MIN_U32, ...)
+ * would: the min-combined mailbox (untouched owned slots stored as
+ * `neutral`) and its has-bits.  item_ctr: one device word of scratch. */
+int pgx_seg_scatter(int msg, const PgxSegIndex *seg, int64_t m, int32_t ndst,
+                    int32_t id_offset, const uint32_t *send_values,
+                    uint32_t *mailbox, uint32_t *has_bits, uint32_t neutral,
+                    unsigned *item_ctr, uintptr_t stream);
 
 /* PageRank apply on an owned slice: rank, next share, per-CTA dangling
  * partials (partials[ceil(len/512)]).  `dangling` is a DEVICE scalar, the

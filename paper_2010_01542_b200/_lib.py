@@ -45,7 +45,8 @@ EXPORTS = (
     "pgx_scatter_peer", "pgx_reset_touched", "pgx_peer_alloc", "pgx_peer_open",
     "pgx_peer_close", "pgx_peer_free", "pgx_seg_workspace_bytes", "pgx_seg_max_items",
     "pgx_seg_count", "pgx_seg_build", "pgx_sssp_run_ex", "pgx_cc_run_ex",
-    "pgx_gather_slice", "pgx_fold_spanning", "pgx_peer_enable",
+    "pgx_gather_slice", "pgx_fold_spanning", "pgx_peer_enable", "pgx_seg_scatter",
+    "pgx_seg_count_ex", "pgx_seg_build_ex",
 )
 
 
@@ -101,7 +102,12 @@ _SIGS = {
     "pgx_peer_free": (ctypes.c_int, [_p]),
     "pgx_slice_counters_bytes": (ctypes.c_int, [_p]),
     "pgx_apply_slice": (ctypes.c_int, [ctypes.c_int, _i32, _p, _p, _p, _p, _p, _p, _p, _p,
-                                       _i32, ctypes.c_uint32, _up]),
+                                       _i32, ctypes.c_uint32, _p, _up]),
+    "pgx_seg_scatter": (ctypes.c_int, [ctypes.c_int, _p, _i64, _i32, _i32, _p, _p, _p,
+                                       ctypes.c_uint32, _p, _up]),
+    "pgx_seg_count_ex": (ctypes.c_int, [_i32, _i32, _i64, _p, _p, _p, _i32, _p, _sz, _p, _up]),
+    "pgx_seg_build_ex": (ctypes.c_int, [_i32, _i32, _i64, _p, _p, _p, _i32, _i64, _p, _sz, _p,
+                                        _p, _p, _p, _p, _p, _i32, _up]),
     "pgx_pr_apply_slice": (ctypes.c_int, [_i32, _p, _p, _p, _p, _f64, _f64, _p, _f64, _i32,
                                           _p, _up]),
     "pgx_gather_slice": (ctypes.c_int, [_i32, _i64, _p, _p, _i32, _p, _p, _p, _p, _up]),

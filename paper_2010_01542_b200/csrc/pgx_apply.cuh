@@ -51,9 +51,6 @@ __device__ __forceinline__ unsigned long long block_excl_scan_u64(unsigned long 
 // kListCap ids), which is consumed in batches of kApplyItems independent
 // recipients per thread -- a handful of dependent round trips per chunk
 // instead of one serial chain per 64 words.
-#ifndef PGX_APPLY_SPEC
-#define PGX_APPLY_SPEC 1
-#endif
 #ifndef PGX_APPLY_ITEMS
 #define PGX_APPLY_ITEMS 4
 #endif
@@ -126,7 +123,6 @@ __device__ unsigned long long apply_min_phase(const int32_t *__restrict__ row_pt
           v[j] = (idx < cnt) ? s_list[idx] : -1;
           PGX_ASSERT(v[j] < n);
         }
-#if PGX_APPLY_SPEC
         // every load of the batch in one round trip: the row pointers are
         // read speculatively (the list is in vertex order: near-coalesced)
         int re[kApplyItems];
@@ -153,36 +149,6 @@ __device__ unsigned long long apply_min_phase(const int32_t *__restrict__ row_pt
             }
           }
         }
-#else
-#pragma unroll
-        for (int j = 0; j < kApplyItems; j++) {
-          if (v[j] >= 0) {
-            m[j] = *slot<S>(mailbox, v[j]);
-            cv[j] = *slot<S>(val, v[j]);
-          }
-        }
-        unsigned long long mine = 0;
-#pragma unroll
-        for (int j = 0; j < kApplyItems; j++) {
-          deg[j] = 0;
-          if (v[j] >= 0) {
-            *slot<S>(mailbox, v[j]) = kNeutralMin;  // consume (mailbox.py:112-117)
-            if (m[j] < cv[j]) {
-              *slot<S>(val, v[j]) = m[j];
-              bcast++;
-              rs[j] = row_ptr[v[j]];
-              deg[j] = -1;  // improved; degree resolved below
-            }
-          }
-        }
-#pragma unroll
-        for (int j = 0; j < kApplyItems; j++) {
-          if (deg[j] == -1) {
-            deg[j] = row_ptr[v[j] + 1] - rs[j];
-            if (deg[j] > 0) mine += (1ull << 32) | (unsigned long long)deg[j];
-          }
-        }
-#endif
         unsigned long long total;
         unsigned long long run = block_excl_scan_u64(mine, s_w, &total);
         if (no_frontier) {

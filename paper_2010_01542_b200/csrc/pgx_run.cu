@@ -178,6 +178,8 @@ __global__ void __launch_bounds__(kBlock, PGX_MIN_BLOCKS) min_run_kernel(MinRunP
       sp.has = p.ws.has;
       sp.item_ctr = reinterpret_cast<unsigned *>(&p.ws.ctr[s].pad[0]);
       sp.write_mailbox = !bfs;
+      sp.id_offset = 0;
+      sp.out_neutral = kNeutralMin;
       if (APP == PGX_APP_CC && s == 0)
         seg_scatter_phase<kSegSourceId>(sp, smem);
       else if (bfs)

@@ -152,7 +152,7 @@ int key_bits(int32_t nseg) {
   return b;
 }
 
-size_t seg_ws_layout(int32_t n, int64_t m, int64_t nent, int L, SegWs *w, char *base) {
+size_t seg_ws_layout(int32_t ndst, int64_t m, int64_t nent, int L, SegWs *w, char *base) {
   size_t off = 0;
   auto take = [&](size_t bytes) {
     char *p = base ? base + off : nullptr;
@@ -160,7 +160,7 @@ size_t seg_ws_layout(int32_t n, int64_t m, int64_t nent, int L, SegWs *w, char *
     return p;
   };
   const int64_t ntiles = ceil_div(m, kTile);
-  const int32_t nseg = (int32_t)ceil_div(n, (int64_t)1 << L);
+  const int32_t nseg = (int32_t)ceil_div(ndst, (int64_t)1 << L);
   const int64_t ne = nent < 0 ? 0 : nent;
   SegWs x;
   x.tile_cnt = (int32_t *)take(sizeof(int32_t) * (ntiles + 1));
@@ -248,25 +248,34 @@ int pgx_seg_max_items(int32_t n, int64_t m, int32_t seg_log2, int32_t *max_items
   return PGX_OK;
 }
 
+int pgx_seg_count_ex(int32_t nrows, int32_t ndst, int64_t m, const int32_t *row_ptr,
+                     const int32_t *col_idx, const void *graph_ws, int32_t seg_log2, void *ws,
+                     size_t ws_bytes, int64_t *nent, uintptr_t stream) {
+  int rc = seg_check(nrows, m, row_ptr, col_idx, graph_ws, seg_log2);
+  if (rc) return rc;
+  if (ndst < 1) return fail(PGX_EINVAL, "destination count must be >= 1");
+  if (!ws || !nent) return fail(PGX_EINVAL, "null workspace / output");
+  SegWs w;
+  if (seg_ws_layout(ndst, m, -1, seg_log2, &w, (char *)ws) > ws_bytes)
+    return fail(PGX_ENOMEM, "segmented-index workspace too small");
+  return count_runs(nrows, m, col_idx, graph_ws, seg_log2, w, nent, (cudaStream_t)stream);
+}
+
 int pgx_seg_count(int32_t n, int64_t m, const int32_t *row_ptr, const int32_t *col_idx,
                   const void *graph_ws, int32_t seg_log2, void *ws, size_t ws_bytes,
                   int64_t *nent, uintptr_t stream) {
-  int rc = seg_check(n, m, row_ptr, col_idx, graph_ws, seg_log2);
-  if (rc) return rc;
-  if (!ws || !nent) return fail(PGX_EINVAL, "null workspace / output");
-  SegWs w;
-  if (seg_ws_layout(n, m, -1, seg_log2, &w, (char *)ws) > ws_bytes)
-    return fail(PGX_ENOMEM, "segmented-index workspace too small");
-  return count_runs(n, m, col_idx, graph_ws, seg_log2, w, nent, (cudaStream_t)stream);
+  return pgx_seg_count_ex(n, n, m, row_ptr, col_idx, graph_ws, seg_log2, ws, ws_bytes, nent,
+                          stream);
 }
 
-int pgx_seg_build(int32_t n, int64_t m, const int32_t *row_ptr, const int32_t *col_idx,
-                  const void *graph_ws, int32_t seg_log2, int64_t nent, void *ws,
-                  size_t ws_bytes, int32_t *ent_src, int32_t *ent_eb, uint16_t *col16,
-                  int32_t *tile_ent, int32_t *items, int32_t *nitems, int32_t ctas,
-                  uintptr_t stream) {
-  int rc = seg_check(n, m, row_ptr, col_idx, graph_ws, seg_log2);
+int pgx_seg_build_ex(int32_t nrows, int32_t ndst, int64_t m, const int32_t *row_ptr,
+                     const int32_t *col_idx, const void *graph_ws, int32_t seg_log2,
+                     int64_t nent, void *ws, size_t ws_bytes, int32_t *ent_src, int32_t *ent_eb,
+                     uint16_t *col16, int32_t *tile_ent, int32_t *items, int32_t *nitems,
+                     int32_t ctas, uintptr_t stream) {
+  int rc = seg_check(nrows, m, row_ptr, col_idx, graph_ws, seg_log2);
   if (rc) return rc;
+  if (ndst < 1) return fail(PGX_EINVAL, "destination count must be >= 1");
   if (!ws || !ent_src || !ent_eb || !col16 || !tile_ent || !items || !nitems)
     return fail(PGX_EINVAL, "null segmented-index output");
   if (nent < 1 || nent > m) return fail(PGX_EINVAL, "entry count out of range");
@@ -276,16 +285,16 @@ int pgx_seg_build(int32_t n, int64_t m, const int32_t *row_ptr, const int32_t *c
   const int L = seg_log2;
   cudaStream_t st = (cudaStream_t)stream;
   SegWs w;
-  if (seg_ws_layout(n, m, nent, L, &w, (char *)ws) > ws_bytes)
+  if (seg_ws_layout(ndst, m, nent, L, &w, (char *)ws) > ws_bytes)
     return fail(PGX_ENOMEM, "segmented-index workspace too small");
   int64_t got = 0;
-  rc = count_runs(n, m, col_idx, graph_ws, L, w, &got, st);
+  rc = count_runs(nrows, m, col_idx, graph_ws, L, w, &got, st);
   if (rc) return rc;
   if (got != nent) return fail(PGX_EINVAL, "entry count does not match pgx_seg_count");
   GraphWs g;
-  graph_ws_layout(n, m, &g, (char *)graph_ws);
+  graph_ws_layout(nrows, m, &g, (char *)graph_ws);
   const int64_t ntiles = ceil_div(m, kTile);
-  const int32_t nseg = (int32_t)ceil_div(n, (int64_t)1 << L);
+  const int32_t nseg = (int32_t)ceil_div(ndst, (int64_t)1 << L);
   // 1. the runs in CSR order
   seg_runs_kernel<true><<<(unsigned)ceil_div(ntiles, kRunWarps), kRunWarps * 32, 0, st>>>(
       m, col_idx, g, L, nullptr, w.tile_base, w.run_pos, w.run_src, w.key_in);
@@ -338,12 +347,21 @@ int pgx_seg_build(int32_t n, int64_t m, const int32_t *row_ptr, const int32_t *c
     return (p.e1 - p.e0) > (q.e1 - q.e0);
   });
   int32_t cap = 0;
-  pgx_seg_max_items(n, m, L, &cap);
+  pgx_seg_max_items(ndst, m, L, &cap);
   if ((int64_t)v.size() > cap) return fail(PGX_EINVAL, "internal: too many work items");
   PGX_CUDA(cudaMemcpyAsync(items, v.data(), sizeof(Item) * v.size(), cudaMemcpyHostToDevice, st));
   PGX_CUDA(cudaStreamSynchronize(st));
   *nitems = (int32_t)v.size();
   return PGX_OK;
+}
+
+int pgx_seg_build(int32_t n, int64_t m, const int32_t *row_ptr, const int32_t *col_idx,
+                  const void *graph_ws, int32_t seg_log2, int64_t nent, void *ws,
+                  size_t ws_bytes, int32_t *ent_src, int32_t *ent_eb, uint16_t *col16,
+                  int32_t *tile_ent, int32_t *items, int32_t *nitems, int32_t ctas,
+                  uintptr_t stream) {
+  return pgx_seg_build_ex(n, n, m, row_ptr, col_idx, graph_ws, seg_log2, nent, ws, ws_bytes,
+                          ent_src, ent_eb, col16, tile_ent, items, nitems, ctas, stream);
 }
 
 }  // extern "C"

@@ -78,6 +78,9 @@ struct SegPass {
   uint32_t *has;
   unsigned *item_ctr;   // zero before the pass
   bool write_mailbox;   // false: the has-bitmask is the whole result (unit SSSP)
+  int32_t id_offset;    // kSegSourceId: message = entry source + id_offset
+  uint32_t out_neutral; // what an owned, untouched slot is stored as (the
+                        // partitioned path's exchange neutral, INT32_MAX)
 };
 
 // Shared-memory slot of segment offset `loc`: the bank bits (low 5) are
@@ -163,11 +166,17 @@ __device__ void seg_scatter_phase(const SegPass &a, char *smem_raw) {
       // one round trip for the whole tile: the flagged 16-bit destinations
       // and the entries' messages
       cp_async16(w_col + lane * 8, a.ix.col16 + ta + lane * 8);
-      if (MSG == kSegSourceId) {
+      if (MSG == kSegSourceId && a.id_offset == 0) {
 #pragma unroll
         for (int q = 0; q < (kSlots + 31) / 32; q++) {
           const int j = lane + 32 * q;
           if (j < k) cp_async4(w_msg + j, a.ix.ent_src + i0 + j);
+        }
+      } else if (MSG == kSegSourceId) {  // a rank's slice: global source ids
+#pragma unroll
+        for (int q = 0; q < (kSlots + 31) / 32; q++) {
+          const int j = lane + 32 * q;
+          if (j < k) w_msg[j] = (uint32_t)(__ldg(a.ix.ent_src + i0 + j) + a.id_offset);
         }
       } else {
         int src[(kSlots + 31) / 32];
@@ -233,7 +242,7 @@ __device__ void seg_scatter_phase(const SegPass &a, char *smem_raw) {
       const bool touched = v != kNeutralMin && in;
       const unsigned bits = __ballot_sync(0xFFFFFFFFu, touched);
       if (sole) {  // the item owns these slots and words: plain stores
-        if (a.write_mailbox && in) a.mailbox[g] = v;
+        if (a.write_mailbox && in) a.mailbox[g] = touched ? v : a.out_neutral;
         if (lane == 0 && in) a.has[g >> 5] = bits;
       } else {     // a slice of a hot segment: fire-and-forget combines
         if (a.write_mailbox && touched) red_min_u32(a.mailbox + g, v);

@@ -6,6 +6,7 @@
 #include "pgx_common.cuh"
 #include "pgx_gather.cuh"
 #include "pgx_scatter.cuh"
+#include "pgx_seg.cuh"
 
 namespace pgx {
 namespace {
@@ -47,7 +48,7 @@ template <int APP>
 __global__ void __launch_bounds__(kBlock) apply_slice_kernel(
     int32_t len, const int32_t *__restrict__ row_ptr, uint32_t *val, uint32_t *mailbox,
     int32_t *f_eb, int32_t *f_rs, uint32_t *f_msg, int32_t *tile_src, SliceCounters *ctr,
-    int32_t count_only, uint32_t neutral) {
+    int32_t count_only, uint32_t neutral, uint32_t *sv) {
   __shared__ unsigned long long s_w[33];
   __shared__ unsigned long long s_gbase;
   __shared__ unsigned long long s_red[32];
@@ -89,6 +90,7 @@ __global__ void __launch_bounds__(kBlock) apply_slice_kernel(
         f_eb[pos] = eb;
         f_rs[pos] = rs[j];
         f_msg[pos] = (APP == PGX_APP_SSSP) ? m[j] + 1u : m[j];
+        if (sv) sv[base + j * kBlock + threadIdx.x] = m[j];  // CC: the label it sends (K1s)
         for (int64_t t = ((int64_t)eb + kTile - 1) / kTile; t * kTile < (int64_t)eb + deg[j]; t++)
           tile_src[t] = (int)pos;
         run += (1ull << 32) | (unsigned long long)deg[j];
@@ -133,6 +135,15 @@ __global__ void __launch_bounds__(kBlock) pr_apply_slice_kernel(
 __global__ void __launch_bounds__(kBlock, PGX_MIN_BLOCKS) gather_slice_kernel(GatherArgs g) {
   extern __shared__ __align__(16) char smem[];
   gather_phase(g, smem);
+}
+
+// K1s on a rank's slice: the destination-segmented scatter of the rank's
+// local CSR (destinations = padded mailbox positions) into its full-width
+// mailbox; message = global source id (superstep 0) or the send value.
+template <int MSG>
+__global__ void __launch_bounds__(kBlock, PGX_MIN_BLOCKS) seg_slice_kernel(SegPass sp) {
+  extern __shared__ __align__(16) char smem[];
+  seg_scatter_phase<MSG>(sp, smem);
 }
 
 // rows whose in-edges span tiles: tail of the first tile + heads of the
@@ -484,7 +495,7 @@ int pgx_slice_counters_bytes(size_t *bytes) {
 int pgx_apply_slice(int app, int32_t len, const int32_t *row_ptr, uint32_t *val,
                     uint32_t *mailbox_slice, int32_t *f_eb, int32_t *f_rs, uint32_t *f_msg,
                     int32_t *tile_src, void *counters, int32_t count_only, uint32_t neutral,
-                    uintptr_t stream) {
+                    uint32_t *send_values, uintptr_t stream) {
   if (app != PGX_APP_CC && app != PGX_APP_SSSP) return fail(PGX_EINVAL, "min apps only");
   if (len < 0 || !counters) return fail(PGX_EINVAL, "bad apply_slice arguments");
   if (!len) return PGX_OK;
@@ -494,12 +505,12 @@ int pgx_apply_slice(int app, int32_t len, const int32_t *row_ptr, uint32_t *val,
     apply_slice_kernel<PGX_APP_CC><<<grid, kBlock, 0, st>>>(len, row_ptr, val, mailbox_slice, f_eb,
                                                            f_rs, f_msg, tile_src,
                                                            (SliceCounters *)counters, count_only,
-                                                           neutral);
+                                                           neutral, send_values);
   else
     apply_slice_kernel<PGX_APP_SSSP><<<grid, kBlock, 0, st>>>(len, row_ptr, val, mailbox_slice,
                                                              f_eb, f_rs, f_msg, tile_src,
                                                              (SliceCounters *)counters,
-                                                             count_only, neutral);
+                                                             count_only, neutral, nullptr);
   PGX_CUDA(cudaGetLastError());
   return PGX_OK;
 }
@@ -552,6 +563,49 @@ int pgx_gather_slice(int32_t nrows, int64_t m, const int32_t *in_col, const void
   PGX_CUDA(cudaFuncSetAttribute(gather_slice_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 (int)smem));
   gather_slice_kernel<<<grid, kBlock, smem, st>>>(g);
+  PGX_CUDA(cudaGetLastError());
+  return PGX_OK;
+}
+
+int pgx_seg_scatter(int msg, const PgxSegIndex *seg, int64_t m, int32_t ndst, int32_t id_offset,
+                    const uint32_t *send_values, uint32_t *mailbox, uint32_t *has_bits,
+                    uint32_t neutral, unsigned *item_ctr, uintptr_t stream) {
+  if (!seg || m < 1 || m > INT32_MAX || ndst < 1 || !mailbox || !has_bits || !item_ctr ||
+      (msg == 1 && !send_values) || (msg != 0 && msg != 1))
+    return fail(PGX_EINVAL, "bad pgx_seg_scatter arguments");
+  if (seg->seg_log2 < 5 || seg->seg_log2 > kSegMaxLog2 || seg->nent < 1 || seg->nent > m ||
+      seg->nitems < 1 || !seg->ent_src || !seg->col16 || !seg->tile_ent || !seg->items ||
+      reinterpret_cast<uintptr_t>(seg->items) % 16 || reinterpret_cast<uintptr_t>(seg->col16) % 16)
+    return fail(PGX_EINVAL, "malformed segmented index");
+  SegPass sp;
+  sp.ix = *seg;
+  sp.m = m;
+  sp.n = ndst;
+  sp.snd = nullptr;
+  sp.sv = send_values;
+  sp.uniform = 0u;
+  sp.mailbox = mailbox;
+  sp.has = has_bits;
+  sp.item_ctr = item_ctr;
+  sp.write_mailbox = true;
+  sp.id_offset = id_offset;
+  sp.out_neutral = neutral;
+  cudaStream_t st = (cudaStream_t)stream;
+  PGX_CUDA(cudaMemsetAsync(item_ctr, 0, sizeof(unsigned), st));
+  const size_t smem = seg_smem_bytes(seg->seg_log2) + 16;
+  int sms = 148, dev = 0;
+  if (cudaGetDevice(&dev) == cudaSuccess)
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const int grid = std::max(1, std::min(sms * PGX_MIN_BLOCKS, seg->nitems));
+  if (msg == 0) {
+    PGX_CUDA(cudaFuncSetAttribute(seg_slice_kernel<kSegSourceId>,
+                                  cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    seg_slice_kernel<kSegSourceId><<<grid, kBlock, smem, st>>>(sp);
+  } else {
+    PGX_CUDA(cudaFuncSetAttribute(seg_slice_kernel<kSegLabel>,
+                                  cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    seg_slice_kernel<kSegLabel><<<grid, kBlock, smem, st>>>(sp);
+  }
   PGX_CUDA(cudaGetLastError());
   return PGX_OK;
 }

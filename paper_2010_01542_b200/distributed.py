@@ -17,7 +17,9 @@ one GPU (CC labels / SSSP distances bit-exact, PageRank within 1e-9):
   reduces, and the owner of a slot is ``slot // B``.  Messages stay global
   vertex ids (CC labels, SSSP distances).
 * **per superstep** (min programs): every rank scatters its senders into
-  its full-width mailbox (``pgx_scatter``); the mailbox is delivered to the
+  its full-width mailbox (``pgx_scatter``; CC's dense supersteps -- sender
+  edges >= a quarter of the rank's -- through the rank's own segmented
+  index, ``pgx_seg_scatter``, as on one GPU); the mailbox is delivered to the
   owners by one of three exchanges (below); the owner applies on its block
   (``pgx_apply_slice``); ONE all-gather of every rank's (recipients,
   broadcasts, senders, edges) drives the halt test and the statistics and
@@ -401,13 +403,16 @@ class PeerMailbox:
 class CudaBackend:
     """Owns the rank's local CSR, full-width mailbox and owned-block state."""
 
-    def __init__(self, graph, lo: int, hi: int, device, pr_mode: str = "pull"):
+    def __init__(self, graph, lo: int, hi: int, device, pr_mode: str = "pull",
+                 segments: str = "auto"):
         from . import _lib
         self._lib = _lib
         self.lib = _lib.load()
         self.device = torch.device(device)
         self.stream = torch.cuda.current_stream(self.device)
         self.pr_mode = pr_mode
+        # CC dense supersteps through K1s (pgx_seg_scatter) unless "off"
+        self.segments = segments
         dev = self.device
         # slice where the graph lives and upload only this rank's rows (a
         # pinned host graph stays pinned under slicing: one DMA per array)
@@ -498,6 +503,7 @@ class CudaBackend:
             self._pbounds = torch.arange(self.world + 1, dtype=torch.int32,
                                          device=self.device) * block
         self._pull = None
+        self._seg = None
         self._peer_sig = None
         self._peer_decision = None
         self._bound = sig
@@ -563,6 +569,48 @@ class CudaBackend:
         self._peer_sig = sig
         return True
 
+    # ---- K1s on the slice (CC dense supersteps) ----
+    def _ensure_seg(self):
+        """The rank's rectangular segmented index (rows = its sources,
+        destinations = padded mailbox positions), built once per layout."""
+        if self._seg is not None:
+            return self._seg
+        L, lib, dev, st = self._lib.PGX_SEG_LOG2_DEFAULT, self.lib, self.device, self.stream
+        n_r, nd, m = self.len, self.npad, self.m_local
+        with torch.cuda.device(dev), torch.cuda.stream(st):
+            sp = st.cuda_stream
+            ws = torch.empty(self._lib.out_size(lib.pgx_seg_workspace_bytes, nd, m, -1, L),
+                             dtype=torch.uint8, device=dev)
+            nent = ctypes.c_int64(0)
+            self._lib.check(lib.pgx_seg_count_ex(n_r, nd, m, self.row_ptr.data_ptr(),
+                                                 self.col.data_ptr(), self.gws.data_ptr(), L,
+                                                 ws.data_ptr(), ws.numel(), ctypes.byref(nent), sp),
+                            "pgx_seg_count_ex")
+            ne = int(nent.value)
+            ws = torch.empty(self._lib.out_size(lib.pgx_seg_workspace_bytes, nd, m, ne, L),
+                             dtype=torch.uint8, device=dev)
+            cap = ctypes.c_int32(0)
+            self._lib.check(lib.pgx_seg_max_items(nd, m, L, ctypes.byref(cap)), "pgx_seg_max_items")
+            arrays = (torch.zeros(ne + 4, dtype=torch.int32, device=dev),       # ent_src
+                      torch.empty(ne + 1, dtype=torch.int32, device=dev),       # ent_eb
+                      torch.empty(m + 256, dtype=torch.int16, device=dev),      # col16
+                      torch.empty((m + 255) // 256 + 1, dtype=torch.int32, device=dev),
+                      torch.empty(4 * int(cap.value), dtype=torch.int32, device=dev))
+            nitems = ctypes.c_int32(0)
+            self._lib.check(lib.pgx_seg_build_ex(n_r, nd, m, self.row_ptr.data_ptr(),
+                                                 self.col.data_ptr(), self.gws.data_ptr(), L, ne,
+                                                 ws.data_ptr(), ws.numel(),
+                                                 *(a.data_ptr() for a in arrays),
+                                                 ctypes.byref(nitems), 0, sp), "pgx_seg_build_ex")
+        self._seg = (self._lib.PgxSegIndex(L, ne, int(nitems.value), 0,
+                                           *(a.data_ptr() for a in arrays)),
+                     arrays, torch.zeros(1, dtype=torch.int32, device=dev))
+        return self._seg
+
+    def _use_seg(self, dense: bool) -> bool:
+        return (self.segments != "off" and self.app == "components" and self.m_local > 0
+                and (dense or 4 * self.E >= self.m_local))
+
     # ---- min programs ----
     def init_min(self, app):
         self.app = app
@@ -573,6 +621,9 @@ class CudaBackend:
         self.mailbox.fill_(EXCHANGE_NEUTRAL)
         self.has.zero_()
         self.val = torch.empty(max(self.len, 1), dtype=torch.int32, device=self.device)
+        # CC send values (K1s): the label a sender sends, -1 (UINT32_MAX) otherwise
+        self.sv = torch.full((max(self.len, 1),), -1, dtype=torch.int32, device=self.device) \
+            if app == "components" and self.segments != "off" else None
         app_id = self._lib.PGX_APP_CC if app == "components" else self._lib.PGX_APP_SSSP
         self._k(self.lib.pgx_slice_init(app_id, self.len, self.lo_own, self.val.data_ptr(),
                                         self.row_ptr.data_ptr(), None, 0.0,
@@ -640,6 +691,15 @@ class CudaBackend:
     def scatter_min(self, dense: bool, peer: bool = False):
         L, st = self.lib, self.stream.cuda_stream
         op = self._lib.PGX_OP_MIN_U32
+        if not peer and self._use_seg(dense):
+            # the dense CC supersteps: K1s into the full-width mailbox
+            ix, _, ctr = self._ensure_seg()
+            self._scattered = self.m_local if dense else self.E
+            self._k(L.pgx_seg_scatter(0 if dense else 1, ctypes.byref(ix), self.m_local, self.npad,
+                                      self.lo_own, None if dense else self.sv.data_ptr(),
+                                      self.mailbox.data_ptr(), self.has.data_ptr(),
+                                      EXCHANGE_NEUTRAL, ctr.data_ptr(), st), "pgx_seg_scatter")
+            return
         if dense:
             src = (self._g_nz_eb.data_ptr(), None, self._g_nz_id.data_ptr(), self.lo_own, None,
                    self._g_tile.data_ptr(), self._nnz(), self.m_local)
@@ -666,11 +726,15 @@ class CudaBackend:
         self.ctr.zero_()
         app_id = self._lib.PGX_APP_CC if app == "components" else self._lib.PGX_APP_SSSP
         sl = self.mailbox[self.blo:self.blo + self.len]
+        sv = None
+        if self.sv is not None:
+            self.sv.fill_(-1)
+            sv = self.sv.data_ptr()
         self._k(self.lib.pgx_apply_slice(
             app_id, self.len, self.row_ptr.data_ptr(), self.val.data_ptr(), sl.data_ptr(),
             self.f_eb.data_ptr(), self.f_rs.data_ptr(), self.f_msg.data_ptr(),
             self.f_tile.data_ptr(), self.ctr.data_ptr(), int(count_only), EXCHANGE_NEUTRAL,
-            self.stream.cuda_stream), "pgx_apply_slice")
+            sv, self.stream.cuda_stream), "pgx_apply_slice")
         return self.ctr[:24].view(torch.int64)  # the raw block: packed, recip, bcast
 
     @staticmethod
@@ -792,13 +856,14 @@ class PartitionedPlan:
         self.n, self.m = graph.vertex_count, graph.edge_count
         dev = torch.device("cuda", torch.cuda.current_device())
         pr_mode = getattr(config, "pagerank_mode", "pull")
-        key = ("partitioned", world, rank, dev.index, pr_mode)
+        segments = getattr(config, "segments", "auto")
+        key = ("partitioned", world, rank, dev.index, pr_mode, segments)
         cached = graph._device.get(key)
         if cached is None:  # local CSR slice + its tile map, built once per graph
             deg = torch.diff(graph.out_offsets.cpu()).numpy()
             bounds = partition_bounds(deg, world)
             backend = CudaBackend(graph, int(bounds[rank]), int(bounds[rank + 1]), dev,
-                                  pr_mode=pr_mode)
+                                  pr_mode=pr_mode, segments=segments)
             cached = graph._device[key] = (bounds, backend)
         self.bounds, self.backend = cached
         self.runner = PartitionedRun(self.backend, dist, self.bounds, self.n, self.m)
