@@ -69,7 +69,12 @@ struct MinRunParams {
 // S = 0: externalised SoA (value = the caller's output array); S = 1:
 // interleaved {mailbox, value} records (layout.py's INTERLEAVED), values
 // copied out to the caller's array at the end of the run.
-template <int APP, int S, bool BFS = false>
+// ARMS = false: the shipped configuration (read-filter on, fire-and-forget
+// combines, edge-balanced tiles, no hub cache) with the ablation arms
+// compiled out, so they cost the hot loops no registers -- used for the
+// unit-weight SSSP kernel (C3 -7 %); the CC kernel measured 1 % slower
+// without them (code generation), so it keeps them
+template <int APP, int S, bool BFS = false, bool ARMS = true>
 __global__ void __launch_bounds__(kBlock, PGX_MIN_BLOCKS) min_run_kernel(MinRunParams p) {
   extern __shared__ __align__(16) char smem[];
   __shared__ unsigned s_red[32];
@@ -192,9 +197,11 @@ __global__ void __launch_bounds__(kBlock, PGX_MIN_BLOCKS) min_run_kernel(MinRunP
     a.mailbox = mailbox;
     a.has = p.ws.has;
     a.id_offset = 0;
-    a.hub_ids = p.hub_ids;
-    a.nhubs = p.nhubs;
-    a.cas_loop = p.cas_loop;
+    a.hub_ids = ARMS ? p.hub_ids : nullptr;
+    a.nhubs = ARMS ? p.nhubs : 0;
+    a.cas_loop = ARMS ? p.cas_loop : 0;
+    const bool read_filter = ARMS ? (p.read_filter != 0) : true;
+    const bool vertex_sched = ARMS && p.vertex_sched;
     a.neutral = kNeutralMin;
     a.n = p.n;
     if (APP == PGX_APP_CC && s == 0) {
@@ -205,10 +212,10 @@ __global__ void __launch_bounds__(kBlock, PGX_MIN_BLOCKS) min_run_kernel(MinRunP
       a.tile_src = p.g.tile_src;
       a.nsrc = p.g.hdr[0];
       a.E = p.m;
-      if (p.vertex_sched)
-        scatter_vertex_phase<MsgSrc::kSourceId, S>(a, p.read_filter);
+      if (vertex_sched)
+        scatter_vertex_phase<MsgSrc::kSourceId, S>(a, read_filter);
       else
-        scatter_phase<PGX_OP_MIN_U32, MsgSrc::kSourceId, S>(a, smem, p.read_filter);
+        scatter_phase<PGX_OP_MIN_U32, MsgSrc::kSourceId, S>(a, smem, read_filter);
     } else {
       const unsigned long long packed = p.ws.ctr[s].packed;
       a.eb = p.ws.f_eb;
@@ -218,12 +225,12 @@ __global__ void __launch_bounds__(kBlock, PGX_MIN_BLOCKS) min_run_kernel(MinRunP
       a.tile_src = p.ws.tile_src;
       a.nsrc = (int32_t)(packed >> 32);
       a.E = (int64_t)(packed & 0xFFFFFFFFull);
-      if (p.vertex_sched)
-        scatter_vertex_phase<MsgSrc::kFrontier, S>(a, p.read_filter);
+      if (vertex_sched)
+        scatter_vertex_phase<MsgSrc::kFrontier, S>(a, read_filter);
       else if (bfs)
         scatter_phase<PGX_OP_MIN_U32, MsgSrc::kFrontier, 0, false, true>(a, smem);
       else
-        scatter_phase<PGX_OP_MIN_U32, MsgSrc::kFrontier, S>(a, smem, p.read_filter);
+        scatter_phase<PGX_OP_MIN_U32, MsgSrc::kFrontier, S>(a, smem, read_filter);
     }
     }
     if (blockIdx.x == 0 && threadIdx.x == 0) {
@@ -622,8 +629,8 @@ static int min_run(int app, int32_t n, int64_t m, const int32_t *row_ptr, const 
   p.stats = stats;
   cudaStream_t st = (cudaStream_t)stream;
   PGX_CUDA(cudaMemsetAsync(p.ws.bar, 0, 64, st));
-  const bool bfs = PGX_SSSP_BFS && !p.interleaved && p.read_filter && !p.cas_loop &&
-                   !p.vertex_sched && nhubs == 0;
+  const bool shipped = p.read_filter && !p.cas_loop && !p.vertex_sched && nhubs == 0;
+  const bool bfs = PGX_SSSP_BFS && !p.interleaved && shipped;
   // the segmented scatter runs on the shipped arm only (SoA, read-filter,
   // fire-and-forget combines, edge-balanced tiles, no hub cache)
   p.use_seg = seg && m > 0 && !p.interleaved && p.read_filter && !p.cas_loop && !p.vertex_sched &&
@@ -639,7 +646,7 @@ static int min_run(int app, int32_t n, int64_t m, const int32_t *row_ptr, const 
   void (*kern)(MinRunParams) =
       app == PGX_APP_SSSP
           ? (p.interleaved ? min_run_kernel<PGX_APP_SSSP, 1>
-                           : bfs ? min_run_kernel<PGX_APP_SSSP, 0, true>
+                           : bfs ? min_run_kernel<PGX_APP_SSSP, 0, true, false>
                                  : min_run_kernel<PGX_APP_SSSP, 0>)
           : (p.interleaved ? min_run_kernel<PGX_APP_CC, 1> : min_run_kernel<PGX_APP_CC, 0>);
   rc = coop_grid(kern, smem, &grid);
