@@ -309,7 +309,7 @@ inline size_t run_ws_layout(int app, int64_t n, int64_t m, int32_t max_steps, Ru
     w.tile_src = (int32_t *)take(sizeof(int32_t) * (size_t)(ceil_div(m, kTile) + 2));
     w.snd[0] = (uint32_t *)take(sizeof(uint32_t) * (size_t)(n / 32 + 2));
     w.snd[1] = (uint32_t *)take(sizeof(uint32_t) * (size_t)(n / 32 + 2));
-    if (app == PGX_APP_CC) {
+    {  // CC and unit-weight SSSP
       w.sv[0] = (uint32_t *)take(sizeof(uint32_t) * (size_t)(n + 4));  // whole uint4 stores
       w.sv[1] = (uint32_t *)take(sizeof(uint32_t) * (size_t)(n + 4));
     }

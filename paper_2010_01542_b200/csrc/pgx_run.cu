@@ -86,7 +86,13 @@ __global__ void __launch_bounds__(kBlock, PGX_MIN_BLOCKS) min_run_kernel(MinRunP
   const unsigned gtid = blockIdx.x * blockDim.x + threadIdx.x;
 
   // ---- setup (algorithms.py:96-97 / 129-134) + superstep-0 senders ----
-  const bool use_sv = APP == PGX_APP_CC && p.use_seg;
+  // unit-weight SSSP on the shipped arm: the has-bit filter (scatter_phase);
+  // the host launches the BFS instantiation only for the default options
+  constexpr bool bfs = BFS && APP == PGX_APP_SSSP && S == 0;
+  // send values (the segmented scatter's messages): CC labels; for
+  // unit-weight SSSP any non-neutral value marks a sender (its messages are
+  // uniform: the has-bitmask is the result)
+  const bool use_sv = (APP == PGX_APP_CC || bfs) && p.use_seg;
   for (unsigned v = gtid; v < (unsigned)p.n; v += nthreads) {
     *slot<S>(val, v) = (APP == PGX_APP_CC) ? v : kNeutralMin;
     if (!BFS) *slot<S>(mailbox, v) = kNeutralMin;  // the bitmap kernel has no mailbox
@@ -122,12 +128,11 @@ __global__ void __launch_bounds__(kBlock, PGX_MIN_BLOCKS) min_run_kernel(MinRunP
   grid_sync<kArriveRed>(p.ws.bar, gen);
   if (APP == PGX_APP_SSSP && gtid == 0) {
     *slot<S>(val, p.source) = 0u;
-    if (p.row_ptr[p.source + 1] > p.row_ptr[p.source])  // the superstep-0 sender
-      p.ws.snd[0][p.source >> 5] = 1u << (p.source & 31);
+    if (p.row_ptr[p.source + 1] > p.row_ptr[p.source]) {  // the superstep-0 sender
+      if (use_sv) p.ws.sv[0][p.source] = 1u;
+      else p.ws.snd[0][p.source >> 5] = 1u << (p.source & 31);
+    }
   }
-  // unit-weight SSSP on the shipped arm: the has-bit filter (scatter_phase);
-  // the host launches the BFS instantiation only for the default options
-  constexpr bool bfs = BFS && APP == PGX_APP_SSSP && S == 0;
   if (gtid == 0) p.stats[PGX_STAT_HDR + 7] = (int64_t)globaltimer();
   unsigned sv_stale = 0u;  // bit b: sv[b] may hold stale senders (grid-uniform)
   bool front_skipped = false;  // the last apply built no frontier (grid-uniform)
@@ -187,8 +192,6 @@ __global__ void __launch_bounds__(kBlock, PGX_MIN_BLOCKS) min_run_kernel(MinRunP
       sp.out_neutral = kNeutralMin;
       if (APP == PGX_APP_CC && s == 0)
         seg_scatter_phase<kSegSourceId>(sp, smem);
-      else if (bfs)
-        seg_scatter_phase<kSegUniform>(sp, smem);
       else
         seg_scatter_phase<kSegLabel>(sp, smem);
     } else {
@@ -257,7 +260,7 @@ __global__ void __launch_bounds__(kBlock, PGX_MIN_BLOCKS) min_run_kernel(MinRunP
                       (p.seg_predict == 2 || (p.seg_predict == 1 && trend));
     const unsigned long long rb =
         bfs ? apply_min_phase<APP, 0, true>(p.row_ptr, val, mailbox, p.n, p.ws, &p.ws.ctr[s + 1],
-                                            smem, at_cap, (uint32_t)s + 1u, snd_out)
+                                            smem, at_cap, (uint32_t)s + 1u, snd_out, sv_out, skip)
             : apply_min_phase<APP, S>(p.row_ptr, val, mailbox, p.n, p.ws, &p.ws.ctr[s + 1], smem,
                                       at_cap, 0u, snd_out, sv_out, skip);
     const unsigned bc = block_sum<unsigned>((unsigned)(rb & 0xFFFFFFFFull), s_red);

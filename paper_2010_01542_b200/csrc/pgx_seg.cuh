@@ -55,7 +55,8 @@ __device__ __forceinline__ void cp_async_wait_all() {
 //   kSegLabel     the source sends sv[src], its send value of this
 //                 superstep (the neutral when it is not a sender: a no-op);
 //   kSegUniform   the sources flagged in the senders bitmap send `uniform`
-//                 (unit-weight SSSP).
+//                 (the first unit-weight SSSP form, kept for A/B builds: the
+//                 run kernel now feeds SSSP send values to kSegLabel).
 enum SegMsg { kSegSourceId = 0, kSegLabel = 1, kSegUniform = 2 };
 
 // work items: about kSegItemsPerCta per persistent CTA, and never more than
