@@ -330,6 +330,30 @@ int pgx_scatter_peer(int dense, const int32_t *col_idx, const int32_t *src_eb,
 int pgx_reset_touched(int32_t n, int32_t lo, int32_t hi, uint32_t *has_bits,
                       uint32_t *mailbox, uint32_t neutral, uintptr_t stream);
 
+/* Unit-weight SSSP over the peer exchange, as bitmaps (the partitioned form
+ * of the single-GPU has-bitmap filter): every message of a superstep is the
+ * same level, so a recipient needs only its has-bit.  pgx_scatter_peer_bfs:
+ * K1 over the rank's frontier filtering on its own full-width has-bitmap
+ * (the local filter copy); a clear bit is set locally and, when another
+ * rank owns the recipient, also in that owner's has-bitmap with a
+ * system-scope red.or over peer memory (peer_has[world] base pointers;
+ * owned bits use system scope too).  lo/hi: the rank's owned range of
+ * bitmap positions (whole 32-bit words).  pgx_apply_slice_bfs: the owned
+ * block's set bits are the recipients (has_block = the owned words);
+ * unreached ones take distance `level` and, with out-edges, join the next
+ * frontier (message level + 1); the block's words are then cleared
+ * (count_only: counted, left set). */
+int pgx_scatter_peer_bfs(const int32_t *col_idx, const int32_t *src_eb,
+                         const int32_t *src_rs, const void *src_msg,
+                         const int32_t *tile_src, int32_t nsrc, int64_t edges,
+                         uint32_t *has_bits, const uint64_t *peer_has,
+                         const int32_t *bounds, int32_t world, int32_t lo,
+                         int32_t hi, uintptr_t stream);
+int pgx_apply_slice_bfs(int32_t len, const int32_t *row_ptr, uint32_t *dist,
+                        uint32_t *has_block, int32_t *f_eb, int32_t *f_rs,
+                        uint32_t *f_msg, int32_t *tile_src, void *counters,
+                        int32_t count_only, uint32_t level, uintptr_t stream);
+
 /* Mailboxes other processes can map (CUDA IPC over NVLink / NVSwitch):
  * pgx_peer_alloc = cudaMalloc + its IPC handle (PGX_IPC_HANDLE_BYTES,
  * may be NULL); pgx_peer_open maps another process's handle (peer access

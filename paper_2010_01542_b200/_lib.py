@@ -46,7 +46,7 @@ EXPORTS = (
     "pgx_peer_close", "pgx_peer_free", "pgx_seg_workspace_bytes", "pgx_seg_max_items",
     "pgx_seg_count", "pgx_seg_build", "pgx_sssp_run_ex", "pgx_cc_run_ex",
     "pgx_gather_slice", "pgx_fold_spanning", "pgx_peer_enable", "pgx_seg_scatter",
-    "pgx_seg_count_ex", "pgx_seg_build_ex",
+    "pgx_seg_count_ex", "pgx_seg_build_ex", "pgx_scatter_peer_bfs", "pgx_apply_slice_bfs",
 )
 
 
@@ -96,6 +96,10 @@ _SIGS = {
     "pgx_scatter_peer": (ctypes.c_int, [ctypes.c_int, _p, _p, _p, _p, _i32, _p, _p, _i32, _i64,
                                         _p, _p, ctypes.c_uint32, _p, _p, _i32, _i32, _i32, _up]),
     "pgx_reset_touched": (ctypes.c_int, [_i32, _i32, _i32, _p, _p, ctypes.c_uint32, _up]),
+    "pgx_scatter_peer_bfs": (ctypes.c_int, [_p, _p, _p, _p, _p, _i32, _i64, _p, _p, _p, _i32,
+                                            _i32, _i32, _up]),
+    "pgx_apply_slice_bfs": (ctypes.c_int, [_i32, _p, _p, _p, _p, _p, _p, _p, _p, _i32,
+                                           ctypes.c_uint32, _up]),
     "pgx_peer_alloc": (ctypes.c_int, [_sz, _p, _p]),
     "pgx_peer_open": (ctypes.c_int, [_p, _p]),
     "pgx_peer_close": (ctypes.c_int, [_p]),

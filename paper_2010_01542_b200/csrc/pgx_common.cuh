@@ -149,6 +149,10 @@ __device__ __forceinline__ void red_min_u32_sys(uint32_t *p, uint32_t v) {
   asm volatile("red.relaxed.sys.global.min.u32 [%0], %1;" :: "l"(p), "r"(v) : "memory");
 }
 
+__device__ __forceinline__ void red_or_b32_sys(uint32_t *p, uint32_t v) {
+  asm volatile("red.relaxed.sys.global.or.b32 [%0], %1;" :: "l"(p), "r"(v) : "memory");
+}
+
 __device__ __forceinline__ void red_or_b32(uint32_t *p, uint32_t v) {
   asm volatile("red.relaxed.gpu.global.or.b32 [%0], %1;" :: "l"(p), "r"(v) : "memory");
 }

@@ -182,7 +182,20 @@ __device__ void scatter_phase(const ScatterArgs &a, char *smem, bool read_filter
           const int x = w[r];
           if (x != kInvalidEdge) PGX_COUNT(2);
           if (x != kInvalidEdge && !((hw[r] >> (x & 31)) & 1u)) {
-            red_or_b32(a.has + (x >> 5), 1u << (x & 31));
+            const uint32_t bit = 1u << (x & 31);
+            if (PEER && x >= a.lo && x < a.hi) {
+              red_or_b32_sys(a.has + (x >> 5), bit);  // peers set owned bits too
+            } else {
+              red_or_b32(a.has + (x >> 5), bit);
+              if (PEER) {
+                // the local bit is this rank's filter; the owner's bit is the
+                // exchange (peer_mb = the ranks' has-bitmaps here), over
+                // NVLink when the owner is another GPU
+                int o = 0;
+                while (o + 1 < a.world && x >= __ldg(a.bounds + o + 1)) o++;
+                red_or_b32_sys(a.peer_mb[o] + (x >> 5), bit);
+              }
+            }
             PGX_COUNT(1);
           }
         }

@@ -33,11 +33,11 @@ struct SliceCounters {       // device counters of one partitioned superstep
 #define PGX_SCATTER_MIN_BLOCKS PGX_MIN_BLOCKS
 #endif
 
-template <int OP, MsgSrc MS, bool PEER = false>
+template <int OP, MsgSrc MS, bool PEER = false, bool BFS = false>
 __global__ void __launch_bounds__(kBlock, PGX_SCATTER_MIN_BLOCKS) scatter_kernel(ScatterArgs a,
                                                                           int read_filter) {
   extern __shared__ __align__(16) char smem[];
-  scatter_phase<OP, MS, 0, PEER>(a, smem, read_filter != 0);
+  scatter_phase<OP, MS, 0, PEER, BFS>(a, smem, read_filter != 0);
   // the peer reds are performed at system scope before the kernel ends, so
   // the collective that follows it on the stream orders them before the
   // owners' apply
@@ -135,6 +135,70 @@ __global__ void __launch_bounds__(kBlock) pr_apply_slice_kernel(
 __global__ void __launch_bounds__(kBlock, PGX_MIN_BLOCKS) gather_slice_kernel(GatherArgs g) {
   extern __shared__ __align__(16) char smem[];
   gather_phase(g, smem);
+}
+
+// Unit-weight SSSP apply of the owned block after a bitmap exchange: the
+// recipients are the set bits of the rank's block of its has-bitmap (its
+// own scatter's and the peers' red.or); an unreached recipient takes
+// distance `level` and, with out-edges, joins the next frontier with
+// message level + 1.  The block's bits are consumed (cleared).
+__global__ void __launch_bounds__(kBlock) apply_slice_bfs_kernel(
+    int32_t len, const int32_t *__restrict__ row_ptr, uint32_t *val, uint32_t *has_block,
+    int32_t *f_eb, int32_t *f_rs, uint32_t *f_msg, int32_t *tile_src, SliceCounters *ctr,
+    int32_t count_only, uint32_t level) {
+  __shared__ unsigned long long s_w[33];
+  __shared__ unsigned long long s_gbase;
+  __shared__ unsigned long long s_red[32];
+  constexpr int kI = 4;
+  const int base = blockIdx.x * kBlock * kI;
+  int deg[kI], rs[kI];
+  unsigned long long mine = 0, recips = 0, bcast = 0;
+#pragma unroll
+  for (int j = 0; j < kI; j++) {
+    const int v = base + j * kBlock + threadIdx.x;
+    deg[j] = 0;
+    const bool got = v < len && ((has_block[v >> 5] >> (v & 31)) & 1u);
+    if (got) {
+      recips++;
+      if (!count_only && val[v] == kNeutralMin) {
+        val[v] = level;
+        bcast++;
+        rs[j] = row_ptr[v];
+        deg[j] = row_ptr[v + 1] - rs[j];
+        if (deg[j] > 0) mine += (1ull << 32) | (unsigned long long)deg[j];
+      }
+    }
+  }
+  unsigned long long total;
+  unsigned long long run = block_excl_scan_u64(mine, s_w, &total);
+  if (total) {
+    if (threadIdx.x == 0) s_gbase = atomicAdd(&ctr->packed, total);
+    __syncthreads();
+    run += s_gbase;
+#pragma unroll
+    for (int j = 0; j < kI; j++) {
+      if (deg[j] > 0) {
+        const unsigned pos = (unsigned)(run >> 32);
+        const int eb = (int)(run & 0xFFFFFFFFull);
+        f_eb[pos] = eb;
+        f_rs[pos] = rs[j];
+        f_msg[pos] = level + 1u;
+        for (int64_t t = ((int64_t)eb + kTile - 1) / kTile; t * kTile < (int64_t)eb + deg[j]; t++)
+          tile_src[t] = (int)pos;
+        run += (1ull << 32) | (unsigned long long)deg[j];
+      }
+    }
+  }
+  recips = block_sum<unsigned long long>(recips, s_red);
+  if (threadIdx.x == 0 && recips) atomicAdd(&ctr->recip, recips);
+  bcast = block_sum<unsigned long long>(bcast, s_red);
+  if (threadIdx.x == 0 && bcast) atomicAdd(&ctr->bcast, bcast);
+}
+
+// the owned block's bits consumed (after every thread read them)
+__global__ void clear_words_kernel(uint32_t *w, int32_t count) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < count; i += gridDim.x * blockDim.x)
+    w[i] = 0u;
 }
 
 // K1s on a rank's slice: the destination-segmented scatter of the rank's
@@ -252,6 +316,10 @@ __global__ void reset_touched_kernel(uint32_t *has, int32_t n, int32_t lo, int32
        wi += gridDim.x * blockDim.x) {
     if (!has[wi]) continue;
     uint32_t rem = foreign_bits(has, wi, n, lo, hi);
+    // only words with foreign bits (owned ranges are whole words): an owned
+    // word may already be receiving the peers' next-superstep bits (the
+    // unit-weight SSSP bitmap exchange) and is never written here
+    if (!rem) continue;
     has[wi] = 0u;
     while (rem) {
       const int b = __ffs(rem) - 1;
@@ -396,6 +464,71 @@ int pgx_scatter_peer(int dense, const int32_t *col_idx, const int32_t *src_eb,
     PGX_CUDA(cudaFuncSetAttribute(scatter_kernel<PGX_OP_MIN_U32, MsgSrc::kSourceId, true>,
                                   cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     scatter_kernel<PGX_OP_MIN_U32, MsgSrc::kSourceId, true><<<grid, kBlock, smem, st>>>(a, rf);
+  }
+  PGX_CUDA(cudaGetLastError());
+  return PGX_OK;
+}
+
+int pgx_scatter_peer_bfs(const int32_t *col_idx, const int32_t *src_eb, const int32_t *src_rs,
+                         const void *src_msg, const int32_t *tile_src, int32_t nsrc,
+                         int64_t edges, uint32_t *has_bits, const uint64_t *peer_has,
+                         const int32_t *bounds, int32_t world, int32_t lo, int32_t hi,
+                         uintptr_t stream) {
+  if (edges < 0 || edges > INT32_MAX || nsrc < 0) return fail(PGX_EINVAL, "bad sizes");
+  if (world < 1 || lo < 0 || hi < lo || !peer_has || !bounds)
+    return fail(PGX_EINVAL, "bad peer arguments");
+  if (edges == 0) return PGX_OK;
+  if (!col_idx || !src_eb || !src_rs || !src_msg || !tile_src || !has_bits)
+    return fail(PGX_EINVAL, "null scatter pointer");
+  ScatterArgs a;
+  memset(&a, 0, sizeof a);
+  a.col = col_idx;
+  a.eb = src_eb;
+  a.rs = src_rs;
+  a.msg = src_msg;
+  a.tile_src = tile_src;
+  a.nsrc = nsrc;
+  a.E = edges;
+  a.mailbox = nullptr;
+  a.has = has_bits;
+  a.neutral = kNeutralMin;
+  a.n = INT32_MAX;
+  a.peer_mb = reinterpret_cast<uint32_t *const *>(peer_has);
+  a.bounds = bounds;
+  a.world = world;
+  a.lo = lo;
+  a.hi = hi;
+  const int64_t tiles = ceil_div(edges, kTile);
+  int sms = 148, dev = 0;
+  if (cudaGetDevice(&dev) == cudaSuccess)
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(ceil_div(tiles, kWarps),
+                                                               (int64_t)sms * PGX_SCATTER_MIN_BLOCKS));
+  cudaStream_t st = (cudaStream_t)stream;
+  const size_t smem = scatter_smem(PGX_OP_MIN_U32);
+  auto k = scatter_kernel<PGX_OP_MIN_U32, MsgSrc::kFrontier, true, true>;
+  PGX_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  k<<<grid, kBlock, smem, st>>>(a, 1);
+  PGX_CUDA(cudaGetLastError());
+  return PGX_OK;
+}
+
+int pgx_apply_slice_bfs(int32_t len, const int32_t *row_ptr, uint32_t *dist,
+                        uint32_t *has_block, int32_t *f_eb, int32_t *f_rs, uint32_t *f_msg,
+                        int32_t *tile_src, void *counters, int32_t count_only, uint32_t level,
+                        uintptr_t stream) {
+  if (len < 0 || !counters || (len && (!row_ptr || !dist || !has_block)))
+    return fail(PGX_EINVAL, "bad apply_slice_bfs arguments");
+  if (!len) return PGX_OK;
+  cudaStream_t st = (cudaStream_t)stream;
+  const int grid = (int)ceil_div(len, kBlock * 4);
+  apply_slice_bfs_kernel<<<grid, kBlock, 0, st>>>(len, row_ptr, dist, has_block, f_eb, f_rs,
+                                                  f_msg, tile_src, (SliceCounters *)counters,
+                                                  count_only, level);
+  if (!count_only) {
+    const int words = (int)ceil_div(len, 32);
+    clear_words_kernel<<<(int)std::min<int64_t>(ceil_div(words, 256), 148 * 8), 256, 0, st>>>(
+        has_block, words);
   }
   PGX_CUDA(cudaGetLastError());
   return PGX_OK;

@@ -525,47 +525,52 @@ class CudaBackend:
 
     # ---- fused peer exchange ----
     def peer_handle(self):
-        """This rank's mappable mailbox (allocated once), or None."""
+        """This rank's mappable mailbox and has-bitmap (allocated once: the
+        min exchange and the unit-weight SSSP bitmap exchange), or None."""
         try:
             if self._peer_mb is None or self._peer_mb.n != self.npad:
                 self._peer_mb = PeerMailbox(self._lib, self.lib, self.npad, self.device)
+                self._peer_has = PeerMailbox(self._lib, self.lib, self.npad // 32 + 2,
+                                             self.device)
         except Exception:
             return None
         return {"pid": os.getpid(), "device": self.device.index, "ptr": self._peer_mb.ptr,
-                "handle": self._peer_mb.handle}
+                "handle": self._peer_mb.handle, "has_ptr": self._peer_has.ptr,
+                "has_handle": self._peer_has.handle}
 
     def close_peers(self):
         CudaBackend._close_all(self.lib, self._opened)  # in place: the finalizer's list
         self._peer_sig = None
 
+    def _map(self, h, ptr_key, handle_key) -> int:
+        if h["pid"] == os.getpid():
+            if h["device"] != self.device.index:
+                with torch.cuda.device(self.device):
+                    self._lib.check(self.lib.pgx_peer_enable(h["device"]), "pgx_peer_enable")
+            return h[ptr_key]
+        p = ctypes.c_void_p()
+        with torch.cuda.device(self.device):
+            self._lib.check(self.lib.pgx_peer_open(h[handle_key], ctypes.byref(p)),
+                            "pgx_peer_open")
+        self._opened.append(int(p.value))
+        return int(p.value)
+
     def open_peers(self, handles) -> bool:
-        """Device array of every rank's mailbox base: IPC-mapped, or the raw
-        pointer for ranks that are threads of this process (peer access
-        enabled when they sit on another GPU)."""
+        """Device arrays of every rank's mailbox and has-bitmap bases:
+        IPC-mapped, or the raw pointers for ranks that are threads of this
+        process (peer access enabled when they sit on another GPU)."""
         sig = tuple((h["pid"], h["ptr"]) for h in handles)
         if sig == self._peer_sig:
             return True
         self.close_peers()
-        ptrs = []
         try:
-            for h in handles:
-                if h["pid"] == os.getpid():
-                    if h["device"] != self.device.index:
-                        with torch.cuda.device(self.device):
-                            self._lib.check(self.lib.pgx_peer_enable(h["device"]),
-                                            "pgx_peer_enable")
-                    ptrs.append(h["ptr"])
-                    continue
-                p = ctypes.c_void_p()
-                with torch.cuda.device(self.device):
-                    self._lib.check(self.lib.pgx_peer_open(h["handle"], ctypes.byref(p)),
-                                    "pgx_peer_open")
-                self._opened.append(int(p.value))
-                ptrs.append(int(p.value))
+            ptrs = [self._map(h, "ptr", "handle") for h in handles]
+            has_ptrs = [self._map(h, "has_ptr", "has_handle") for h in handles]
         except Exception:
             self.close_peers()
             return False
         self._peer_ptrs = torch.tensor(ptrs, dtype=torch.int64, device=self.device)
+        self._peer_has_ptrs = torch.tensor(has_ptrs, dtype=torch.int64, device=self.device)
         self._peer_sig = sig
         return True
 
@@ -616,10 +621,12 @@ class CudaBackend:
         self.app = app
         if self.peer_active:
             self.mailbox = self._peer_mb.tensor
+            self.has = self._peer_has.tensor   # peers set bits in it (SSSP)
         else:
             self.mailbox = torch.empty(self.npad, dtype=torch.int32, device=self.device)
         self.mailbox.fill_(EXCHANGE_NEUTRAL)
         self.has.zero_()
+        self._level = 0  # supersteps scattered (unit-weight SSSP: the next level)
         self.val = torch.empty(max(self.len, 1), dtype=torch.int32, device=self.device)
         # CC send values (K1s): the label a sender sends, -1 (UINT32_MAX) otherwise
         self.sv = torch.full((max(self.len, 1),), -1, dtype=torch.int32, device=self.device) \
@@ -656,9 +663,12 @@ class CudaBackend:
         if self._last == "dense":  # every foreign slot holds a stale partial
             self.mailbox[:self.blo].fill_(EXCHANGE_NEUTRAL)
             self.mailbox[self.blo + self.block:].fill_(EXCHANGE_NEUTRAL)
-        # sparse: the compaction reset the foreign touched slots
+        # sparse: the compaction reset the foreign touched slots.  Foreign
+        # has-words only: the owned words were consumed by the apply, and a
+        # peer may already be setting next-superstep bits in them (SSSP)
         if self._last is not None:
-            self.has.zero_()
+            self.has[:self.blo // 32].zero_()
+            self.has[(self.blo + self.block) // 32:].zero_()
 
     def exchanged(self, kind: str):
         self._last = kind
@@ -708,6 +718,17 @@ class CudaBackend:
             src = (self.f_eb.data_ptr(), self.f_rs.data_ptr(), None, 0,
                    self.f_msg.data_ptr(), self.f_tile.data_ptr(), self.nsrc, self.E)
             self._scattered = self.E
+        self._level += 1
+        if peer and self.app == "sssp":
+            # unit-weight SSSP: the exchange is the owners' has-bits
+            rc = L.pgx_scatter_peer_bfs(self.col.data_ptr(), self.f_eb.data_ptr(),
+                                        self.f_rs.data_ptr(), self.f_msg.data_ptr(),
+                                        self.f_tile.data_ptr(), self.nsrc, self.E,
+                                        self.has.data_ptr(), self._peer_has_ptrs.data_ptr(),
+                                        self._pbounds.data_ptr(), self.world, self.blo,
+                                        self.blo + self.block, st)
+            self._k(rc, "pgx_scatter_peer_bfs")
+            return
         if peer:
             rc = L.pgx_scatter_peer(int(dense), self.col.data_ptr(), *src,
                                     self.mailbox.data_ptr(), self.has.data_ptr(),
@@ -725,6 +746,15 @@ class CudaBackend:
         (decode_counts) -- no host synchronisation."""
         self.ctr.zero_()
         app_id = self._lib.PGX_APP_CC if app == "components" else self._lib.PGX_APP_SSSP
+        own = self.has[self.blo // 32:(self.blo + self.block) // 32]
+        if app == "sssp" and self._last == "peer":
+            # the bitmap exchange: the owned block's bits are the recipients
+            self._k(self.lib.pgx_apply_slice_bfs(
+                self.len, self.row_ptr.data_ptr(), self.val.data_ptr(), own.data_ptr(),
+                self.f_eb.data_ptr(), self.f_rs.data_ptr(), self.f_msg.data_ptr(),
+                self.f_tile.data_ptr(), self.ctr.data_ptr(), int(count_only), self._level,
+                self.stream.cuda_stream), "pgx_apply_slice_bfs", 1 if count_only else 2)
+            return self.ctr[:24].view(torch.int64)
         sl = self.mailbox[self.blo:self.blo + self.len]
         sv = None
         if self.sv is not None:
@@ -735,6 +765,10 @@ class CudaBackend:
             self.f_eb.data_ptr(), self.f_rs.data_ptr(), self.f_msg.data_ptr(),
             self.f_tile.data_ptr(), self.ctr.data_ptr(), int(count_only), EXCHANGE_NEUTRAL,
             sv, self.stream.cuda_stream), "pgx_apply_slice")
+        # the owned has-words (set by this rank's own scatter) are consumed
+        # here, before the counters' all-gather lets any peer start the next
+        # superstep
+        own.zero_()
         return self.ctr[:24].view(torch.int64)  # the raw block: packed, recip, bcast
 
     @staticmethod

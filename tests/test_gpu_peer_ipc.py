@@ -90,5 +90,6 @@ def test_peer_exchange_across_processes(tmp_path):
             assert modes == {"peer"}
         else:  # dense collective for the big supersteps, peer for the tail
             assert "peer" in modes and modes <= {"dense", "sparse", "peer"}
-        assert opened == world - 1  # the other rank's mailbox came through IPC
+        # the other rank's mailbox and has-bitmap came through IPC
+        assert opened == 2 * (world - 1)
     assert np.array_equal(out["api"], O.run_cc(n, off, tgt).values.astype(np.int64))
