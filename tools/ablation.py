@@ -24,11 +24,12 @@ ARMS = [  # name, read_filter, cas_loop, vertex_sched, layout
     ("final (externalised + edge tiles + hybrid)", 1, 0, 0, EX),
     ("final with the interleaved layout", 1, 0, 0, IL),
     ("final, red.min without read-filter", 0, 0, 0, EX),
+    ("final, K1 only (no segmented scatter)", 1, 0, 0, EX, "off"),
 ]
 FINAL = 4
 
 
-def set_arm(rf, cas, vs, layout):
+def set_arm(rf, cas, vs, layout, segments="auto"):
     _lib.set_option(_lib.PGX_OPT_READ_FILTER, rf)
     _lib.set_option(_lib.PGX_OPT_CAS_LOOP, cas)
     _lib.set_option(_lib.PGX_OPT_VERTEX_SCHED, vs)
@@ -58,7 +59,8 @@ def main():
         order = [ARMS[FINAL]] + [a for i, a in enumerate(ARMS) if i != FINAL]
         for name, *opts in order:   # final first: the reference arm
             set_arm(*opts)
-            plan = pgx.plan_run(g, prog)
+            seg = opts[4] if len(opts) > 4 else "auto"
+            plan = pgx.plan_run(g, prog, pgx.EngineConfig(segments=seg))
             ms, rep = time_plan(plan, prog, reps)
             if ref is None:
                 ref = rep
