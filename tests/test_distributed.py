@@ -132,3 +132,21 @@ def test_partition_bounds_edge_balanced():
     for r in range(2):
         load = int((deg[b[r]:b[r + 1]] + 1).sum())
         assert load * 2 < total + int((deg + 1).max()) * 2
+
+
+def test_owner_blocked_layout():
+    """Padded owner blocks: block = the largest range rounded up to 64;
+    vertex v of owner r sits at r * B + (v - lo_r); positions are ordered
+    like the vertices and never land in a block's padding."""
+    from paper_2010_01542_b200.distributed import owner_block, padded_positions
+    bounds = np.array([0, 70, 75, 200], dtype=np.int64)
+    B = owner_block(bounds)
+    assert B == 128 and B % 64 == 0
+    v = torch.arange(200, dtype=torch.int32)
+    pos = padded_positions(v, bounds, B, chunk=17).numpy()
+    owner = np.searchsorted(bounds[1:-1], np.arange(200), side="right")
+    assert np.array_equal(pos, owner * B + np.arange(200) - bounds[owner])
+    assert np.all(np.diff(pos) > 0)
+    sizes = np.diff(bounds)
+    assert np.all(pos - owner * B < sizes[owner])
+    assert owner_block(np.array([0, 0, 0])) == 64       # empty graph: one line
