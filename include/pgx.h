@@ -134,7 +134,10 @@ typedef struct PgxSegIndex {
   int32_t reserved;
   const int32_t *ent_src;   /* [nent+4] source of each entry (16-byte
                                aligned; 4 slots of padding)                */
-  const int32_t *ent_eb;    /* [nent+1] first edge (segment order); [nent] = m */
+  const int32_t *ent_eb;    /* [nent+1] first edge (segment order); [nent] = m
+                               (build output; the scatter finds entries from
+                               col16's flags and does not read it: may be
+                               NULL / freed for a run)                     */
   const uint16_t *col16;    /* [m+256]  shared-memory slot of (destination -
                                segment base), bank-swizzled; bit 15 flags
                                the first edge of an entry                  */

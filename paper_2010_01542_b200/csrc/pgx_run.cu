@@ -597,7 +597,7 @@ static int min_run(int app, int32_t n, int64_t m, const int32_t *row_ptr, const 
     return fail(PGX_EINVAL, "hub count must be in [0, pgx_hub_capacity()]");
   if (seg) {
     if (seg->seg_log2 < 5 || seg->seg_log2 > kSegMaxLog2 || seg->nent < 1 || seg->nent > m ||
-        seg->nitems < 1 || !seg->ent_src || !seg->ent_eb || !seg->col16 || !seg->tile_ent ||
+        seg->nitems < 1 || !seg->ent_src || !seg->col16 || !seg->tile_ent ||
         !seg->items || reinterpret_cast<uintptr_t>(seg->items) % 16 ||
         reinterpret_cast<uintptr_t>(seg->ent_src) % 16 ||
         reinterpret_cast<uintptr_t>(seg->col16) % 16)

@@ -607,8 +607,12 @@ class CudaBackend:
                                                  ws.data_ptr(), ws.numel(),
                                                  *(a.data_ptr() for a in arrays),
                                                  ctypes.byref(nitems), 0, sp), "pgx_seg_build_ex")
-        self._seg = (self._lib.PgxSegIndex(L, ne, int(nitems.value), 0,
-                                           *(a.data_ptr() for a in arrays)),
+        # ent_eb (arrays[1]) is a build output the scatter never reads: freed
+        ent_src, _, col16, tile_ent, items = arrays
+        arrays = (ent_src, col16, tile_ent, items)
+        self._seg = (self._lib.PgxSegIndex(L, ne, int(nitems.value), 0, ent_src.data_ptr(), None,
+                                           col16.data_ptr(), tile_ent.data_ptr(),
+                                           items.data_ptr()),
                      arrays, torch.zeros(1, dtype=torch.int32, device=dev))
         return self._seg
 

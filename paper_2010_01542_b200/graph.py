@@ -106,9 +106,12 @@ class DeviceCSR:
                                          tile_ent.data_ptr(), items.data_ptr(),
                                          ctypes.byref(nitems), 0, sp), "pgx_seg_build")
             del ws
-        self.seg_arrays = (ent_src, ent_eb, col16, tile_ent, items)
+        # ent_eb (4 B per entry, 3.5 GB on C5) is a build output the scatter
+        # never reads (entry boundaries are col16's flags): freed here
+        del ent_eb
+        self.seg_arrays = (ent_src, col16, tile_ent, items)
         self.seg = _lib.PgxSegIndex(L, ne, int(nitems.value), 0, ent_src.data_ptr(),
-                                    ent_eb.data_ptr(), col16.data_ptr(), tile_ent.data_ptr(),
+                                    None, col16.data_ptr(), tile_ent.data_ptr(),
                                     items.data_ptr())
 
     def ensure_hubs(self, stream=None) -> None:
