@@ -33,7 +33,7 @@
 extern "C" {
 #endif
 
-#define PGX_ABI_VERSION 4
+#define PGX_ABI_VERSION 5
 
 #define PGX_OK 0
 #define PGX_EINVAL (-1)   /* bad argument / unsupported configuration */
@@ -84,7 +84,10 @@ const char *pgx_last_error(void);
 #define PGX_OPT_SEG_PREDICT 6   /* CC: the apply builds no frontier when the next superstep is
                                    predicted segmented, which then runs segmented (0 never,
                                    1 predicted -- default, 2 after every segmented superstep) */
-#define PGX_OPT_COUNT 7
+#define PGX_OPT_PULL_MIN_EDGES 7 /* unit-weight SSSP with an in-CSR (pgx_sssp_run_dir): bottom-up
+                                   superstep when its senders hold at least m * value / 1024 edges
+                                   (0 = every superstep after the first, 1025 = never; default 128) */
+#define PGX_OPT_COUNT 8
 
 /* PGX_OPT_LAYOUT values (LayoutMode, layout.py:31-33).  EXTERNALISED is the
  * default SoA (value[], mailbox[] apart).  INTERLEAVED keeps one {mailbox,
@@ -229,6 +232,20 @@ int pgx_sssp_run_ex(int32_t n, int64_t m, const int32_t *row_ptr,
                     const PgxSegIndex *seg, int32_t source,
                     int32_t max_supersteps, uint32_t *dist, void *run_ws,
                     size_t run_ws_bytes, int64_t *stats, uintptr_t stream);
+/* unit-weight SSSP, direction-optimising: as pgx_sssp_run_ex (seg may be
+ * NULL), plus the in-CSR (in_row_ptr / in_col: the transpose of (row_ptr,
+ * col_idx), rows sorted by source id).  A superstep whose senders hold at
+ * least PGX_OPT_PULL_MIN_EDGES of the edges runs bottom-up: every vertex
+ * tests its in-edges against the senders bitmap until the first sender
+ * (the has-message bitmask is the superstep's whole result, every message
+ * of a superstep being equal).  Results and statistics are identical to
+ * pgx_sssp_run. */
+int pgx_sssp_run_dir(int32_t n, int64_t m, const int32_t *row_ptr,
+                     const int32_t *col_idx, const void *graph_ws,
+                     const PgxSegIndex *seg, const int32_t *in_row_ptr,
+                     const int32_t *in_col, int32_t source,
+                     int32_t max_supersteps, uint32_t *dist, void *run_ws,
+                     size_t run_ws_bytes, int64_t *stats, uintptr_t stream);
 int pgx_cc_run_ex(int32_t n, int64_t m, const int32_t *row_ptr,
                   const int32_t *col_idx, const void *graph_ws,
                   const PgxSegIndex *seg, int32_t max_supersteps,

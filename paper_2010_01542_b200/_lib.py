@@ -16,7 +16,7 @@ from .errors import ConfigError, ExecutionError
 PKG_DIR = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.environ.get("PGX_LIB") or os.path.join(PKG_DIR, "libpgx.so")
 
-PGX_ABI_VERSION = 4
+PGX_ABI_VERSION = 5
 PGX_OK, PGX_EINVAL, PGX_ECUDA, PGX_ENOMEM = 0, -1, -2, -3
 PGX_APP_PAGERANK, PGX_APP_CC, PGX_APP_SSSP, PGX_APP_PAGERANK_PULL = 0, 1, 2, 3
 PGX_OP_MIN_U32, PGX_OP_SUM_F64 = 0, 1
@@ -25,6 +25,7 @@ PGX_OPT_READ_FILTER, PGX_OPT_CTAS_PER_SM, PGX_OPT_CAS_LOOP, PGX_OPT_VERTEX_SCHED
 PGX_OPT_LAYOUT = 4
 PGX_OPT_SEG_MIN_EDGES = 5
 PGX_OPT_SEG_PREDICT = 6
+PGX_OPT_PULL_MIN_EDGES = 7
 PGX_SEG_LOG2_DEFAULT = 14
 PGX_IPC_HANDLE_BYTES = 64
 PGX_LAYOUT_EXTERNALISED, PGX_LAYOUT_INTERLEAVED = 0, 1
@@ -47,6 +48,7 @@ EXPORTS = (
     "pgx_seg_count", "pgx_seg_build", "pgx_sssp_run_ex", "pgx_cc_run_ex",
     "pgx_gather_slice", "pgx_fold_spanning", "pgx_peer_enable", "pgx_seg_scatter",
     "pgx_seg_count_ex", "pgx_seg_build_ex", "pgx_scatter_peer_bfs", "pgx_apply_slice_bfs",
+    "pgx_sssp_run_dir",
 )
 
 
@@ -125,6 +127,8 @@ _SIGS = {
                                      _p, _p, _p, _i32, _up]),
     "pgx_sssp_run_ex": (ctypes.c_int, [_i32, _i64, _p, _p, _p, _p, _i32, _i32, _p, _p, _sz, _p,
                                        _up]),
+    "pgx_sssp_run_dir": (ctypes.c_int, [_i32, _i64, _p, _p, _p, _p, _p, _p, _i32, _i32, _p, _p,
+                                        _sz, _p, _up]),
     "pgx_cc_run_ex": (ctypes.c_int, [_i32, _i64, _p, _p, _p, _p, _i32, _p, _p, _sz, _p, _up]),
     "pgx_rmat_keys": (ctypes.c_int, [_i32, _i64, _i64, _f64, _f64, _f64, _u64, _i32,
                                      _i64, _i64, _p, _i64, _p, _up]),

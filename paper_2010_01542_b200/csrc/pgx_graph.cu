@@ -16,6 +16,7 @@ int g_opt[PGX_OPT_COUNT] = {
     /* PGX_OPT_LAYOUT */ PGX_LAYOUT_EXTERNALISED,
     /* PGX_OPT_SEG_MIN_EDGES */ 256,  // segmented scatter from m/4 sender edges
     /* PGX_OPT_SEG_PREDICT */ 1,      // skip the frontier before predicted segmented supersteps
+    /* PGX_OPT_PULL_MIN_EDGES */ 128, // unit-weight SSSP bottom-up from m/8 sender edges
 };
 
 namespace {

@@ -31,6 +31,7 @@
 #include "pgx_apply.cuh"
 #include "pgx_common.cuh"
 #include "pgx_gather.cuh"
+#include "pgx_pull.cuh"
 #include "pgx_scatter.cuh"
 #include "pgx_seg.cuh"
 
@@ -64,6 +65,12 @@ struct MinRunParams {
   int32_t use_seg;
   int64_t seg_min_edges;
   int32_t seg_predict;  // PGX_OPT_SEG_PREDICT
+  // bottom-up supersteps of unit-weight SSSP (pgx_pull.cuh) for supersteps
+  // whose senders hold at least pull_min_edges edges; use_pull = 0: none
+  const int32_t *in_row_ptr;
+  const int32_t *in_col;
+  int32_t use_pull;
+  int64_t pull_min_edges;
 };
 
 // S = 0: externalised SoA (value = the caller's output array); S = 1:
@@ -125,7 +132,14 @@ __global__ void __launch_bounds__(kBlock, PGX_MIN_BLOCKS) min_run_kernel(MinRunP
       p.ws.ctr[0].bcast = (unsigned)p.n;  // every vertex broadcasts its id
     }
   }
-  grid_sync<kArriveRed>(p.ws.bar, gen);
+  // the unit-weight SSSP kernel reads its per-superstep counters through
+  // shared memory (grid_sync_bc); s_bc[0] = packed counts of the next
+  // superstep's senders, s_bc[1] = recipients word, s_bc[2..3] scratch
+  __shared__ unsigned long long s_bc[4];
+  if constexpr (bfs)
+    grid_sync_bc(p.ws.bar, gen, &p.ws.ctr[0].packed, nullptr, s_bc);
+  else
+    grid_sync<kArriveRed>(p.ws.bar, gen);
   if (APP == PGX_APP_SSSP && gtid == 0) {
     *slot<S>(val, p.source) = 0u;
     if (p.row_ptr[p.source + 1] > p.row_ptr[p.source]) {  // the superstep-0 sender
@@ -140,7 +154,7 @@ __global__ void __launch_bounds__(kBlock, PGX_MIN_BLOCKS) min_run_kernel(MinRunP
 
   for (int s = 0;; s++) {
     // ---- scatter(s): senders push along out-edges into the mailbox ----
-    const unsigned long long packed_s = p.ws.ctr[s].packed;
+    const unsigned long long packed_s = bfs ? s_bc[0] : p.ws.ctr[s].packed;
     const int64_t edges_s = (APP == PGX_APP_CC && s == 0) ? p.m
                                                           : (int64_t)(packed_s & 0xFFFFFFFFull);
     // a segmented superstep needs exact send values: after a K1 superstep
@@ -149,7 +163,11 @@ __global__ void __launch_bounds__(kBlock, PGX_MIN_BLOCKS) min_run_kernel(MinRunP
     // (after an apply that predicted a segmented superstep and built no
     // frontier, the segmented pass runs whatever the edge count: a wrong
     // guess costs at most one dense pass; the send values are exact)
-    const bool seg_s = p.use_seg && edges_s > 0 &&
+    // unit-weight SSSP: a superstep whose senders hold many edges runs
+    // bottom-up (pgx_pull.cuh) -- the same has-bitmask from the receivers
+    const bool pull_s = bfs && p.use_pull && s >= 1 && edges_s > 0 &&
+                        edges_s >= p.pull_min_edges;
+    const bool seg_s = !pull_s && p.use_seg && edges_s > 0 &&
                        (edges_s >= p.seg_min_edges || front_skipped) &&
                        !((sv_stale >> (s & 1)) & 1u);
     if (p.use_seg && s >= 1 && (p.ws.ctr[s - 1].packed >> 32) != 0ull) {
@@ -175,7 +193,64 @@ __global__ void __launch_bounds__(kBlock, PGX_MIN_BLOCKS) min_run_kernel(MinRunP
           if (nx[wi]) nx[wi] = 0u;
       }
     }
-    if (seg_s) {
+    if (pull_s) {
+      if constexpr (bfs) {
+        PullArgs pa;
+        pa.in_row_ptr = p.in_row_ptr;
+        pa.in_col = p.in_col;
+        pa.dist = val;
+        pa.n = p.n;
+        pa.m = p.m;
+        pa.level = (uint32_t)s;
+        pa.snd = p.ws.snd[0];
+        pa.has = p.ws.has;
+        pa.q_eb = p.ws.f_eb;  // the frontier of superstep s is not read
+        pa.q_rs = p.ws.f_rs;
+        pa.q_v = reinterpret_cast<uint32_t *>(p.ws.f_msg);
+        pa.q_tile = p.ws.tile_src;
+        pa.q_ctr = p.ws.misc;
+#ifndef PGX_PULL_TIMING
+#define PGX_PULL_TIMING 0
+#endif
+        const uint64_t t0 = PGX_PULL_TIMING ? globaltimer() : 0;
+        pull_senders_phase(pa);
+        if (PGX_PULL_TIMING && gtid == 0) {
+          p.ws.misc[2] = ~0ull;
+          p.ws.misc[3] = 0ull;
+          p.ws.misc[4] = ~0ull;
+          p.ws.misc[5] = 0ull;
+        }
+        grid_sync<kArriveRed>(p.ws.bar, gen);
+        const uint64_t t1 = PGX_PULL_TIMING ? globaltimer() : 0;
+        pull_probe_phase(pa);
+        if (PGX_PULL_TIMING) {  // debug build: spread of the CTAs' phase-B finish times
+          __syncthreads();
+          if (threadIdx.x == 0) {
+            atomicMin(&p.ws.misc[2], (unsigned long long)globaltimer());
+            atomicMax(&p.ws.misc[3], (unsigned long long)globaltimer());
+          }
+        }
+        grid_sync_bc(p.ws.bar, gen, pa.q_ctr, nullptr, s_bc + 2);
+        const uint64_t t2 = PGX_PULL_TIMING ? globaltimer() : 0;
+        pull_remainder_phase(pa, s_bc[2], smem);
+        if (PGX_PULL_TIMING) {  // debug build (tools): phase times of the pull superstep
+          __syncthreads();
+          if (threadIdx.x == 0) {
+            atomicMin(&p.ws.misc[4], (unsigned long long)globaltimer());
+            atomicMax(&p.ws.misc[5], (unsigned long long)globaltimer());
+          }
+          grid_sync<kArriveRed>(p.ws.bar, gen);
+          if (gtid == 0)
+            printf("pull s=%d A=%.1f B=%.1f (first CTA done %.1f, last %.1f) C=%.1f us "
+                   "(first CTA done %.1f, last %.1f), remainder %u entries %u edges\n", s,
+                   (t1 - t0) * 1e-3, (t2 - t1) * 1e-3, (p.ws.misc[2] - t1) * 1e-3,
+                   (p.ws.misc[3] - t1) * 1e-3, (globaltimer() - t2) * 1e-3,
+                   ((long long)p.ws.misc[4] - (long long)t2) * 1e-3,
+                   ((long long)p.ws.misc[5] - (long long)t2) * 1e-3,
+                   (unsigned)(*pa.q_ctr >> 32), (unsigned)(*pa.q_ctr & 0xFFFFFFFFull));
+        }
+      }
+    } else if (seg_s) {
       // dense superstep: the segmented shared-memory scatter (pgx_seg.cuh)
       SegPass sp;
       sp.ix = p.seg;
@@ -220,7 +295,7 @@ __global__ void __launch_bounds__(kBlock, PGX_MIN_BLOCKS) min_run_kernel(MinRunP
       else
         scatter_phase<PGX_OP_MIN_U32, MsgSrc::kSourceId, S>(a, smem, read_filter);
     } else {
-      const unsigned long long packed = p.ws.ctr[s].packed;
+      const unsigned long long packed = bfs ? packed_s : p.ws.ctr[s].packed;
       a.eb = p.ws.f_eb;
       a.rs = p.ws.f_rs;
       a.ids = nullptr;
@@ -271,10 +346,14 @@ __global__ void __launch_bounds__(kBlock, PGX_MIN_BLOCKS) min_run_kernel(MinRunP
     }
     front_skipped = skip;
     e_prev = (int)edges_s;
-    grid_sync<kArriveRed>(p.ws.bar, gen);
+    if constexpr (bfs)
+      grid_sync_bc(p.ws.bar, gen, &p.ws.ctr[s + 1].packed,
+                   reinterpret_cast<const unsigned long long *>(&p.ws.ctr[s].recip), s_bc);
+    else
+      grid_sync<kArriveRed>(p.ws.bar, gen);
 
     // ---- stats + halt test (engine.py:284-300) ----
-    const unsigned nrecip = p.ws.ctr[s].recip;
+    const unsigned nrecip = bfs ? (unsigned)s_bc[1] : p.ws.ctr[s].recip;
     if (blockIdx.x == 0 && threadIdx.x == 0) {
       const StepCounters c = p.ws.ctr[s];
       const int64_t senders = (int64_t)(c.packed >> 32);
@@ -592,7 +671,8 @@ static int min_run(int app, int32_t n, int64_t m, const int32_t *row_ptr, const 
                    const void *graph_ws, const int32_t *hub_ids, int32_t nhubs,
                    int32_t source, int32_t max_supersteps, uint32_t *val,
                    void *run_ws, size_t run_ws_bytes, int64_t *stats, uintptr_t stream,
-                   const PgxSegIndex *seg = nullptr) {
+                   const PgxSegIndex *seg = nullptr, const int32_t *in_row_ptr = nullptr,
+                   const int32_t *in_col = nullptr) {
   if (nhubs < 0 || nhubs > kHubs || (nhubs > 0 && !hub_ids))
     return fail(PGX_EINVAL, "hub count must be in [0, pgx_hub_capacity()]");
   if (seg) {
@@ -642,6 +722,12 @@ static int min_run(int app, int32_t n, int64_t m, const int32_t *row_ptr, const 
   else memset(&p.seg, 0, sizeof p.seg);
   p.seg_min_edges = (m * (int64_t)g_opt[PGX_OPT_SEG_MIN_EDGES]) / 1024;
   p.seg_predict = g_opt[PGX_OPT_SEG_PREDICT];
+  // bottom-up supersteps: the unit-weight (bitmap) kernel with an in-CSR
+  p.in_row_ptr = in_row_ptr;
+  p.in_col = in_col;
+  p.use_pull = app == PGX_APP_SSSP && bfs && in_row_ptr && (m == 0 || in_col) &&
+               g_opt[PGX_OPT_PULL_MIN_EDGES] <= 1024;
+  p.pull_min_edges = (m * (int64_t)g_opt[PGX_OPT_PULL_MIN_EDGES]) / 1024;
   size_t smem = scatter_smem(PGX_OP_MIN_U32, nhubs);
   if (p.use_seg) smem = std::max(smem, seg_smem_bytes(p.seg.seg_log2) + 16);
   int grid = 0;
@@ -672,6 +758,19 @@ int pgx_sssp_run_ex(int32_t n, int64_t m, const int32_t *row_ptr, const int32_t 
                     int64_t *stats, uintptr_t stream) {
   return min_run(PGX_APP_SSSP, n, m, row_ptr, col_idx, graph_ws, nullptr, 0, source,
                  max_supersteps, dist, run_ws, run_ws_bytes, stats, stream, seg);
+}
+
+int pgx_sssp_run_dir(int32_t n, int64_t m, const int32_t *row_ptr, const int32_t *col_idx,
+                     const void *graph_ws, const PgxSegIndex *seg, const int32_t *in_row_ptr,
+                     const int32_t *in_col, int32_t source, int32_t max_supersteps,
+                     uint32_t *dist, void *run_ws, size_t run_ws_bytes, int64_t *stats,
+                     uintptr_t stream) {
+  if (!in_row_ptr || (m > 0 && !in_col)) return fail(PGX_EINVAL, "null in-CSR pointer");
+  if (reinterpret_cast<uintptr_t>(in_col) % 32)  // 256-bit sector loads (pgx_pull.cuh)
+    return fail(PGX_EINVAL, "in_col must be 32-byte aligned");
+  return min_run(PGX_APP_SSSP, n, m, row_ptr, col_idx, graph_ws, nullptr, 0, source,
+                 max_supersteps, dist, run_ws, run_ws_bytes, stats, stream, seg, in_row_ptr,
+                 in_col);
 }
 
 int pgx_cc_run_ex(int32_t n, int64_t m, const int32_t *row_ptr, const int32_t *col_idx,

@@ -86,6 +86,12 @@ class EngineConfig:
     #: over runs; host graphs uploaded for one run use K1 throughout),
     #: "on" always, "off" never.  Results and statistics are identical.
     segments: str = "auto"
+    #: unit-weight SSSP direction-optimising supersteps (pgx_pull.cuh): a
+    #: superstep whose senders hold >= m/8 edges runs bottom-up over the
+    #: in-CSR.  "auto" builds the transpose for graphs that live on the GPU
+    #: (graph preprocessing, amortised like the segmented index), "on"
+    #: always, "off" never (push only).  Results and statistics are identical.
+    direction: str = "auto"
 
 
 @dataclass(frozen=True)
@@ -171,6 +177,8 @@ def _validate(program: VertexProgram, config: EngineConfig) -> None:
         raise ConfigError(f"bad hub_cache: {config.hub_cache!r}")
     if config.segments not in ("auto", "on", "off"):
         raise ConfigError(f"bad segments: {config.segments!r}")
+    if config.direction not in ("auto", "on", "off"):
+        raise ConfigError(f"bad direction: {config.direction!r}")
     if program.comm_mode is CommMode.PUSH and program.combine is None:
         raise ConfigError("push-mode programs must declare a combine function")
     if config.combiner is CombinerKind.CAS and program.comm_mode is CommMode.PUSH \
@@ -233,6 +241,7 @@ class LaunchPlan:
     pull: bool = False
     hubs: bool = False
     seg: Any = None          # _lib.PgxSegIndex when the segmented scatter is on
+    bottom_up: bool = False  # SSSP: direction-optimising (in-CSR bottom-up supersteps)
 
     def _hub_args(self):
         c = self.csr
@@ -266,6 +275,15 @@ class LaunchPlan:
                                       self.values.data_ptr(), self.ws.data_ptr(),
                                       self.ws_bytes, self.stats.data_ptr(), sp)
             _lib.check(rc, "pgx_pagerank_run")
+        elif self.app == "sssp" and self.bottom_up:
+            rc = lib.pgx_sssp_run_dir(c.n, c.m, c.row_ptr.data_ptr(), c.col_idx.data_ptr(),
+                                      c.ws.data_ptr(),
+                                      ctypes.byref(self.seg) if self.seg is not None else None,
+                                      c.in_row_ptr.data_ptr(), c.in_col.data_ptr(),
+                                      self.low["source"], self.max_steps,
+                                      self.values.data_ptr(), self.ws.data_ptr(),
+                                      self.ws_bytes, self.stats.data_ptr(), sp)
+            _lib.check(rc, "pgx_sssp_run_dir")
         elif self.app == "components" and self.seg is not None:
             rc = lib.pgx_cc_run_ex(c.n, c.m, c.row_ptr.data_ptr(), c.col_idx.data_ptr(),
                                    c.ws.data_ptr(), ctypes.byref(self.seg), self.max_steps,
@@ -337,6 +355,13 @@ def plan_run(graph: Graph, program: VertexProgram,
              and graph.device.type == "cuda")):
         csr.ensure_segments(stream)
         seg = csr.seg
+    # direction-optimising SSSP (bottom-up supersteps need the in-CSR; the
+    # hub-cache ablation arm runs push only)
+    bottom_up = app == "sssp" and not hubs and csr.m > 0 and (
+        config.direction == "on" or
+        (config.direction == "auto" and graph.device.type == "cuda"))
+    if bottom_up:
+        csr.ensure_transpose(stream)
     csr.runs += 1
     app_id = _lib.PGX_APP_PAGERANK_PULL if pull else _APP_ID[app]
     ws_bytes = _lib.out_size(lib.pgx_run_workspace_bytes, app_id, n, m, max_steps)
@@ -347,7 +372,7 @@ def plan_run(graph: Graph, program: VertexProgram,
         vdt = torch.float64 if app == "pagerank" else torch.int32
         values = torch.empty(n, dtype=vdt, device=dev)
     return LaunchPlan(app, csr, values, stats, ws, ws_bytes, max_steps, low, stream, pull, hubs,
-                      seg)
+                      seg, bottom_up)
 
 
 def collect(plan: LaunchPlan, program: VertexProgram, wall: float | None = None) -> RunReport:

@@ -6,7 +6,7 @@ the PR push arm walk).  Reports the fraction of edges whose destination
 already occurs earlier in the same round, and the mean distinct
 destinations per round.  usage: dup_rate.py C2,C4"""
 import os, sys, json
-sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__)))))
 import numpy as np
 from oracle import oracle as O
 

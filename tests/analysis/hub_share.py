@@ -3,7 +3,7 @@
 PageRank pull fold), and the segmented index's edges per entry at several
 segment sizes.  usage: hub_share.py C4,C2  -> profiles/hub_share_r2.json"""
 import json, os, sys
-sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__)))))
 import numpy as np
 from oracle import oracle as O
 

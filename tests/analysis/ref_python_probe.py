@@ -9,7 +9,7 @@ handed to pregelite.from_edges as stored edge arrays.
 
 usage: ref_python_probe.py C1:3,C2:1   (config:repeats)"""
 import json, os, sys, time
-ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+ROOT = os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 sys.path.insert(0, os.path.join(ROOT, "baseline", "_ref"))
 sys.path.insert(0, ROOT)
 import numpy as np

@@ -61,27 +61,46 @@ def seg_threshold():
     set_(256)
 
 
+@pytest.fixture
+def pull_threshold():
+    """Set PGX_OPT_PULL_MIN_EDGES (bottom-up SSSP supersteps from m * v /
+    1024 sender edges) for one test, restore the shipped value."""
+    def set_(v):
+        _lib.set_option(_lib.PGX_OPT_PULL_MIN_EDGES, v)
+    yield set_
+    set_(128)
+
+
 # modes: pull / push (PageRank lowering, min programs with the shipped
 # segment policy: device graphs get the segmented scatter for supersteps
 # with >= m/4 sender edges), hubs (hub-cache arm), k1 (segments off: K1 in
 # every superstep), segall (the segmented scatter whenever its send values
 # are exact: every superstep until the first K1 one), segskip (default
 # threshold, the apply never builds a frontier after a segmented superstep,
-# so every superstep after one runs segmented too)
-@pytest.mark.parametrize("mode", ["pull", "push", "hubs", "k1", "segall", "segskip"])
+# so every superstep after one runs segmented too), bu / buall (unit-weight
+# SSSP direction-optimising at the shipped threshold / bottom-up in every
+# superstep after the first), push1 (SSSP push only)
+@pytest.mark.parametrize("mode", ["pull", "push", "hubs", "k1", "segall", "segskip", "bu",
+                                  "buall", "push1"])
 @pytest.mark.parametrize("r", RUNS, ids=lambda r: r.id)
-def test_golden_reference_runs(r, mode, seg_threshold):
+def test_golden_reference_runs(r, mode, seg_threshold, pull_threshold):
     if mode == "push" and r.app != "pagerank":
         pytest.skip("pagerank_mode only changes the PageRank lowering")
     if mode in ("hubs", "k1", "segall", "segskip") and r.app == "pagerank":
         pytest.skip("hub_cache / segments only change the min combiner")
+    if mode in ("bu", "buall", "push1") and r.app != "sssp":
+        pytest.skip("direction only changes unit-weight SSSP")
     g = pgx.from_edges(r.src, r.dst, r.n, undirected=r.undirected, device="cuda")
     cap = r.kwargs.get("max_supersteps")
     cfg = pgx.EngineConfig(max_supersteps=cap if cap else pgx.DEFAULT_MAX_SUPERSTEPS,
                            pagerank_mode="push" if mode == "push" else "pull",
                            hub_cache="on" if mode == "hubs" else "off",
                            segments="off" if mode == "k1" else
-                           "on" if mode.startswith("seg") else "auto")
+                           "on" if mode.startswith("seg") else "auto",
+                           direction="on" if mode.startswith("bu") else
+                           "off" if mode == "push1" else "auto")
+    if mode == "buall":
+        pull_threshold(0)
     if mode == "segall":
         seg_threshold(0)
     elif mode == "segskip":
@@ -253,6 +272,29 @@ def test_c3_sssp_known_answer(graphs, hubs):
         [4194304, 97364, 1730927, 1490812, 146756, 2024, 6]
     assert [s.messages_sent for s in rep.supersteps] == \
         [97364, 36379100, 27861844, 339319, 2142, 6, 0]
+
+
+@pytest.mark.parametrize("direction", ["off", "on", "all", "never"])
+def test_c3_sssp_directions(graphs, direction, pull_threshold):
+    """Bottom-up supersteps (pgx_pull.cuh) at C3's size: push only, the
+    shipped threshold (supersteps 1 and 2 bottom-up), every superstep after
+    the first bottom-up, and the threshold above m (no bottom-up with the
+    in-CSR bound): one distance vector, one set of statistics."""
+    g = graphs("C3")
+    if direction == "all":
+        pull_threshold(0)
+    elif direction == "never":
+        pull_threshold(1025)
+    rep = pgx.run(g, pgx.sssp(0), pgx.EngineConfig(direction="off" if direction == "off"
+                                                   else "on"))
+    assert sha(rep.values, "<u4") == \
+        "bd08774026f70bbd29b80c977187f880654c0d8cbd2b42ba0988fed279ffa1e2"
+    assert [s.active_count for s in rep.supersteps] == \
+        [4194304, 97364, 1730927, 1490812, 146756, 2024, 6]
+    assert [s.messages_sent for s in rep.supersteps] == \
+        [97364, 36379100, 27861844, 339319, 2142, 6, 0]
+    assert [s.recipients for s in rep.supersteps] == \
+        [97364, 1730927, 1490812, 146756, 2024, 6, 0]
 
 
 @pytest.mark.parametrize("mode", ["pull", "push"])

@@ -23,6 +23,7 @@ import pytest
 import torch
 
 import paper_2010_01542_b200 as pgx
+from paper_2010_01542_b200 import _lib
 from oracle import oracle as O
 from paper_2010_01542_b200.rmat import rmat_graph
 
@@ -136,11 +137,18 @@ def test_randomized_gpu_vs_oracle(case):
     assert [s.active_count for s in cc.supersteps] == want.active_counts
     assert [s.messages_sent for s in cc.supersteps] == want.messages_sent
     source = int(np.argmax(np.diff(off)))
-    sp = pgx.run(g, pgx.sssp(source))
     want = O.run_sssp(n, off, tgt, source)
-    assert np.array_equal(sp.values, want.values)
-    assert [s.active_count for s in sp.supersteps] == want.active_counts
-    assert [s.messages_sent for s in sp.supersteps] == want.messages_sent
+    # push only, direction-optimising (shipped threshold), bottom-up in
+    # every superstep after the first
+    for direction, thr in (("off", 128), ("on", 128), ("on", 0)):
+        _lib.set_option(_lib.PGX_OPT_PULL_MIN_EDGES, thr)
+        try:
+            sp = pgx.run(g, pgx.sssp(source), pgx.EngineConfig(direction=direction))
+        finally:
+            _lib.set_option(_lib.PGX_OPT_PULL_MIN_EDGES, 128)
+        assert np.array_equal(sp.values, want.values), (direction, thr)
+        assert [s.active_count for s in sp.supersteps] == want.active_counts
+        assert [s.messages_sent for s in sp.supersteps] == want.messages_sent
     for mode in ("pull", "push"):
         pr = pgx.run(g, pgx.pagerank(), pgx.EngineConfig(pagerank_mode=mode))
         want = O.run_pagerank(n, off, tgt)
@@ -171,11 +179,16 @@ def test_large_hub_rows_and_long_runs_vs_oracle(case):
     g = pgx.from_csr(torch.from_numpy(off).cuda(), torch.from_numpy(tgt).cuda())
     cap = 30_000
     for source in (0, n - 1):
-        sp = pgx.run(g, pgx.sssp(source), pgx.EngineConfig(max_supersteps=cap))
         want = O.run_sssp(n, off, tgt, source, cap)
-        assert np.array_equal(sp.values, want.values), (name, source)
-        assert [s.active_count for s in sp.supersteps] == want.active_counts
-        assert [s.messages_sent for s in sp.supersteps] == want.messages_sent
+        for thr in (128, 0):  # shipped direction threshold / bottom-up throughout
+            _lib.set_option(_lib.PGX_OPT_PULL_MIN_EDGES, thr)
+            try:
+                sp = pgx.run(g, pgx.sssp(source), pgx.EngineConfig(max_supersteps=cap))
+            finally:
+                _lib.set_option(_lib.PGX_OPT_PULL_MIN_EDGES, 128)
+            assert np.array_equal(sp.values, want.values), (name, source, thr)
+            assert [s.active_count for s in sp.supersteps] == want.active_counts
+            assert [s.messages_sent for s in sp.supersteps] == want.messages_sent
     cc = pgx.run(g, pgx.connected_components(), pgx.EngineConfig(max_supersteps=cap))
     want = O.run_cc(n, off, tgt, max_steps=cap)
     assert np.array_equal(cc.values, want.values)

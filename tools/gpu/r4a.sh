@@ -1,0 +1,6 @@
+set -x
+timeout 600 python tools/probe.py C3 5 > gpurun_out/r4a_bu.log 2>&1
+timeout 600 python tools/probe.py C3 5 pull_min_edges=1025 > gpurun_out/r4a_push.log 2>&1
+for v in t u4 u1; do PGX_LIB=$PWD/exp/libpgx_$v.so timeout 600 python tools/probe.py C3 3 > gpurun_out/r4a_$v.log 2>&1; done
+timeout 1500 python -m pytest tests/test_gpu.py tests/test_gpu_properties.py -x -q -p no:cacheprovider > gpurun_out/r4a_tests.log 2>&1; echo "rc=$?"
+tail -3 gpurun_out/r4a_tests.log
