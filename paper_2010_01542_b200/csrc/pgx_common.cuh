@@ -163,30 +163,41 @@ __device__ __forceinline__ __attribute__((unused)) unsigned lanemask_lt() {
   return m;
 }
 
-// Grid barrier for a co-resident (cooperative) grid.  The gpu-scope
-// fences on both sides also invalidate L1 (CCTL.IVALL), so the weak,
-// L1-cacheable mailbox / has-bit reads of the next phase never see values
-// from before the barrier.
+// Grid barrier for a co-resident (cooperative) grid.  After the barrier
+// the weak, L1-cacheable mailbox / has-bit reads of the next phase must not
+// see values from before it: the acquire poll invalidates L1 (CCTL.IVALL
+// in the SASS), and the release add orders the CTA's writes (bar.sync,
+// then MEMBAR.ALL.GPU + RED by thread 0; PTX release is cumulative over
+// what happens-before it through the bar.sync).
 struct GridBarrier {
   unsigned count;
   unsigned gen;
 };
 
-// Two arrival schemes, chosen per kernel by measurement:
-//   kArriveRed: a monotonic arrival counter (zeroed before every launch);
-//     every CTA arrives with one fire-and-forget red.release and polls
-//     with ld.acquire until the whole generation arrived -- no atomic
-//     return value and no last-arriver hop on the critical path (CC / SSSP:
-//     C2 -2 %, C3 -2 %);
+// Two arrival schemes:
+//   kArriveRed (every kernel): a monotonic arrival counter (zeroed before
+//     every launch); every CTA arrives with one fire-and-forget
+//     red.release and polls with ld.acquire until the whole generation
+//     arrived -- no atomic return value and no last-arriver hop on the
+//     critical path.  1.30 us per barrier at 148 CTAs, 1.54 us with the
+//     sequentially consistent fences of PGX_BAR_SC = 1 (MEMBAR.SC.GPU on
+//     both sides), 2.06 us for kArriveAtomic (tools/barrier_bench.cu);
+//     C1 -14 %, C3 -4 %, C2 -1.4 %, C4 -0.6 % against the fenced version;
 //   kArriveAtomic: atomicAdd with return, the last arriver flips `gen`
-//     (PageRank: C4 is 0.7 % faster with it).
+//     (kept for A/B builds: -DPGX_BAR_DEFAULT=kArriveAtomic).
 enum BarrierKind { kArriveAtomic = 0, kArriveRed = 1 };
 
-template <int KIND = kArriveAtomic>
+#ifndef PGX_BAR_SC
+#define PGX_BAR_SC 0       // 1: sequentially consistent fences around the red arrival
+#endif
+#ifndef PGX_BAR_DEFAULT
+#define PGX_BAR_DEFAULT kArriveRed
+#endif
+template <int KIND = PGX_BAR_DEFAULT>
 __device__ __forceinline__ void grid_sync(GridBarrier *bar, unsigned &gen) {
   __syncthreads();
   if (threadIdx.x == 0) {
-    __threadfence();
+    if (KIND != kArriveRed || PGX_BAR_SC) __threadfence();
     if (KIND == kArriveRed) {
       const unsigned target = (gen + 1) * gridDim.x;
       asm volatile("red.release.gpu.global.add.u32 [%0], %1;" ::"l"(&bar->count), "r"(1u)
@@ -206,7 +217,10 @@ __device__ __forceinline__ void grid_sync(GridBarrier *bar, unsigned &gen) {
         }
       }
     }
-    __threadfence();
+    // without PGX_BAR_SC the red barrier's release add (MEMBAR.ALL.GPU +
+    // RED) and acquire poll (which invalidates L1: CCTL.IVALL) carry the
+    // ordering
+    if (KIND != kArriveRed || PGX_BAR_SC) __threadfence();
   }
   gen += 1;
   __syncthreads();
@@ -230,13 +244,13 @@ __device__ __forceinline__ void grid_sync_bc(GridBarrier *bar, unsigned &gen,
                                              unsigned long long *s_out) {
   __syncthreads();
   if (threadIdx.x == 0) {
-    __threadfence();
+    if (PGX_BAR_SC) __threadfence();
     const unsigned target = (gen + 1) * gridDim.x;
     asm volatile("red.release.gpu.global.add.u32 [%0], %1;" ::"l"(&bar->count), "r"(1u)
                  : "memory");
     while ((int)(ld_acquire(&bar->count) - target) < 0) {
     }
-    __threadfence();
+    if (PGX_BAR_SC) __threadfence();
     if (a) s_out[0] = ld_relaxed_u64(a);
     if (b) s_out[1] = ld_relaxed_u64(b);
   }
