@@ -97,6 +97,21 @@ def test_pull_pagerank_rejects_a_misaligned_in_col():
     assert b"32-byte aligned" in lib.pgx_last_error()
 
 
+def test_direction_optimising_sssp_rejects_a_bad_in_csr():
+    """pgx_sssp_run_dir checks its in-CSR before anything touches the
+    device: a null in_row_ptr (or in_col with edges) and a misaligned
+    in_col (256-bit sector loads) are PGX_EINVAL."""
+    lib = _lib.load()
+    fake = 1 << 20  # never dereferenced: the argument checks come first
+    args = lambda irp, ic: (10, 20, fake, fake, fake, None, irp, ic, 0, 10, fake, fake, 1 << 20,
+                            fake, 0)
+    assert lib.pgx_sssp_run_dir(*args(None, fake)) == _lib.PGX_EINVAL
+    assert b"in-CSR" in lib.pgx_last_error()
+    assert lib.pgx_sssp_run_dir(*args(fake, None)) == _lib.PGX_EINVAL
+    assert lib.pgx_sssp_run_dir(*args(fake, fake + 4)) == _lib.PGX_EINVAL
+    assert b"32-byte aligned" in lib.pgx_last_error()
+
+
 def test_integration_doc_covers_every_entry_point():
     doc = open(os.path.join(ROOT, "INTEGRATION.md")).read()
     assert [s for s in _lib.EXPORTS if s not in doc] == []
