@@ -104,6 +104,15 @@ __host__ __device__ constexpr size_t seg_smem_bytes(int seg_log2) {
   return ((size_t)4 << seg_log2) + (size_t)kWarps * kSegWinWords * 4;
 }
 
+// superstep 0 of CC (messages = source ids, no send-value loads) is bound
+// by instruction issue: two edges per lane and round there (C5 superstep 0
+// 2.75 -> 2.71 ms, the run -0.6 %); the label supersteps keep one edge per
+// lane (pairs measured 5 % slower there: 4.12 vs 3.92 ms on C5), four per
+// lane for superstep 0 measured the same as two
+#ifndef PGX_SEG_PAIRS
+#define PGX_SEG_PAIRS 1
+#endif
+
 template <int MSG>
 __device__ void seg_scatter_phase(const SegPass &a, char *smem_raw) {
   uint32_t *smem = reinterpret_cast<uint32_t *>(smem_raw);
@@ -228,8 +237,48 @@ __device__ void seg_scatter_phase(const SegPass &a, char *smem_raw) {
           }
         }
       };
+#if PGX_SEG_PAIRS
+      // two consecutive edges per lane and round (one 32-bit destination
+      // pair load, one ballot per edge parity): 64 edges per round, for the
+      // source-id superstep
+      const uint32_t lt = (1u << lane) - 1u;  // lanes below this one
+      auto rounds2 = [&](auto checked) {
+        const uint32_t *w_col2 = reinterpret_cast<const uint32_t *>(w_col);
+#pragma unroll
+        for (int r = 0; r < kItems / 2; r++) {
+          const int el = r * 64 + 2 * lane;
+          const uint32_t cc = w_col2[r * 32 + lane];
+          const uint32_t c0 = cc & 0xFFFFu, c1 = cc >> 16;
+          const bool f0 = (c0 & kSegEntryFlag) != 0u, f1 = (c1 & kSegEntryFlag) != 0u;
+          const unsigned b0 = __ballot_sync(0xFFFFFFFFu, f0);
+          const unsigned b1 = __ballot_sync(0xFFFFFFFFu, f1);
+          const int sidx0 = cur + __popc(b0 & (lt | (1u << lane))) + __popc(b1 & lt);
+          const int sidx1 = sidx0 + (int)f1;
+          cur += __popc(b0) + __popc(b1);
+          if (!decltype(checked)::value || (el >= ea && el < ez)) {
+            const uint32_t msg = w_msg[sidx0];
+            const int loc = (int)(c0 & lmask);
+            if (msg < s_mb[loc]) atomicMin(s_mb + loc, msg);
+          }
+          if (!decltype(checked)::value || (el + 1 >= ea && el + 1 < ez)) {
+            const uint32_t msg = w_msg[sidx1];
+            const int loc = (int)(c1 & lmask);
+            if (msg < s_mb[loc]) atomicMin(s_mb + loc, msg);
+          }
+        }
+      };
+      if (MSG != kSegSourceId) {
+        if (ea == 0 && ez == kTile) rounds(std::false_type{});  // interior tile
+        else rounds(std::true_type{});
+      } else if (ea == 0 && ez == kTile) {
+        rounds2(std::false_type{});
+      } else {
+        rounds2(std::true_type{});
+      }
+#else
       if (ea == 0 && ez == kTile) rounds(std::false_type{});  // interior tile
       else rounds(std::true_type{});
+#endif
       t = tn;
     }
     __syncthreads();

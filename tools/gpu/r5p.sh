@@ -1,0 +1,6 @@
+for r in 1 2; do
+timeout 900 python tools/seg_check.py C2,C5 shipped > gpurun_out/r5p_cur_$r.log 2>&1
+PGX_LIB=$PWD/exp/libpgx_pairs0.so timeout 900 python tools/seg_check.py C2,C5 shipped > gpurun_out/r5p_pairs_$r.log 2>&1
+PGX_LIB=$PWD/exp/libpgx_quads0.so timeout 900 python tools/seg_check.py C2,C5 shipped > gpurun_out/r5p_quads_$r.log 2>&1
+done
+PGX_LIB=$PWD/exp/libpgx_quads0.so timeout 1500 python -m pytest tests/test_gpu.py tests/test_gpu_c5.py -x -q -p no:cacheprovider > gpurun_out/r5p_tests.log 2>&1; echo "rc=$?"
