@@ -33,7 +33,7 @@
 extern "C" {
 #endif
 
-#define PGX_ABI_VERSION 5
+#define PGX_ABI_VERSION 6
 
 #define PGX_OK 0
 #define PGX_EINVAL (-1)   /* bad argument / unsupported configuration */
@@ -276,6 +276,23 @@ int pgx_pagerank_pull_run(int32_t n, int64_t m, const int32_t *row_ptr,
                           int32_t max_supersteps, double *rank, void *run_ws,
                           size_t run_ws_bytes, int64_t *stats,
                           uintptr_t stream);
+
+/* Hub sources of the pull fold (the north star's hybrid path, pull form):
+ * in_col_hubs is a copy of in_col in which every edge FROM one of `nhubs`
+ * hub sources (the highest out-degree vertices) holds (0x80000000 | slot);
+ * hub_slot[v] is v's slot or -1 (n entries).  Each CTA keeps the hub
+ * shares in shared memory, so those edges cost no scattered global load.
+ * Results are bit-identical to pgx_pagerank_pull_run.  Replaces the same
+ * reference interface (engine.py:425-457 fold, algorithms.py:27-84).
+ * nhubs <= pgx_pr_hub_capacity(); nhubs = 0 is pgx_pagerank_pull_run. */
+int pgx_pr_hub_capacity(int32_t *capacity);
+int pgx_pagerank_pull_hubs_run(int32_t n, int64_t m, const int32_t *row_ptr,
+                               const int32_t *in_row_ptr, const int32_t *in_col_hubs,
+                               const void *in_graph_ws, const int32_t *hub_slot,
+                               int32_t nhubs, int32_t iterations, double damping,
+                               double base, double r0, int32_t max_supersteps,
+                               double *rank, void *run_ws, size_t run_ws_bytes,
+                               int64_t *stats, uintptr_t stream);
 
 /* ---------------------------------------------------------------- */
 /* phases of the partitioned multi-GPU superstep.     */

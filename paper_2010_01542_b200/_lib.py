@@ -16,7 +16,7 @@ from .errors import ConfigError, ExecutionError
 PKG_DIR = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.environ.get("PGX_LIB") or os.path.join(PKG_DIR, "libpgx.so")
 
-PGX_ABI_VERSION = 5
+PGX_ABI_VERSION = 6
 PGX_OK, PGX_EINVAL, PGX_ECUDA, PGX_ENOMEM = 0, -1, -2, -3
 PGX_APP_PAGERANK, PGX_APP_CC, PGX_APP_SSSP, PGX_APP_PAGERANK_PULL = 0, 1, 2, 3
 PGX_OP_MIN_U32, PGX_OP_SUM_F64 = 0, 1
@@ -40,7 +40,8 @@ EXPORTS = (
     "pgx_abi_version", "pgx_last_error", "pgx_set_option", "pgx_device_sm_count",
     "pgx_offsets_to_i32", "pgx_graph_workspace_bytes", "pgx_graph_prepare",
     "pgx_run_workspace_bytes", "pgx_hub_capacity", "pgx_sssp_run", "pgx_cc_run",
-    "pgx_pagerank_run", "pgx_pagerank_pull_run", "pgx_rmat_keys", "pgx_microbench",
+    "pgx_pagerank_run", "pgx_pagerank_pull_run", "pgx_pr_hub_capacity",
+    "pgx_pagerank_pull_hubs_run", "pgx_rmat_keys", "pgx_microbench",
     "pgx_slice_init", "pgx_scatter", "pgx_slice_counters_bytes", "pgx_apply_slice",
     "pgx_pr_apply_slice", "pgx_touched_scratch_bytes", "pgx_touched", "pgx_scatter_pairs",
     "pgx_scatter_peer", "pgx_reset_touched", "pgx_peer_alloc", "pgx_peer_open",
@@ -89,6 +90,9 @@ _SIGS = {
                                         _i32, _p, _p, _sz, _p, _up]),
     "pgx_pagerank_pull_run": (ctypes.c_int, [_i32, _i64, _p, _p, _p, _p, _i32, _f64, _f64,
                                              _f64, _i32, _p, _p, _sz, _p, _up]),
+    "pgx_pr_hub_capacity": (ctypes.c_int, [_p]),
+    "pgx_pagerank_pull_hubs_run": (ctypes.c_int, [_i32, _i64, _p, _p, _p, _p, _p, _i32, _i32,
+                                                  _f64, _f64, _f64, _i32, _p, _p, _sz, _p, _up]),
     "pgx_slice_init": (ctypes.c_int, [ctypes.c_int, _i32, _i32, _p, _p, _p, _f64, _up]),
     "pgx_scatter": (ctypes.c_int, [ctypes.c_int, ctypes.c_int, _p, _p, _p, _p, _i32, _p, _p,
                                    _i32, _i64, _p, _p, ctypes.c_uint32, _up]),

@@ -63,6 +63,13 @@ constexpr int kHubs = 12288;         // hub recipients cached per CTA (48 KB sme
 constexpr int kInvalidEdge = 0x7FFFFFFF;  // never a vertex id (n < 2^31 - 1)
 constexpr int kApplyListBytes = 12288 * 4;  // apply: vertex-id list segment (fits the scatter windows)
 constexpr int kMaxCtas = 4096;
+// pull PageRank: hub sources whose shares each CTA keeps in shared memory.
+// With the fold's per-warp staging (kWarps * kSlots * 8 = 66 KB) a 96 KB
+// table takes the 164 KB shared-memory carveout and leaves 92 KB of L1,
+// which the fold's scattered loads need in flight: C4 5.76 ms (no table),
+// 5.33 (6K), 5.29 (12K), 5.59 (14K, 60 KB of L1), 9.33 (20K, 28 KB of L1)
+// (tools/pr_hub_probe.py, DESIGN.md 3 K3)
+constexpr int kPrHubCap = 12288;
 constexpr int kCompactBlock = 1024;
 
 // ---- host-side error state and knobs (defined in pgx_graph.cu) ----------
@@ -322,6 +329,7 @@ struct RunWs {
   void *mailbox;           // [n]   u32 (min) or f64 (sum); pull PR: folded sums
   double *share2;          // pull PR: second share buffer
   double *head, *tail;     // pull PR: per-tile partials of tile-spanning rows
+  double *hub_share[2];    // pull PR: [kPrHubCap] x 2 hub sources' shares (by slot)
   uint32_t *snd[2];        // [n/32+2] x 2 senders bitmaps (segmented scatter; min apps)
   uint32_t *sv[2];         // CC: [n] x 2 send values (the neutral for non-senders)
 };
@@ -345,12 +353,15 @@ inline size_t run_ws_layout(int app, int64_t n, int64_t m, int32_t max_steps, Ru
   // interleaved layout (min programs): {mailbox, value} records
   w.mailbox = take(W * (size_t)(n + 1) * (interleaved && !pr ? 2 : 1));
   w.share2 = w.head = w.tail = nullptr;
+  w.hub_share[0] = w.hub_share[1] = nullptr;
   w.snd[0] = w.snd[1] = nullptr;
   w.sv[0] = w.sv[1] = nullptr;
   if (app == PGX_APP_PAGERANK_PULL) {
     w.share2 = (double *)take(sizeof(double) * (size_t)(n + 1));
     w.head = (double *)take(sizeof(double) * (size_t)(ceil_div(m, kTile) + 2));
     w.tail = (double *)take(sizeof(double) * (size_t)(ceil_div(m, kTile) + 2));
+    w.hub_share[0] = (double *)take(sizeof(double) * (size_t)kPrHubCap);
+    w.hub_share[1] = (double *)take(sizeof(double) * (size_t)kPrHubCap);
   }
   if (!pr) {
     w.f_eb = (int32_t *)take(sizeof(int32_t) * (size_t)(n + 1));

@@ -28,8 +28,17 @@ struct GatherArgs {
   const double *share;      // shares broadcast last superstep
   double *folded, *head, *tail;
   int32_t n;                // vertex bound of in_col values (checked builds)
+  const double *s_hub;      // HUBS: shared-memory copy of the hub sources' shares
 };
 
+// HUBS: in_col holds (0x80000000 | slot) for an edge from hub source
+// hub_ids[slot] (the highest out-degree vertices); its share is read from the
+// CTA's shared-memory copy s_hub[slot] instead of a scattered global load.
+// A warp-wide scattered load costs one L1 tag cycle per distinct line
+// (hit or miss), which is what bounds the fold (K3); lanes
+// whose source is a hub drop out of it.  Same values, same order: the
+// result is bit-identical to the plain fold.
+template <bool HUBS = false>
 __device__ __forceinline__ void gather_phase(const GatherArgs &a, char *smem) {
   const int lane = (int)lane_id();
   const int warp = threadIdx.x >> 5;
@@ -79,17 +88,24 @@ __device__ __forceinline__ void gather_phase(const GatherArgs &a, char *smem) {
     const int64_t a1 = min(e1, a0 + 8);
     const bool active = a0 < e1;
     int col[8];
-    if (active && a1 - a0 == 8) {
+    const bool full = active && a1 - a0 == 8;
+    if (full) {
       ld_stream8(a.in_col + a0, pol, col);
     } else {
 #pragma unroll
-      for (int j = 0; j < 8; j++) col[j] = (a0 + j < a1) ? ld_stream(a.in_col + a0 + j, pol) : -1;
+      for (int j = 0; j < 8; j++) col[j] = (a0 + j < a1) ? ld_stream(a.in_col + a0 + j, pol) : 0;
     }
     double x[8];
 #pragma unroll
     for (int j = 0; j < 8; j++) {
-      PGX_ASSERT(col[j] < a.n);
-      x[j] = (col[j] >= 0) ? __ldg(a.share + col[j]) : 0.0;
+      const bool valid = full || a0 + j < a1;
+      if (HUBS) {
+        PGX_ASSERT(col[j] < a.n);
+        x[j] = !valid ? 0.0 : (col[j] < 0) ? a.s_hub[col[j] & 0x7FFFFFFF] : __ldg(a.share + col[j]);
+      } else {
+        PGX_ASSERT(col[j] >= 0 && col[j] < a.n);
+        x[j] = valid ? __ldg(a.share + col[j]) : 0.0;
+      }
     }
     // row holding a0: largest idx with s_eb[idx] <= a0 (binary search over
     // the <= 258 staged row starts), then the starts of the next 8 rows as

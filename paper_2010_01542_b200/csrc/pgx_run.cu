@@ -550,8 +550,15 @@ struct PrPullParams {
   double damping, base, r0;
   int32_t max_steps;
   int64_t *stats;
+  const int32_t *hub_slot;    // HUBS: [n] slot of a hub source, -1 otherwise
+  int32_t nhubs;
 };
 
+// HUBS: the in-CSR holds (0x80000000 | slot) for edges from the nhubs hub
+// sources; the compute writes their next shares to a compact slot-indexed
+// array as well, and every CTA copies it into shared memory (coalesced)
+// before each fold (pgx_gather.cuh)
+template <bool HUBS>
 __global__ void __launch_bounds__(kBlock, PGX_MIN_BLOCKS) pagerank_pull_kernel(PrPullParams p) {
   extern __shared__ __align__(16) char smem[];
   __shared__ double s_red[32];
@@ -561,6 +568,9 @@ __global__ void __launch_bounds__(kBlock, PGX_MIN_BLOCKS) pagerank_pull_kernel(P
   double *folded = reinterpret_cast<double *>(p.ws.mailbox);
   double *share_cur = reinterpret_cast<double *>(p.ws.f_msg);
   double *share_nxt = p.ws.share2;
+  double *hub_cur = p.ws.hub_share[0];
+  double *hub_nxt = p.ws.hub_share[1];
+  double *s_hub = reinterpret_cast<double *>(smem + (size_t)kWarps * kSlots * 8);
   const unsigned nthreads = gridDim.x * blockDim.x;
   const unsigned gtid = blockIdx.x * blockDim.x + threadIdx.x;
   const int last = p.iterations - 1;
@@ -571,7 +581,12 @@ __global__ void __launch_bounds__(kBlock, PGX_MIN_BLOCKS) pagerank_pull_kernel(P
   for (unsigned v = gtid; v < (unsigned)p.n; v += nthreads) {
     const int deg = p.row_ptr[v + 1] - p.row_ptr[v];
     p.rank[v] = p.r0;
-    share_cur[v] = deg ? __ddiv_rn(p.r0, (double)deg) : 0.0;
+    const double sh = deg ? __ddiv_rn(p.r0, (double)deg) : 0.0;
+    share_cur[v] = sh;
+    if (HUBS) {
+      const int slot = p.hub_slot[v];
+      if (slot >= 0) hub_cur[slot] = sh;
+    }
     my_dangling += deg ? 0ull : 1ull;
   }
   unsigned long long bd = block_sum<unsigned long long>(my_dangling, s_ured);
@@ -599,13 +614,20 @@ __global__ void __launch_bounds__(kBlock, PGX_MIN_BLOCKS) pagerank_pull_kernel(P
   g.head = p.ws.head;
   g.tail = p.ws.tail;
   g.n = p.n;
+  g.s_hub = s_hub;
 
   for (int s = 0;; s++) {
     if (blockIdx.x == 0 && threadIdx.x == 0)
       p.stats[PGX_STAT_HDR + (int64_t)s * PGX_STAT_FIELDS + 7] = (int64_t)globaltimer();
+    if (HUBS) {  // the hub shares of last superstep into shared memory
+      const double2 *src = reinterpret_cast<const double2 *>(hub_cur);
+      double2 *dst = reinterpret_cast<double2 *>(s_hub);
+      for (int h = threadIdx.x; h < (p.nhubs + 1) / 2; h += kBlock) dst[h] = __ldcg(src + h);
+      __syncthreads();
+    }
     // ---- fold (engine.py:425-457): in-neighbour shares of last superstep
     g.share = share_cur;
-    gather_phase(g, smem);
+    gather_phase<HUBS>(g, smem);
     grid_sync(p.ws.bar, gen);
     const uint64_t t_fold = globaltimer();
 
@@ -616,7 +638,7 @@ __global__ void __launch_bounds__(kBlock, PGX_MIN_BLOCKS) pagerank_pull_kernel(P
     const double dn = __ddiv_rn(dangling, dn_n);
     double my_d = 0.0;
     for (unsigned v0 = gtid; v0 < (unsigned)p.n; v0 += kPrUnroll * nthreads) {
-      int es[kPrUnroll], ee[kPrUnroll], r0[kPrUnroll], r1[kPrUnroll];
+      int es[kPrUnroll], ee[kPrUnroll], r0[kPrUnroll], r1[kPrUnroll], hs[kPrUnroll];
       double fv[kPrUnroll];
 #pragma unroll
       for (int j = 0; j < kPrUnroll; j++) {
@@ -627,6 +649,7 @@ __global__ void __launch_bounds__(kBlock, PGX_MIN_BLOCKS) pagerank_pull_kernel(P
           r0[j] = p.row_ptr[v];
           r1[j] = p.row_ptr[v + 1];
           fv[j] = folded[v];
+          if (HUBS) hs[j] = p.hub_slot[v];
         }
       }
 #pragma unroll
@@ -647,7 +670,11 @@ __global__ void __launch_bounds__(kBlock, PGX_MIN_BLOCKS) pagerank_pull_kernel(P
         p.rank[v] = r;
         const int deg = r1[j] - r0[j];
         if (deg == 0) my_d = __dadd_rn(my_d, r);
-        else if (s != last) share_nxt[v] = __ddiv_rn(r, (double)deg);
+        else if (s != last) {
+          const double sh = __ddiv_rn(r, (double)deg);
+          share_nxt[v] = sh;
+          if (HUBS && hs[j] >= 0) hub_nxt[hs[j]] = sh;
+        }
       }
     }
     const double bsum = block_sum<double>(my_d, s_red);
@@ -678,6 +705,9 @@ __global__ void __launch_bounds__(kBlock, PGX_MIN_BLOCKS) pagerank_pull_kernel(P
     double *tmp = share_cur;
     share_cur = share_nxt;
     share_nxt = tmp;
+    tmp = hub_cur;
+    hub_cur = hub_nxt;
+    hub_nxt = tmp;
   }
 }
 
@@ -876,16 +906,22 @@ int pgx_pagerank_run(int32_t n, int64_t m, const int32_t *row_ptr, const int32_t
   return PGX_OK;
 }
 
-int pgx_pagerank_pull_run(int32_t n, int64_t m, const int32_t *row_ptr,
-                          const int32_t *in_row_ptr, const int32_t *in_col,
-                          const void *in_graph_ws, int32_t iterations, double damping,
-                          double base, double r0, int32_t max_supersteps, double *rank,
-                          void *run_ws, size_t run_ws_bytes, int64_t *stats, uintptr_t stream) {
+}  // extern "C"
+
+namespace {
+int pagerank_pull_launch(int32_t n, int64_t m, const int32_t *row_ptr, const int32_t *in_row_ptr,
+                         const int32_t *in_col, const void *in_graph_ws,
+                         const int32_t *hub_slot, int32_t nhubs, int32_t iterations,
+                         double damping, double base, double r0, int32_t max_supersteps,
+                         double *rank, void *run_ws, size_t run_ws_bytes, int64_t *stats,
+                         uintptr_t stream) {
   int rc = check_graph(n, m, in_row_ptr, in_col, in_graph_ws);
   if (rc) return rc;
   if (!row_ptr) return fail(PGX_EINVAL, "null out-CSR offsets");
   if (reinterpret_cast<uintptr_t>(in_col) % 32)  // 256-bit id loads in the fold
     return fail(PGX_EINVAL, "in_col must be 32-byte aligned");
+  if (nhubs < 0 || nhubs > kPrHubCap) return fail(PGX_EINVAL, "nhubs must be in [0, pgx_pr_hub_capacity()]");
+  if (nhubs > 0 && !hub_slot) return fail(PGX_EINVAL, "null hub_slot");
   if (iterations < 1) return fail(PGX_EINVAL, "iterations must be >= 1");
   if (!(damping >= 0.0 && damping <= 1.0)) return fail(PGX_EINVAL, "damping must be in [0, 1]");
   if (max_supersteps < 1) return fail(PGX_EINVAL, "superstep cap must be >= 1");
@@ -907,16 +943,56 @@ int pgx_pagerank_pull_run(int32_t n, int64_t m, const int32_t *row_ptr,
   p.r0 = r0;
   p.max_steps = max_supersteps;
   p.stats = stats;
+  p.hub_slot = hub_slot;
+  p.nhubs = nhubs;
   cudaStream_t st = (cudaStream_t)stream;
   PGX_CUDA(cudaMemsetAsync(p.ws.bar, 0, 64, st));
   PGX_CUDA(cudaMemsetAsync(p.ws.misc, 0, 64, st));
-  const size_t smem = (size_t)kWarps * kSlots * 8 + 16;
+  const size_t smem = (size_t)kWarps * kSlots * 8 + 16 + (size_t)((nhubs + 1) & ~1) * 8;
   int grid = 0;
-  rc = coop_grid(pagerank_pull_kernel, smem, &grid);
-  if (rc) return rc;
   void *args[] = {&p};
-  PGX_CUDA(cudaLaunchCooperativeKernel((void *)pagerank_pull_kernel, grid, kBlock, args, smem, st));
+  if (nhubs > 0) {
+    rc = coop_grid(pagerank_pull_kernel<true>, smem, &grid);
+    if (rc) return rc;
+    PGX_CUDA(cudaLaunchCooperativeKernel((void *)pagerank_pull_kernel<true>, grid, kBlock, args,
+                                         smem, st));
+  } else {
+    rc = coop_grid(pagerank_pull_kernel<false>, smem, &grid);
+    if (rc) return rc;
+    PGX_CUDA(cudaLaunchCooperativeKernel((void *)pagerank_pull_kernel<false>, grid, kBlock, args,
+                                         smem, st));
+  }
   return PGX_OK;
+}
+}  // namespace
+
+extern "C" {
+
+int pgx_pr_hub_capacity(int32_t *capacity) {
+  if (!capacity) return fail(PGX_EINVAL, "null output pointer");
+  *capacity = kPrHubCap;
+  return PGX_OK;
+}
+
+int pgx_pagerank_pull_run(int32_t n, int64_t m, const int32_t *row_ptr,
+                          const int32_t *in_row_ptr, const int32_t *in_col,
+                          const void *in_graph_ws, int32_t iterations, double damping,
+                          double base, double r0, int32_t max_supersteps, double *rank,
+                          void *run_ws, size_t run_ws_bytes, int64_t *stats, uintptr_t stream) {
+  return pagerank_pull_launch(n, m, row_ptr, in_row_ptr, in_col, in_graph_ws, nullptr, 0,
+                              iterations, damping, base, r0, max_supersteps, rank, run_ws,
+                              run_ws_bytes, stats, stream);
+}
+
+int pgx_pagerank_pull_hubs_run(int32_t n, int64_t m, const int32_t *row_ptr,
+                               const int32_t *in_row_ptr, const int32_t *in_col_hubs,
+                               const void *in_graph_ws, const int32_t *hub_slot, int32_t nhubs,
+                               int32_t iterations, double damping, double base, double r0,
+                               int32_t max_supersteps, double *rank, void *run_ws,
+                               size_t run_ws_bytes, int64_t *stats, uintptr_t stream) {
+  return pagerank_pull_launch(n, m, row_ptr, in_row_ptr, in_col_hubs, in_graph_ws, hub_slot,
+                              nhubs, iterations, damping, base, r0, max_supersteps, rank, run_ws,
+                              run_ws_bytes, stats, stream);
 }
 
 }  // extern "C"

@@ -75,6 +75,13 @@ class EngineConfig:
     #: PageRank lowering: "pull" (the reference's comm mode, algorithms.py:80;
     #: in-neighbour fold, no atomics) or "push" (scatter with red.add.f64)
     pagerank_mode: str = "pull"
+    #: pull PageRank: the highest out-degree sources' shares kept in each
+    #: CTA's shared memory (pgx_pagerank_pull_hubs_run; bit-identical
+    #: results; the in-CSR's hub edges are encoded once per graph): "auto"
+    #: for graphs of >= 2^24 edges (C4 5.76 -> 5.29 ms; on C1 the table's
+    #: staging costs more than it saves: 0.133 -> 0.154 ms), "on" always,
+    #: "off" never
+    pagerank_hubs: str = "auto"
     #: shared-memory combiner for hub recipients (CC / SSSP, ablation arm;
     #: measured slower on B200): "auto" builds
     #: the hub encoding from the second run on a device CSR (amortised graph
@@ -173,6 +180,8 @@ def _validate(program: VertexProgram, config: EngineConfig) -> None:
         raise ConfigError(f"bad combiner kind: {config.combiner!r}")
     if config.pagerank_mode not in ("pull", "push"):
         raise ConfigError(f"bad pagerank_mode: {config.pagerank_mode!r}")
+    if config.pagerank_hubs not in ("auto", "on", "off"):
+        raise ConfigError(f"bad pagerank_hubs: {config.pagerank_hubs!r}")
     if config.hub_cache not in ("auto", "on", "off"):
         raise ConfigError(f"bad hub_cache: {config.hub_cache!r}")
     if config.segments not in ("auto", "on", "off"):
@@ -258,13 +267,21 @@ class LaunchPlan:
             it, d = self.low["iterations"], self.low["damping"]
             base = (1.0 - d) / c.n      # algorithms.py:49 (host float math)
             r0 = 1.0 / c.n              # algorithms.py:50
-            rc = lib.pgx_pagerank_pull_run(c.n, c.m, c.row_ptr.data_ptr(),
-                                           c.in_row_ptr.data_ptr(), c.in_col.data_ptr(),
-                                           c.in_ws.data_ptr(), it, d, base, r0,
-                                           self.max_steps, self.values.data_ptr(),
-                                           self.ws.data_ptr(), self.ws_bytes,
-                                           self.stats.data_ptr(), sp)
-            _lib.check(rc, "pgx_pagerank_pull_run")
+            if self.hubs and c.pr_nhubs > 0:
+                rc = lib.pgx_pagerank_pull_hubs_run(
+                    c.n, c.m, c.row_ptr.data_ptr(), c.in_row_ptr.data_ptr(),
+                    c.pr_hub_col.data_ptr(), c.in_ws.data_ptr(), c.pr_hub_slot.data_ptr(),
+                    c.pr_nhubs, it, d, base, r0, self.max_steps, self.values.data_ptr(),
+                    self.ws.data_ptr(), self.ws_bytes, self.stats.data_ptr(), sp)
+                _lib.check(rc, "pgx_pagerank_pull_hubs_run")
+            else:
+                rc = lib.pgx_pagerank_pull_run(c.n, c.m, c.row_ptr.data_ptr(),
+                                               c.in_row_ptr.data_ptr(), c.in_col.data_ptr(),
+                                               c.in_ws.data_ptr(), it, d, base, r0,
+                                               self.max_steps, self.values.data_ptr(),
+                                               self.ws.data_ptr(), self.ws_bytes,
+                                               self.stats.data_ptr(), sp)
+                _lib.check(rc, "pgx_pagerank_pull_run")
         elif self.app == "pagerank":
             it, d = self.low["iterations"], self.low["damping"]
             base = (1.0 - d) / c.n      # algorithms.py:49 (host float math)
@@ -344,6 +361,10 @@ def plan_run(graph: Graph, program: VertexProgram,
                                   (config.hub_cache == "auto" and csr.runs >= 1))
     if hubs:
         csr.ensure_hubs(stream)
+    if pull and csr.m > 0 and (config.pagerank_hubs == "on" or
+                               (config.pagerank_hubs == "auto" and csr.m >= 1 << 24)):
+        csr.ensure_pr_hubs(stream)
+        hubs = True
     seg = None
     # "auto": CC on device-resident graphs (the index is graph preparation,
     # amortised over runs; a host graph uploaded for one run keeps K1

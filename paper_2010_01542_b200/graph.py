@@ -63,6 +63,9 @@ class DeviceCSR:
     in_ws: torch.Tensor | None = None        # tile map of the transpose
     hub_col: torch.Tensor | None = None      # col_idx with hub edges encoded
     hub_ids: torch.Tensor | None = None      # hub slot -> vertex
+    pr_hub_col: torch.Tensor | None = None   # in_col with hub-source edges encoded
+    pr_hub_slot: torch.Tensor | None = None  # vertex -> hub slot (or -1)
+    pr_nhubs: int = 0
     runs: int = 0                            # device runs on this CSR
     seg: object = None                       # _lib.PgxSegIndex (segmented scatter)
     seg_arrays: tuple = ()                   # the tensors seg points into
@@ -142,6 +145,36 @@ class DeviceCSR:
             enc = torch.where(s >= 0, s | torch.tensor(-2 ** 31, dtype=torch.int32, device=dev),
                               self.col_idx)
             self.hub_col, self.hub_ids = enc.contiguous(), idx.to(torch.int32).contiguous()
+
+    def ensure_pr_hubs(self, stream=None) -> None:
+        """Encode the hub SOURCES of the pull fold (pgx_pagerank_pull_hubs_run).
+
+        Hubs are the (at most pgx_pr_hub_capacity) highest out-degree
+        vertices; an in-CSR edge from hub h is stored as (0x80000000 |
+        slot(h)) and its share is read from each CTA's shared-memory table.
+        Needs the transpose; one pass over in_col, once per graph.
+        """
+        if self.pr_hub_col is not None:
+            return
+        self.ensure_transpose(stream)
+        dev = self.row_ptr.device
+        st = torch.cuda.current_stream(dev) if stream is None else stream
+        lib = _lib.load()
+        cap = ctypes.c_int32(0)
+        _lib.check(lib.pgx_pr_hub_capacity(ctypes.byref(cap)), "pgx_pr_hub_capacity")
+        with torch.cuda.device(dev), torch.cuda.stream(st):
+            outdeg = torch.diff(self.row_ptr)
+            h = min(int(cap.value), self.n, int(os.environ.get("PGX_PR_HUBS", cap.value)))
+            vals, idx = torch.topk(outdeg, h, sorted=True)
+            idx = idx[vals >= 2]          # a hub must send >= 2 edges
+            slot = torch.full((self.n,), -1, dtype=torch.int32, device=dev)
+            slot[idx] = torch.arange(idx.numel(), dtype=torch.int32, device=dev)
+            s = slot[self.in_col.long()]
+            enc = torch.where(s >= 0, s | torch.tensor(-2 ** 31, dtype=torch.int32, device=dev),
+                              self.in_col)
+            del s
+            self.pr_hub_col, self.pr_hub_slot = enc.contiguous(), slot
+            self.pr_nhubs = int(idx.numel())
 
     def ensure_transpose(self, stream=None) -> None:
         """Build the in-CSR on the device (sort by (dst, src)), once."""

@@ -14,6 +14,7 @@ shares with red.add.f64 in arrival order, the reference folds them in
 adjacency order.
 """
 
+import ctypes
 import hashlib
 
 import numpy as np
@@ -79,13 +80,17 @@ def pull_threshold():
 # threshold, the apply never builds a frontier after a segmented superstep,
 # so every superstep after one runs segmented too), bu / buall (unit-weight
 # SSSP direction-optimising at the shipped threshold / bottom-up in every
-# superstep after the first), push1 (SSSP push only)
+# superstep after the first), push1 (SSSP push only), prhubs / prhubs3
+# (pull PageRank with the shared-memory hub-source table: every source of
+# out-degree >= 2 a hub / only the top 3)
 @pytest.mark.parametrize("mode", ["pull", "push", "hubs", "k1", "segall", "segskip", "bu",
-                                  "buall", "push1"])
+                                  "buall", "push1", "prhubs", "prhubs3"])
 @pytest.mark.parametrize("r", RUNS, ids=lambda r: r.id)
-def test_golden_reference_runs(r, mode, seg_threshold, pull_threshold):
-    if mode == "push" and r.app != "pagerank":
-        pytest.skip("pagerank_mode only changes the PageRank lowering")
+def test_golden_reference_runs(r, mode, seg_threshold, pull_threshold, monkeypatch):
+    if mode in ("push", "prhubs", "prhubs3") and r.app != "pagerank":
+        pytest.skip("pagerank_mode / pagerank_hubs only change the PageRank lowering")
+    if mode == "prhubs3":
+        monkeypatch.setenv("PGX_PR_HUBS", "3")
     if mode in ("hubs", "k1", "segall", "segskip") and r.app == "pagerank":
         pytest.skip("hub_cache / segments only change the min combiner")
     if mode in ("bu", "buall", "push1") and r.app != "sssp":
@@ -94,6 +99,7 @@ def test_golden_reference_runs(r, mode, seg_threshold, pull_threshold):
     cap = r.kwargs.get("max_supersteps")
     cfg = pgx.EngineConfig(max_supersteps=cap if cap else pgx.DEFAULT_MAX_SUPERSTEPS,
                            pagerank_mode="push" if mode == "push" else "pull",
+                           pagerank_hubs="on" if mode.startswith("prhubs") else "off",
                            hub_cache="on" if mode == "hubs" else "off",
                            segments="off" if mode == "k1" else
                            "on" if mode.startswith("seg") else "auto",
@@ -231,13 +237,14 @@ def test_gpu_rmat_matches_baseline_hashes(graphs, name):
     assert sha(g.out_targets, "<i4") == CSR_HASHES[name][1]
 
 
-@pytest.mark.parametrize("mode", ["pull", "push"])
+@pytest.mark.parametrize("mode", ["pull", "push", "pull-hubs"])
 def test_c1_pagerank_vs_oracle(graphs, mode):
     g = graphs("C1")
     off = g.out_offsets.cpu().numpy()
     tgt = g.out_targets.cpu().numpy()
     want = O.run_pagerank(g.vertex_count, off, tgt)
-    rep = pgx.run(g, pgx.pagerank(), pgx.EngineConfig(pagerank_mode=mode))
+    rep = pgx.run(g, pgx.pagerank(), pgx.EngineConfig(
+        pagerank_mode=mode[:4], pagerank_hubs="on" if mode == "pull-hubs" else "auto"))
     assert rel_err(rep.values, want.values) <= PR_RTOL
     assert rep.superstep_count == 10
     assert [s.messages_sent for s in rep.supersteps] == [40_445] * 9 + [0]
@@ -297,16 +304,34 @@ def test_c3_sssp_directions(graphs, direction, pull_threshold):
         [97364, 1730927, 1490812, 146756, 2024, 6, 0]
 
 
-@pytest.mark.parametrize("mode", ["pull", "push"])
+@pytest.mark.parametrize("mode", ["pull", "push", "pull-nohubs"])
 def test_c4_pagerank_vs_oracle(graphs, mode):
     g = graphs("C4")
-    rep = pgx.run(g, pgx.pagerank(), pgx.EngineConfig(pagerank_mode=mode))
+    rep = pgx.run(g, pgx.pagerank(), pgx.EngineConfig(
+        pagerank_mode=mode[:4], pagerank_hubs="off" if mode == "pull-nohubs" else "auto"))
     off = g.out_offsets.cpu().numpy()
     tgt = g.out_targets.cpu().numpy()
     want = O.run_pagerank(g.vertex_count, off, tgt)
     assert rel_err(rep.values, want.values) <= PR_RTOL
     assert [s.messages_sent for s in rep.supersteps] == [3_751_426] * 9 + [0]
     assert abs(rep.values[0] - 0.0001216244232021811) / 0.0001216244232021811 <= PR_RTOL
+
+
+@pytest.mark.parametrize("name", ["C1", "C4"])
+def test_pagerank_hub_table_bit_identical(graphs, name):
+    """The shared-memory hub-source table changes where a hub's share is
+    read from, not the values or the summation order: ranks are
+    bit-identical with and without it (C4's default takes the table)."""
+    g = graphs(name)
+    on = pgx.run(g, pgx.pagerank(), pgx.EngineConfig(pagerank_hubs="on"))
+    off = pgx.run(g, pgx.pagerank(), pgx.EngineConfig(pagerank_hubs="off"))
+    assert np.array_equal(on.values, off.values)
+    cap = ctypes.c_int32(0)
+    _lib.check(_lib.load().pgx_pr_hub_capacity(ctypes.byref(cap)), "pgx_pr_hub_capacity")
+    csr = g.device_csr(torch.device("cuda", 0))
+    assert csr.pr_nhubs == cap.value
+    enc = csr.pr_hub_col
+    assert int((enc < 0).sum()) > 0
 
 
 def test_load_cache_pinned_and_on_device(tmp_path):

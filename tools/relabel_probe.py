@@ -1,4 +1,5 @@
-"""Experiment: does an in-degree-descending vertex relabelling (hot recipients
+"""usage: relabel_probe.py C2,C3,C4 in|out|sum
+Experiment: does a degree-descending vertex relabelling (hot recipients
 packed into few cache lines) speed up the scatter?  Timing only."""
 import os, sys
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
@@ -8,12 +9,17 @@ from paper_2010_01542_b200.graph import Graph
 from paper_2010_01542_b200.rmat import rmat_graph
 
 
+KEY = sys.argv[2] if len(sys.argv) > 2 else "in"   # in | out | sum
+
+
 def relabel(g):
     n, m = g.vertex_count, g.edge_count
     off = g.out_offsets
     col = g.out_targets.to(torch.int64)
     indeg = torch.bincount(col, minlength=n)
-    order = torch.argsort(-indeg, stable=True)           # new -> old
+    outdeg = torch.diff(off.to(torch.int64))
+    key = {"in": indeg, "out": outdeg, "sum": indeg + outdeg}[KEY]
+    order = torch.argsort(-key, stable=True)             # new -> old
     new_id = torch.empty_like(order)
     new_id[order] = torch.arange(n, device=order.device)  # old -> new
     src = torch.repeat_interleave(torch.arange(n, device=off.device), torch.diff(off))
@@ -36,7 +42,7 @@ def time_run(g, prog, reps=5):
     return float(np.median(ms)), rep
 
 
-for cfg in ("C2", "C3", "C4"):
+for cfg in (sys.argv[1] if len(sys.argv) > 1 else "C2,C3,C4").split(","):
     g = rmat_graph(cfg)
     r, new_id = relabel(g)
     if cfg == "C2":
