@@ -175,4 +175,29 @@ __device__ __forceinline__ void gather_phase(const GatherArgs &a, char *smem) {
 }
 
 
+// A tile-spanning row's fold: tail[t0] + head[t0 + 1] + ... + head[t1], in
+// tile order (deterministic).  The loads are issued kSpanBatch at a time
+// ahead of the ordered adds: a hub row spans many tiles (C4's largest
+// ~70) and one dependent load per tile was the compute phase's critical
+// path.
+#ifndef PGX_SPAN_BATCH
+#define PGX_SPAN_BATCH 16
+#endif
+constexpr int kSpanBatch = PGX_SPAN_BATCH;
+
+__device__ __forceinline__ double span_sum(const double *head, const double *tail, int64_t t0,
+                                           int64_t t1) {
+  double f = tail[t0];
+  int64_t t = t0 + 1;
+  for (; t + kSpanBatch <= t1 + 1; t += kSpanBatch) {
+    double h[kSpanBatch];
+#pragma unroll
+    for (int j = 0; j < kSpanBatch; j++) h[j] = head[t + j];
+#pragma unroll
+    for (int j = 0; j < kSpanBatch; j++) f = __dadd_rn(f, h[j]);
+  }
+  for (; t <= t1; t++) f = __dadd_rn(f, head[t]);
+  return f;
+}
+
 }  // namespace pgx

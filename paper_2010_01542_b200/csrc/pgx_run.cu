@@ -662,8 +662,7 @@ __global__ void __launch_bounds__(kBlock, PGX_MIN_BLOCKS) pagerank_pull_kernel(P
           if (t0 == t1) {
             f = fv[j];
           } else {
-            f = p.ws.tail[t0];
-            for (int64_t t = t0 + 1; t <= t1; t++) f = __dadd_rn(f, p.ws.head[t]);
+            f = span_sum(p.ws.head, p.ws.tail, t0, t1);
           }
         }
         const double r = __dadd_rn(p.base, __dmul_rn(p.damping, __dadd_rn(f, dn)));
@@ -695,6 +694,9 @@ __global__ void __launch_bounds__(kBlock, PGX_MIN_BLOCKS) pagerank_pull_kernel(P
       record_step(p.stats, s, p.n, (s == last) ? 0 : nspread, p.m, nspread, p.n,
                   (s == last) ? 0 : nspread);
       p.stats[PGX_STAT_HDR + (int64_t)s * PGX_STAT_FIELDS + 5] = (int64_t)globaltimer();
+#if PGX_PR_FOLD_STAMP  // timing probe builds: the fold's end in field 6
+      p.stats[PGX_STAT_HDR + (int64_t)s * PGX_STAT_FIELDS + 6] = (int64_t)t_fold;
+#endif
       (void)t_fold;
       if (s == last || cap) {
         p.stats[0] = s + 1;

@@ -217,9 +217,7 @@ __global__ void fold_spanning_kernel(int32_t nspan, const int32_t *rows, const i
                                      double *folded) {
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < nspan; i += gridDim.x * blockDim.x) {
     const int a = t0[i], b = t1[i];
-    double f = tail[a];
-    for (int t = a + 1; t <= b; t++) f = __dadd_rn(f, head[t]);
-    folded[rows[i]] = f;
+    folded[rows[i]] = span_sum(head, tail, a, b);
   }
 }
 
