@@ -78,9 +78,9 @@ class EngineConfig:
     #: pull PageRank: the highest out-degree sources' shares kept in each
     #: CTA's shared memory (pgx_pagerank_pull_hubs_run; bit-identical
     #: results; the in-CSR's hub edges are encoded once per graph): "auto"
-    #: for graphs of >= 2^24 edges (C4 5.76 -> 5.29 ms; on C1 the table's
-    #: staging costs more than it saves: 0.133 -> 0.154 ms), "on" always,
-    #: "off" never
+    #: for graphs that live on the GPU with >= 2^24 edges (C4 5.76 -> 5.29
+    #: ms; on C1 the table's staging costs more than it saves: 0.133 ->
+    #: 0.154 ms), "on" always, "off" never
     pagerank_hubs: str = "auto"
     #: shared-memory combiner for hub recipients (CC / SSSP, ablation arm;
     #: measured slower on B200): "auto" builds
@@ -361,8 +361,11 @@ def plan_run(graph: Graph, program: VertexProgram,
                                   (config.hub_cache == "auto" and csr.runs >= 1))
     if hubs:
         csr.ensure_hubs(stream)
+    # "auto": graphs that live on the GPU (the encoding is graph preparation
+    # amortised over runs, like the segmented index) with >= 2^24 edges
     if pull and csr.m > 0 and (config.pagerank_hubs == "on" or
-                               (config.pagerank_hubs == "auto" and csr.m >= 1 << 24)):
+                               (config.pagerank_hubs == "auto" and csr.m >= 1 << 24
+                                and graph.device.type == "cuda")):
         csr.ensure_pr_hubs(stream)
         hubs = True
     seg = None
