@@ -162,19 +162,10 @@ class DeviceCSR:
         lib = _lib.load()
         cap = ctypes.c_int32(0)
         _lib.check(lib.pgx_pr_hub_capacity(ctypes.byref(cap)), "pgx_pr_hub_capacity")
+        h = min(int(cap.value), int(os.environ.get("PGX_PR_HUBS", cap.value)))
         with torch.cuda.device(dev), torch.cuda.stream(st):
-            outdeg = torch.diff(self.row_ptr)
-            h = min(int(cap.value), self.n, int(os.environ.get("PGX_PR_HUBS", cap.value)))
-            vals, idx = torch.topk(outdeg, h, sorted=True)
-            idx = idx[vals >= 2]          # a hub must send >= 2 edges
-            slot = torch.full((self.n,), -1, dtype=torch.int32, device=dev)
-            slot[idx] = torch.arange(idx.numel(), dtype=torch.int32, device=dev)
-            s = slot[self.in_col.long()]
-            enc = torch.where(s >= 0, s | torch.tensor(-2 ** 31, dtype=torch.int32, device=dev),
-                              self.in_col)
-            del s
-            self.pr_hub_col, self.pr_hub_slot = enc.contiguous(), slot
-            self.pr_nhubs = int(idx.numel())
+            enc, slot, nh = encode_hub_sources(self.row_ptr, self.in_col, h)
+            self.pr_hub_col, self.pr_hub_slot, self.pr_nhubs = enc, slot, nh
 
     def ensure_transpose(self, stream=None) -> None:
         """Build the in-CSR on the device (sort by (dst, src)), once."""
@@ -202,6 +193,24 @@ class DeviceCSR:
             _lib.check(lib.pgx_graph_prepare(n, m, in_row_ptr.data_ptr(), ws.data_ptr(),
                                              ws_bytes, st.cuda_stream), "pgx_graph_prepare")
         self.in_row_ptr, self.in_col, self.in_ws = in_row_ptr, in_col, ws
+
+
+def encode_hub_sources(row_ptr: torch.Tensor, in_col: torch.Tensor, capacity: int):
+    """The pull fold's hub-source encoding (pgx_pagerank_pull_hubs_run):
+    hubs are the (at most ``capacity``) highest out-degree vertices that
+    send >= 2 edges, in descending out-degree order; an in-CSR edge from
+    hub h becomes (0x80000000 | slot(h)).  Returns (encoded in_col, the
+    vertex -> slot map with -1 for non-hubs, the hub count)."""
+    n = int(row_ptr.numel()) - 1
+    dev = in_col.device
+    outdeg = torch.diff(row_ptr.to(torch.int64))
+    vals, idx = torch.topk(outdeg, min(int(capacity), n), sorted=True)
+    idx = idx[vals >= 2]
+    slot = torch.full((n,), -1, dtype=torch.int32, device=dev)
+    slot[idx] = torch.arange(idx.numel(), dtype=torch.int32, device=dev)
+    s = slot[in_col.long()]
+    enc = torch.where(s >= 0, s | torch.tensor(-2 ** 31, dtype=torch.int32, device=dev), in_col)
+    return enc.contiguous(), slot, int(idx.numel())
 
 
 class Graph:
