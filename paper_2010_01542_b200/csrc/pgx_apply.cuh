@@ -55,6 +55,9 @@ __device__ __forceinline__ unsigned long long block_excl_scan_u64(unsigned long 
 #define PGX_APPLY_ITEMS 4
 #endif
 constexpr int kApplyItems = PGX_APPLY_ITEMS;
+#ifndef PGX_APPLY_PREFETCH
+#define PGX_APPLY_PREFETCH 1
+#endif
 constexpr int kListCap = kApplyListBytes / (int)sizeof(int32_t);
 
 // Returns (recipients counted) << 32 | (broadcasts) for this thread.  With
@@ -84,14 +87,30 @@ __device__ unsigned long long apply_min_phase(const int32_t *__restrict__ row_pt
   // groups go to consecutive CTAs, which spreads the dense
   // (low-id) region of a power-law graph over the whole grid
   const int groups = (words + 31) >> 5;
+#if PGX_APPLY_PREFETCH
+  // the next chunk's word is loaded before this chunk is processed: a
+  // quiet chunk then costs a barrier, not a load round trip
+  auto load_word = [&](int gb) -> uint32_t {
+    const int g = gb + (int)(threadIdx.x >> 5) * gridDim.x + blockIdx.x;
+    const int wi = g * 32 + (int)lane_id();
+    return (g < groups && wi < words) ? ws.has[wi] : 0u;
+  };
+  uint32_t next_word = load_word(0);
+#endif
   for (int gb = 0; gb < groups; gb += gridDim.x * kWarps) {  // block-uniform
     const int g = gb + (int)(threadIdx.x >> 5) * gridDim.x + blockIdx.x;
     const int wi = g * 32 + (int)lane_id();
+#if PGX_APPLY_PREFETCH
+    const uint32_t word = next_word;
+    next_word = load_word(gb + gridDim.x * kWarps);
+    if (word) ws.has[wi] = 0u;
+#else
     uint32_t word = 0;
     if (g < groups && wi < words) {
       word = ws.has[wi];
       if (word) ws.has[wi] = 0u;
     }
+#endif
     if (!__syncthreads_or(word != 0)) continue;  // quiet chunk: one barrier
     const int c = __popc(word);
     recips += c;
