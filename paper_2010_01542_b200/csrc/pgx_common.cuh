@@ -61,7 +61,14 @@ constexpr int kSlots = kTile + 2;    // sources per warp tile (+ sentinel)
 constexpr uint32_t kNeutralMin = 0xFFFFFFFFu;
 constexpr int kHubs = 12288;         // hub recipients cached per CTA (48 KB smem)
 constexpr int kInvalidEdge = 0x7FFFFFFF;  // never a vertex id (n < 2^31 - 1)
-constexpr int kApplyListBytes = 12288 * 4;  // apply: vertex-id list segment (fits the scatter windows)
+#ifndef PGX_APPLY_LIST
+#define PGX_APPLY_LIST 24576
+#endif
+// apply: vertex-id list segment, inside the scatter windows (99 KB); 24576
+// entries hold a dense C5 chunk (~15 K recipients) in one segment (C5
+// -0.3 %, C2 -0.5 % vs 12288, profiles/ab_r2_apply_list.log)
+constexpr int kApplyListBytes = PGX_APPLY_LIST * 4;
+static_assert(kApplyListBytes <= kWarps * kSlots * 12, "the list lives in the scatter windows");
 constexpr int kMaxCtas = 4096;
 // pull PageRank: hub sources whose shares each CTA keeps in shared memory.
 // With the fold's per-warp staging (kWarps * kSlots * 8 = 66 KB) a 96 KB
