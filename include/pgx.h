@@ -277,6 +277,26 @@ int pgx_pagerank_pull_run(int32_t n, int64_t m, const int32_t *row_ptr,
                           size_t run_ws_bytes, int64_t *stats,
                           uintptr_t stream);
 
+/* connected_components() from host memory with superstep 0 hidden under the
+ * upload (engine.py:255-316's first superstep: every vertex sends its id).
+ * pgx_cc_prescatter_init clears the run's mailbox / has-bitmask; once the
+ * offsets and the tile map (pgx_graph_prepare) are on the device,
+ * pgx_cc_source_scatter combines the messages of the edges [e_lo, e_hi)
+ * (only those targets need to have landed) -- call it for every chunk as
+ * its copy completes, on one stream; pgx_cc_run_prescattered then runs
+ * the remaining supersteps (K1, shipped options) from the apply of
+ * superstep 0.  Same labels and statistics as pgx_cc_run. */
+int pgx_cc_prescatter_init(int32_t n, int64_t m, int32_t max_supersteps, void *run_ws,
+                           size_t run_ws_bytes, uintptr_t stream);
+int pgx_cc_source_scatter(int32_t n, int64_t m, const int32_t *row_ptr, const int32_t *col_idx,
+                          const void *graph_ws, int64_t e_lo, int64_t e_hi,
+                          int32_t max_supersteps, void *run_ws, size_t run_ws_bytes,
+                          uintptr_t stream);
+int pgx_cc_run_prescattered(int32_t n, int64_t m, const int32_t *row_ptr,
+                            const int32_t *col_idx, const void *graph_ws,
+                            int32_t max_supersteps, uint32_t *labels, void *run_ws,
+                            size_t run_ws_bytes, int64_t *stats, uintptr_t stream);
+
 /* Hub sources of the pull fold (the north star's hybrid path, pull form):
  * in_col_hubs is a copy of in_col in which every edge FROM one of `nhubs`
  * hub sources (the highest out-degree vertices) holds (0x80000000 | slot);

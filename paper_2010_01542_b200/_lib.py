@@ -41,7 +41,8 @@ EXPORTS = (
     "pgx_offsets_to_i32", "pgx_graph_workspace_bytes", "pgx_graph_prepare",
     "pgx_run_workspace_bytes", "pgx_hub_capacity", "pgx_sssp_run", "pgx_cc_run",
     "pgx_pagerank_run", "pgx_pagerank_pull_run", "pgx_pr_hub_capacity",
-    "pgx_pagerank_pull_hubs_run", "pgx_rmat_keys", "pgx_microbench",
+    "pgx_pagerank_pull_hubs_run", "pgx_cc_prescatter_init", "pgx_cc_source_scatter",
+    "pgx_cc_run_prescattered", "pgx_rmat_keys", "pgx_microbench",
     "pgx_slice_init", "pgx_scatter", "pgx_slice_counters_bytes", "pgx_apply_slice",
     "pgx_pr_apply_slice", "pgx_touched_scratch_bytes", "pgx_touched", "pgx_scatter_pairs",
     "pgx_scatter_peer", "pgx_reset_touched", "pgx_peer_alloc", "pgx_peer_open",
@@ -91,6 +92,11 @@ _SIGS = {
     "pgx_pagerank_pull_run": (ctypes.c_int, [_i32, _i64, _p, _p, _p, _p, _i32, _f64, _f64,
                                              _f64, _i32, _p, _p, _sz, _p, _up]),
     "pgx_pr_hub_capacity": (ctypes.c_int, [_p]),
+    "pgx_cc_prescatter_init": (ctypes.c_int, [_i32, _i64, _i32, _p, _sz, _up]),
+    "pgx_cc_source_scatter": (ctypes.c_int, [_i32, _i64, _p, _p, _p, _i64, _i64, _i32, _p, _sz,
+                                             _up]),
+    "pgx_cc_run_prescattered": (ctypes.c_int, [_i32, _i64, _p, _p, _p, _i32, _p, _p, _sz, _p,
+                                               _up]),
     "pgx_pagerank_pull_hubs_run": (ctypes.c_int, [_i32, _i64, _p, _p, _p, _p, _p, _i32, _i32,
                                                   _f64, _f64, _f64, _i32, _p, _p, _sz, _p, _up]),
     "pgx_slice_init": (ctypes.c_int, [ctypes.c_int, _i32, _i32, _p, _p, _p, _f64, _up]),

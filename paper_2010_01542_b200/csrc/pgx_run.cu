@@ -88,7 +88,11 @@ struct MinRunParams {
 // compiled out, so they cost the hot loops no registers -- used for the
 // unit-weight SSSP kernel (C3 -7 %); the CC kernel measured 1 % slower
 // without them (code generation), so it keeps them
-template <int APP, int S, bool BFS = false, bool ARMS = true>
+// PRE = true (CC, K1 only): superstep 0's messages are already in the
+// mailbox / has-bitmask, scattered chunk by chunk while the CSR was being
+// uploaded (pgx_cc_source_scatter); the kernel starts with the apply of
+// superstep 0.  PRE = false compiles to the unchanged kernel.
+template <int APP, int S, bool BFS = false, bool ARMS = true, bool PRE = false>
 __global__ void __launch_bounds__(kBlock, PGX_MIN_BLOCKS) min_run_kernel(MinRunParams p) {
   extern __shared__ __align__(16) char smem[];
   __shared__ unsigned s_red[32];
@@ -116,13 +120,13 @@ __global__ void __launch_bounds__(kBlock, PGX_MIN_BLOCKS) min_run_kernel(MinRunP
   const bool val_lazy = PGX_VAL_LAZY && APP == PGX_APP_CC && S == 0 && p.use_seg;
   for (unsigned v = gtid; v < (unsigned)p.n; v += nthreads) {
     if (!val_lazy) *slot<S>(val, v) = (APP == PGX_APP_CC) ? v : kNeutralMin;
-    if (!BFS) *slot<S>(mailbox, v) = kNeutralMin;  // the bitmap kernel has no mailbox
+    if (!BFS && !PRE) *slot<S>(mailbox, v) = kNeutralMin;  // the bitmap kernel has no mailbox
     // CC (PGX_SV_LAZY): the send buffers are cleared by the streaming
     // stores under the first two segmented supersteps instead (below)
     if (use_sv && !(PGX_SV_LAZY && APP == PGX_APP_CC)) p.ws.sv[0][v] = p.ws.sv[1][v] = kNeutralMin;
   }
   for (unsigned wi = gtid; wi < (unsigned)(p.n / 32 + 2); wi += nthreads) {
-    p.ws.has[wi] = 0u;
+    if (!PRE) p.ws.has[wi] = 0u;
     p.ws.snd[0][wi] = 0u;
     p.ws.snd[1][wi] = 0u;
   }
@@ -226,7 +230,9 @@ __global__ void __launch_bounds__(kBlock, PGX_MIN_BLOCKS) min_run_kernel(MinRunP
           if (nx[wi]) nx[wi] = 0u;
       }
     }
-    if (pull_s) {
+    if (PRE && s == 0) {
+      // superstep 0 was scattered during the upload (pgx_cc_source_scatter)
+    } else if (pull_s) {
       if constexpr (bfs) {
         PullArgs pa;
         pa.in_row_ptr = p.in_row_ptr;
@@ -737,7 +743,7 @@ static int min_run(int app, int32_t n, int64_t m, const int32_t *row_ptr, const 
                    int32_t source, int32_t max_supersteps, uint32_t *val,
                    void *run_ws, size_t run_ws_bytes, int64_t *stats, uintptr_t stream,
                    const PgxSegIndex *seg = nullptr, const int32_t *in_row_ptr = nullptr,
-                   const int32_t *in_col = nullptr) {
+                   const int32_t *in_col = nullptr, bool pre = false) {
   if (nhubs < 0 || nhubs > kHubs || (nhubs > 0 && !hub_ids))
     return fail(PGX_EINVAL, "hub count must be in [0, pgx_hub_capacity()]");
   if (seg) {
@@ -793,6 +799,8 @@ static int min_run(int app, int32_t n, int64_t m, const int32_t *row_ptr, const 
   p.use_pull = app == PGX_APP_SSSP && bfs && in_row_ptr && (m == 0 || in_col) &&
                g_opt[PGX_OPT_PULL_MIN_EDGES] <= 1024;
   p.pull_min_edges = (m * (int64_t)g_opt[PGX_OPT_PULL_MIN_EDGES]) / 1024;
+  if (pre && (app != PGX_APP_CC || p.use_seg || p.interleaved || !shipped))
+    return fail(PGX_EINVAL, "a pre-scattered run is CC on K1 with the shipped options");
   size_t smem = scatter_smem(PGX_OP_MIN_U32, nhubs);
   if (p.use_seg) smem = std::max(smem, seg_smem_bytes(p.seg.seg_log2) + 16);
   int grid = 0;
@@ -802,7 +810,9 @@ static int min_run(int app, int32_t n, int64_t m, const int32_t *row_ptr, const 
           ? (p.interleaved ? min_run_kernel<PGX_APP_SSSP, 1>
                            : bfs ? min_run_kernel<PGX_APP_SSSP, 0, true, false>
                                  : min_run_kernel<PGX_APP_SSSP, 0>)
-          : (p.interleaved ? min_run_kernel<PGX_APP_CC, 1> : min_run_kernel<PGX_APP_CC, 0>);
+          : (p.interleaved ? min_run_kernel<PGX_APP_CC, 1>
+             : pre         ? min_run_kernel<PGX_APP_CC, 0, false, true, true>
+                           : min_run_kernel<PGX_APP_CC, 0>);
   rc = coop_grid(kern, smem, &grid);
   if (rc) return rc;
   PGX_CUDA(cudaLaunchCooperativeKernel((void *)kern, grid, kBlock, args, smem, st));
@@ -844,6 +854,14 @@ int pgx_cc_run_ex(int32_t n, int64_t m, const int32_t *row_ptr, const int32_t *c
                   uintptr_t stream) {
   return min_run(PGX_APP_CC, n, m, row_ptr, col_idx, graph_ws, nullptr, 0, 0, max_supersteps,
                  labels, run_ws, run_ws_bytes, stats, stream, seg);
+}
+
+int pgx_cc_run_prescattered(int32_t n, int64_t m, const int32_t *row_ptr,
+                            const int32_t *col_idx, const void *graph_ws,
+                            int32_t max_supersteps, uint32_t *labels, void *run_ws,
+                            size_t run_ws_bytes, int64_t *stats, uintptr_t stream) {
+  return min_run(PGX_APP_CC, n, m, row_ptr, col_idx, graph_ws, nullptr, 0, 0, max_supersteps,
+                 labels, run_ws, run_ws_bytes, stats, stream, nullptr, nullptr, nullptr, true);
 }
 
 int pgx_cc_run(int32_t n, int64_t m, const int32_t *row_ptr, const int32_t *col_idx,

@@ -99,6 +99,11 @@ class EngineConfig:
     #: (graph preprocessing, amortised like the segmented index), "on"
     #: always, "off" never (push only).  Results and statistics are identical.
     direction: str = "auto"
+    #: connected components of a graph in host memory: superstep 0 (every
+    #: vertex sends its id) is combined chunk by chunk while the targets
+    #: upload (pgx_cc_source_scatter), the run starts at its apply.  "auto"
+    #: on, "off" uploads first.  Results and statistics are identical.
+    overlap_upload: str = "auto"
 
 
 @dataclass(frozen=True)
@@ -186,6 +191,8 @@ def _validate(program: VertexProgram, config: EngineConfig) -> None:
         raise ConfigError(f"bad hub_cache: {config.hub_cache!r}")
     if config.segments not in ("auto", "on", "off"):
         raise ConfigError(f"bad segments: {config.segments!r}")
+    if config.overlap_upload not in ("auto", "off"):
+        raise ConfigError(f"bad overlap_upload: {config.overlap_upload!r}")
     if config.direction not in ("auto", "on", "off"):
         raise ConfigError(f"bad direction: {config.direction!r}")
     if program.comm_mode is CommMode.PUSH and program.combine is None:
@@ -251,6 +258,7 @@ class LaunchPlan:
     hubs: bool = False
     seg: Any = None          # _lib.PgxSegIndex when the segmented scatter is on
     bottom_up: bool = False  # SSSP: direction-optimising (in-CSR bottom-up supersteps)
+    prescattered: bool = False  # CC: superstep 0 combined during the upload (first launch)
 
     def _hub_args(self):
         c = self.csr
@@ -301,6 +309,19 @@ class LaunchPlan:
                                       self.values.data_ptr(), self.ws.data_ptr(),
                                       self.ws_bytes, self.stats.data_ptr(), sp)
             _lib.check(rc, "pgx_sssp_run_dir")
+        elif self.app == "components" and self.prescattered:
+            # the first launch after the upload pipeline (plan_run); a later
+            # launch of the same plan runs superstep 0 itself
+            self.prescattered = False
+            rc = lib.pgx_cc_run_prescattered(c.n, c.m, c.row_ptr.data_ptr(),
+                                             c.col_idx.data_ptr(), c.ws.data_ptr(),
+                                             self.max_steps, self.values.data_ptr(),
+                                             self.ws.data_ptr(), self.ws_bytes,
+                                             self.stats.data_ptr(), sp)
+            if rc == _lib.PGX_EINVAL:  # ablation options set: the plain run
+                self.launch()
+                return
+            _lib.check(rc, "pgx_cc_run_prescattered")
         elif self.app == "components" and self.seg is not None:
             rc = lib.pgx_cc_run_ex(c.n, c.m, c.row_ptr.data_ptr(), c.col_idx.data_ptr(),
                                    c.ws.data_ptr(), ctypes.byref(self.seg), self.max_steps,
@@ -343,10 +364,15 @@ def plan_run(graph: Graph, program: VertexProgram,
                        and config.device is None else
                        (device if device is not None else config.device))
     stream = torch.cuda.current_stream(dev)
-    csr = graph.device_csr(dev, stream)
+    app = low["app"]
+    # CC from host memory: superstep 0 under the upload (_upload_overlapped)
+    overlap = (app == "components" and config.overlap_upload == "auto"
+               and graph.device.type != "cuda" and graph.out_targets.dtype == torch.int32
+               and graph.edge_count > 0 and config.hub_cache == "off"
+               and config.segments != "on" and graph._device.get(dev.index) is None)
+    csr = graph.device_csr(dev, stream, defer_targets=overlap)
     n, m = csr.n, csr.m
     lib = _lib.load()
-    app = low["app"]
     max_steps = int(config.max_supersteps)
     pull = app == "pagerank" and config.pagerank_mode == "pull"
     if app == "pagerank":
@@ -395,8 +421,45 @@ def plan_run(graph: Graph, program: VertexProgram,
                             dtype=torch.int64, device=dev)
         vdt = torch.float64 if app == "pagerank" else torch.int32
         values = torch.empty(n, dtype=vdt, device=dev)
+    if overlap:
+        _upload_overlapped(graph, csr, ws, ws_bytes, max_steps, stream, lib)
     return LaunchPlan(app, csr, values, stats, ws, ws_bytes, max_steps, low, stream, pull, hubs,
-                      seg, bottom_up)
+                      seg, bottom_up, overlap)
+
+
+#: edges per chunk of the CC upload pipeline (256 MB of targets)
+_OVERLAP_CHUNK = 1 << 26
+
+
+def _upload_overlapped(graph, csr, ws, ws_bytes, max_steps, stream, lib) -> None:
+    """Copy the targets of a host graph in chunks on a copy stream and
+    combine each landed chunk's superstep-0 messages (source ids) into the
+    run's mailbox on ``stream`` (pgx_cc_source_scatter): the PCIe copy,
+    the longest part of a run from host memory, hides superstep 0.  The
+    offsets and the tile map are on the device already (device_csr)."""
+    host = graph.out_targets
+    n, m = csr.n, csr.m
+    dev = csr.col_idx.device
+    sp = stream.cuda_stream
+    _lib.check(lib.pgx_cc_prescatter_init(n, m, max_steps, ws.data_ptr(), ws_bytes, sp),
+               "pgx_cc_prescatter_init")
+    copy = torch.cuda.Stream(device=dev)
+    ready = torch.cuda.Event()
+    ready.record(stream)            # offsets, tile map, cleared mailbox first
+    copy.wait_event(ready)
+    for lo in range(0, m, _OVERLAP_CHUNK):
+        hi = min(m, lo + _OVERLAP_CHUNK)
+        with torch.cuda.stream(copy):
+            csr.col_idx[lo:hi].copy_(host[lo:hi], non_blocking=True)
+            landed = torch.cuda.Event()
+            landed.record(copy)
+        stream.wait_event(landed)
+        _lib.check(lib.pgx_cc_source_scatter(n, m, csr.row_ptr.data_ptr(),
+                                             csr.col_idx.data_ptr(), csr.ws.data_ptr(), lo, hi,
+                                             max_steps, ws.data_ptr(), ws_bytes, sp),
+                   "pgx_cc_source_scatter")
+    csr.col_idx.record_stream(copy)
+    csr.h2d_bytes += m * host.element_size()
 
 
 def collect(plan: LaunchPlan, program: VertexProgram, wall: float | None = None) -> RunReport:

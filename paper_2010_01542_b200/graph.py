@@ -306,8 +306,12 @@ class Graph:
     def drop_device_cache(self) -> None:
         self._device.clear()
 
-    def device_csr(self, device=None, stream=None) -> DeviceCSR:
-        """The int32 device CSR + tile map, built once per device."""
+    def device_csr(self, device=None, stream=None, defer_targets: bool = False) -> DeviceCSR:
+        """The int32 device CSR + tile map, built once per device.
+
+        ``defer_targets`` (host graphs with int32 targets): the targets are
+        only allocated on the device; the caller copies them (the CC upload
+        pipeline of engine.plan_run) and counts their bytes."""
         dev = torch.device("cuda", torch.cuda.current_device()) if device is None \
             else torch.device(device)
         key = dev.index
@@ -326,10 +330,13 @@ class Graph:
                 h2d += off.numel() * off.element_size()
                 off = off.to(dev, non_blocking=True)
             tgt = self.out_targets
-            if tgt.device != dev:
-                h2d += tgt.numel() * tgt.element_size()
-                tgt = tgt.to(dev, non_blocking=True)
-            col = tgt if tgt.dtype == torch.int32 else tgt.to(torch.int32)
+            if defer_targets and tgt.device != dev and tgt.dtype == torch.int32:
+                col = torch.empty(m, dtype=torch.int32, device=dev)
+            else:
+                if tgt.device != dev:
+                    h2d += tgt.numel() * tgt.element_size()
+                    tgt = tgt.to(dev, non_blocking=True)
+                col = tgt if tgt.dtype == torch.int32 else tgt.to(torch.int32)
             row_ptr = torch.empty(n + 1, dtype=torch.int32, device=dev)
             _lib.check(lib.pgx_offsets_to_i32(off.to(torch.int64).data_ptr(),
                                               row_ptr.data_ptr(), n + 1,

@@ -134,7 +134,7 @@ def test_program_validation_and_lowering():
     with pytest.raises(pgx.ConfigError):
         pgx.run(g, pgx.sssp(0), pgx.EngineConfig(max_supersteps=0))
     for bad in (dict(segments="yes"), dict(direction="pull"), dict(pagerank_mode="both"),
-                dict(hub_cache="maybe"), dict(pagerank_hubs="yes")):
+                dict(hub_cache="maybe"), dict(pagerank_hubs="yes"), dict(overlap_upload="on")):
         with pytest.raises(pgx.ConfigError):
             pgx.run(g, pgx.sssp(0), pgx.EngineConfig(**bad))
     with pytest.raises(pgx.ConfigError):

@@ -23,6 +23,7 @@ import torch
 
 import paper_2010_01542_b200 as pgx
 from paper_2010_01542_b200 import _lib
+from paper_2010_01542_b200 import engine as engine_mod
 from golden_cases import DANGLING_RANKS, PATH3_RANKS, load_runs
 from oracle import oracle as O
 from paper_2010_01542_b200.rmat import rmat_graph
@@ -84,7 +85,7 @@ def pull_threshold():
 # (pull PageRank with the shared-memory hub-source table: every source of
 # out-degree >= 2 a hub / only the top 3)
 @pytest.mark.parametrize("mode", ["pull", "push", "hubs", "k1", "segall", "segskip", "bu",
-                                  "buall", "push1", "prhubs", "prhubs3"])
+                                  "buall", "push1", "prhubs", "prhubs3", "hostcc"])
 @pytest.mark.parametrize("r", RUNS, ids=lambda r: r.id)
 def test_golden_reference_runs(r, mode, seg_threshold, pull_threshold, monkeypatch):
     if mode in ("push", "prhubs", "prhubs3") and r.app != "pagerank":
@@ -95,7 +96,12 @@ def test_golden_reference_runs(r, mode, seg_threshold, pull_threshold, monkeypat
         pytest.skip("hub_cache / segments only change the min combiner")
     if mode in ("bu", "buall", "push1") and r.app != "sssp":
         pytest.skip("direction only changes unit-weight SSSP")
-    g = pgx.from_edges(r.src, r.dst, r.n, undirected=r.undirected, device="cuda")
+    if mode == "hostcc" and r.app != "components":
+        pytest.skip("the upload pipeline runs connected components")
+    if mode == "hostcc":  # host graph: superstep 0 under the upload, 7-edge chunks
+        monkeypatch.setattr(engine_mod, "_OVERLAP_CHUNK", 7)
+    g = pgx.from_edges(r.src, r.dst, r.n, undirected=r.undirected,
+                       device="cpu" if mode == "hostcc" else "cuda")
     cap = r.kwargs.get("max_supersteps")
     cfg = pgx.EngineConfig(max_supersteps=cap if cap else pgx.DEFAULT_MAX_SUPERSTEPS,
                            pagerank_mode="push" if mode == "push" else "pull",
@@ -332,6 +338,32 @@ def test_pagerank_hub_table_bit_identical(graphs, name):
     assert csr.pr_nhubs == cap.value
     enc = csr.pr_hub_col
     assert int((enc < 0).sum()) > 0
+
+
+@pytest.mark.parametrize("chunk", [1 << 26, 1 << 20, 100_003])
+def test_cc_upload_pipeline_matches(graphs, chunk, monkeypatch):
+    """C2 from pinned host memory with superstep 0 combined while the
+    targets upload (engine._upload_overlapped): labels and every
+    per-superstep statistic equal the plain upload and the device graph."""
+    monkeypatch.setattr(engine_mod, "_OVERLAP_CHUNK", chunk)
+    g = graphs("C2")
+    host = pgx.Graph(g.vertex_count, g.out_offsets.cpu(), g.out_targets.cpu()).pin_memory()
+    ref = pgx.run(g, pgx.connected_components())
+    for cfg in (pgx.EngineConfig(), pgx.EngineConfig(overlap_upload="off")):
+        host.drop_device_cache()
+        plan = pgx.plan_run(host, pgx.connected_components(), cfg)
+        assert plan.prescattered == (cfg.overlap_upload == "auto")
+        plan.launch()
+        rep = pgx.collect(plan, pgx.connected_components())
+        assert np.array_equal(rep.values, ref.values)
+        assert rep.superstep_count == ref.superstep_count
+        for a, b in zip(rep.supersteps, ref.supersteps):
+            assert (a.active_count, a.messages_sent, a.edges, a.senders, a.recipients) == \
+                (b.active_count, b.messages_sent, b.edges, b.senders, b.recipients)
+        # a second launch of the same plan runs superstep 0 itself
+        plan.launch()
+        assert np.array_equal(pgx.collect(plan, pgx.connected_components()).values, ref.values)
+    host.drop_device_cache()
 
 
 def test_load_cache_pinned_and_on_device(tmp_path):
